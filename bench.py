@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- batched 1-D complex fp32 FFT on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): N=4096, batch=65536 per GPU, split
+re/im layout, forward.  A step is one execute of the whole batch.  Inputs
+(2 GiB) and outputs (2 GiB) per GPU are far larger than the 126 MB L2, so no
+flush is needed between steps.  Multi-GPU: the batch shards with no
+communication (weak scaling, per-GPU batch fixed), timed per rank with CUDA
+events and reduced with MAX.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's
+own CPU path (oracle/_ref: compile_pipeline + interpret, fp64) on the host's
+cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched 1-D complex FFT GFLOP/s (5N log2N) and % of HBM roofline at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--layout", choices=["split", "interleaved"], default="split")
+    ap.add_argument("--direction", choices=["forward", "inverse"], default="forward")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON)")
+    return ap.parse_args()
+
+
+def gflop(n: int, batch: int) -> float:
+    return 5.0 * n * math.log2(n) * batch / 1e9
+
+
+def workload(a) -> dict:
+    return {"workload": f"c2c fp32 FFT N={a.n} batch={a.batch}/GPU {a.layout} {a.direction}",
+            "n": a.n, "batch_per_gpu": a.batch, "layout": a.layout, "direction": a.direction,
+            "l2": "inputs+outputs (16N*batch = %.1f GiB/GPU) exceed the 126 MB L2; no flush"
+                  % (16 * a.n * a.batch / 2 ** 30),
+            "parallelism": f"batch-sharded x{a.gpus}, no collective"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sms.append(float(f[0]))
+                maxs.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# ------------------------------------------------------------ CPU legs
+def cpu_reference_rate(a, budget_s: float, threads: int) -> dict:
+    """The reference's own CPU path (compile_pipeline + interpret, fp64,
+    oracle/_ref) batch-parallel over `threads` host cores on a bounded sample
+    of the workload; GFLOP/s of 5N log2N."""
+    import oracle
+    ref = oracle.Ref()
+    alg, radix = "stockham", 4  # the reference's best interpreter config at N=4096
+    lay = a.layout
+    ref.compile(a.n, alg, radix, lay)
+    chunk = max(threads * 4, 8)
+    x = np.stack([ref.seeded_input(a.n, 1 + b) for b in range(chunk)])
+    if lay == "split":
+        x = oracle.relayout_to_split(x)
+    x = x.astype(np.float32).astype(np.float64)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        ref.forward(x, alg, radix, lay, threads=threads)
+        done += chunk
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": gflop(a.n, done) / el, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+            "sample": f"{done} transforms of N={a.n} {lay} (fp32-rounded seeded_input), "
+                      f"compile_pipeline(stockham, radix 4)+interpret fp64, {el:.1f} s wall, "
+                      f"{threads} threads"}
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    import paper_2308_00497_b200 as fg
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n, batch = a.n, a.batch
+    direction = fg.FORWARD if a.direction == "forward" else fg.INVERSE
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=a.layout, batch=batch, device=local,
+                                                 algorithm="stockham"))
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    if a.layout == "split":
+        in0 = torch.rand(batch, n, device=dev, generator=g) * 2 - 1
+        in1 = torch.rand(batch, n, device=dev, generator=g) * 2 - 1
+        out0, out1 = torch.empty_like(in0), torch.empty_like(in1)
+    else:
+        in0 = torch.rand(batch, n, 2, device=dev, generator=g) * 2 - 1
+        in1 = out1 = None
+        out0 = torch.empty_like(in0)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.execute(in0, out0, in1, out1, direction=direction, stream=stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if a.profile:
+        return None
+
+    # ---- timed region: K steps, one event pair per launch on the launching stream
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        t_begin = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_begin.record(stream)
+        for i in range(a.steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    total_ms = t_begin.elapsed_time(t_end)
+    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in zip(starts, ends)]))
+    t = torch.tensor([total_ms, kern_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / a.steps
+    value = gflop(n, batch) * world / (ms_per_step / 1e3)
+
+    # ---- e2e: public API with pinned HOST buffers (H2D + D2H inside every step)
+    e2e = None
+    if a.e2e_steps > 0:
+        h_in0 = in0.cpu().pin_memory()
+        h_out0 = torch.empty_like(h_in0).pin_memory()
+        h_in1 = in1.cpu().pin_memory() if in1 is not None else None
+        h_out1 = torch.empty_like(h_in1).pin_memory() if h_in1 is not None else None
+        plan.execute_host(h_in0, h_out0, h_in1, h_out1, direction=direction)  # warm (staging alloc)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(a.e2e_steps):
+            plan.execute_host(h_in0, h_out0, h_in1, h_out1, direction=direction)
+        el = torch.tensor([(time.perf_counter() - t0) / a.e2e_steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        nbytes = batch * n * 8
+        e2e = {"value": gflop(n, batch) * world / float(el[0]), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "ms_per_step": float(el[0]) * 1e3,
+               "path": "fftgen_execute_host (C ABI), pinned host fp32, chunked H2D/kernel/D2H on 2 streams"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return None
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    alg_bytes = 16.0 * n * batch  # read + write fp32 complex once per transform
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            prof = json.load(f)
+        traffic = prof.get(f"{a.layout}_{n}_{batch}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    cpu = None
+    if world == 1 and not a.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_rate(a, a.cpu_seconds, os.cpu_count() or 1)
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "error": str(e)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: uniform [-1,1) re/im generated on device (torch.rand), resident in HBM",
+        "config": workload(a),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "kernel": f"fft_block_kernel<{n}>", "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel_ms_avg": round(kern_ms, 4)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": a.steps * plan.launches(),
+        "clocks": clk.summary(),
+        "impl": "ours",
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    import oracle
+    if not os.path.exists(oracle.REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfftgen_ref.so not built"}))
+        return None
+    # each step = a bounded sample of the workload (the full 65536-transform
+    # batch would take ~1 min per step on the interpreter)
+    per_step = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
+    for _ in range(a.warmup):
+        cpu_reference_rate(a, per_step / 2, threads)
+    vals, samples = [], []
+    for _ in range(a.steps):
+        r = cpu_reference_rate(a, per_step, threads)
+        vals.append(r["value"])
+        samples.append(r["sample"])
+    v = float(np.mean(vals))
+    line = {
+        "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(gflop(a.n, a.batch) / v * 1e3, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: fp32-rounded seeded_input (verify.cpp:69-78)", "config": workload(a),
+        "impl": "reference",
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                         "sample": samples[-1]},
+        "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference = unmodified fftgen compile_pipeline+interpret (oracle/_ref), batch-parallel "
+                "one transform per thread; ms_per_step extrapolated to the full batch",
+    }
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,144 @@
+/* include/fftgen_b200.h -- the drop-in C ABI of the B200 FFT hot path.
+ *
+ * Replaces the reference's plan -> execute path (arxiv 2308.00497,
+ * /root/reference/proj):
+ *
+ *   reference                                          here
+ *   ---------------------------------------------     -------------------------------
+ *   PipelineConfig            include/fftgen/driver.hpp:26-35   fftgen_config
+ *   compile_pipeline()        include/fftgen/driver.hpp:44-45   fftgen_plan_create()
+ *   CompiledPipeline          include/fftgen/driver.hpp:37-42   fftgen_plan (opaque)
+ *   interpret()               include/fftgen/exec.hpp:26-27     fftgen_execute() (device buffers)
+ *                                                               fftgen_execute_host() (host fp32)
+ *                                                               fftgen_interpret_f64() (ComplexBuffer storage)
+ *   emitted C ABI fft()       src/emit_c.cpp:88                 fftgen_interpret_f64()
+ *   print_pipeline()          include/fftgen/rewrite.hpp:91-92  fftgen_plan_pipeline_text()
+ *   fftgen::Error hierarchy   include/fftgen/error.hpp:16-71    fftgen_status codes
+ *
+ * Extensions the north star requires: a batch count, an inverse direction,
+ * fp32 storage, two complex layouts with caller-owned device pointers and a
+ * CUDA stream.  Plain pointers and integers only; no torch / C++ types.
+ *
+ * Semantics:
+ *   forward  X[j] = sum_k x[k] exp(-2 pi i jk/N)   (unit_root, matrix.cpp:14-35)
+ *   inverse  X[j] = sum_k x[k] exp(+2 pi i jk/N)   unnormalised (FFTW/cuFFT convention)
+ *   interleaved: transform b, element e at ((float2*)in0)[b*dist + e]
+ *   split:       re at in0[b*dist + e], im at in1[b*dist + e]
+ *                (dist = n: planar arrays; the reference ComplexBuffer's
+ *                 [re n | im n] block per transform is in1 = in0 + n, dist = 2n)
+ *   out-of-place (in and out must not overlap); kernels are enqueued on the
+ *   caller's stream; the plan owns its twiddle tables and scratch.
+ *   Plan creation and destruction are thread-safe; a plan may be executed
+ *   concurrently from several host threads on different streams only when
+ *   it needs no scratch (fftgen_plan_scratch_bytes() == 0).
+ */
+#ifndef FFTGEN_B200_H
+#define FFTGEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFTGEN_B200_ABI_VERSION 1
+
+typedef struct fftgen_plan fftgen_plan;
+
+/* Status codes.  fftgen.hpp maps them back onto the reference's exception
+ * classes (error.hpp:16-71): PLAN -> PlanError, DIMENSION -> DimensionError,
+ * FUSE -> FuseError, EXEC/CUDA/NOMEM -> ExecError, INVALID -> DimensionError. */
+typedef enum {
+  FFTGEN_OK = 0,
+  FFTGEN_ERR_PLAN = 1,      /* non-power-of-two n, bad radix, size cap      (PlanError) */
+  FFTGEN_ERR_DIMENSION = 2, /* sizes / dist / batch do not line up          (DimensionError) */
+  FFTGEN_ERR_EXEC = 3,      /* bad layout / direction / pointer at execute  (ExecError) */
+  FFTGEN_ERR_FUSE = 4,      /* radix above the kernel cap 64                (FuseError) */
+  FFTGEN_ERR_INVALID = 5,   /* NULL handle or config                        */
+  FFTGEN_ERR_CUDA = 6,      /* CUDA runtime failure (device, launch)        */
+  FFTGEN_ERR_NOMEM = 7      /* device allocation failed                     */
+} fftgen_status;
+
+enum { FFTGEN_LAYOUT_INTERLEAVED = 0, FFTGEN_LAYOUT_SPLIT = 1 };     /* ComplexLayout, loopir.hpp:187 */
+enum { FFTGEN_ALG_COOLEY_TUKEY = 0, FFTGEN_ALG_STOCKHAM = 1 };       /* Algorithm, driver.hpp:21 */
+enum { FFTGEN_FORWARD = -1, FFTGEN_INVERSE = 1 };
+
+typedef struct {
+  int64_t n;          /* transform size, power of two >= 1                    (PipelineConfig.n) */
+  int32_t algorithm;  /* FFTGEN_ALG_*; selects the reference op list that
+                         introspection reports (default Cooley-Tukey, like
+                         PipelineConfig.algorithm); execution always uses the
+                         self-sorting Stockham passes                         */
+  int32_t radix;      /* power of two >= 2 (PipelineConfig.radix, default 2)   */
+  int32_t layout;     /* FFTGEN_LAYOUT_*                                  (PipelineConfig.layout) */
+  int32_t device;     /* CUDA device ordinal                                   */
+  int64_t batch;      /* transforms per execute, >= 1                          */
+} fftgen_config;
+
+/* Fills the PipelineConfig defaults (driver.hpp:26-35) plus batch=1, device=0. */
+void fftgen_config_init(fftgen_config *cfg);
+
+/* Plan creation (compile_pipeline).  Validates like plan_cooley_tukey /
+ * plan_stockham (formula.cpp:150-197): PlanError for a non-power-of-two n or a
+ * radix that is not a power of two >= 2, FuseError for radix > 64 when n > 64.
+ * Builds the execution passes and uploads the fp64-accurate fp32 twiddle
+ * tables to `device`. */
+fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg);
+fftgen_status fftgen_plan_destroy(fftgen_plan *plan);
+
+/* Execute on device buffers (the hot path).  `dist` is in complex elements
+ * for interleaved and in floats for split; dist >= n.  `stream` is a
+ * cudaStream_t (NULL = legacy default stream). */
+fftgen_status fftgen_execute(const fftgen_plan *plan, int direction,
+                             const void *in0, const void *in1,
+                             void *out0, void *out1, int64_t dist, void *stream);
+
+/* Execute on HOST fp32 buffers with the same addressing as fftgen_execute.
+ * Host->device copies, kernels and device->host copies are pipelined in
+ * chunks over two streams; pinned host memory gives full PCIe bandwidth.
+ * Blocks until the result is in `out`. */
+fftgen_status fftgen_execute_host(const fftgen_plan *plan, int direction,
+                                  const float *in0, const float *in1,
+                                  float *out0, float *out1, int64_t dist);
+
+/* interpret() drop-in on the reference's own storage: `batch` consecutive
+ * ComplexBuffers of 2n doubles each in the plan's layout (interleaved:
+ * (re,im) pairs; split: [re n | im n]).  Values are rounded to fp32 on the
+ * device, transformed in fp32 and widened back.  Also the batched analogue of
+ * the emitted `void fft(const double *in, double *out, long n)`. */
+fftgen_status fftgen_interpret_f64(const fftgen_plan *plan, int direction,
+                                   const double *in, double *out);
+
+const char *fftgen_error_string(fftgen_status status);
+/* Detail message of the most recent failure on the calling thread. */
+const char *fftgen_last_error(void);
+int fftgen_abi_version(void);
+
+/* ---- introspection (parity of plan indices) -------------------------- */
+/* Reference Stockham stage radices in application order (formula.cpp:182-195).
+ * Returns the count; copies at most cap entries. */
+int fftgen_plan_radices(const fftgen_plan *plan, int64_t *radices, int cap);
+/* The reference's fused operator list for (n, algorithm, radix)
+ * (rewrite.cpp:94-184), one op per entry: desc = {kind, p0, p1, p2} with kind
+ * 0 FusedMKIV(m, copies) 1 FusedIKMV(n, copies) 2 FusedPKIV(m, total, k)
+ * 3 TwiddleMul(len) 4 Permute(m, total). */
+int fftgen_plan_num_ops(const fftgen_plan *plan);
+fftgen_status fftgen_plan_op(const fftgen_plan *plan, int idx, int64_t desc[4]);
+/* Source-index map of a data-movement op (y[o] = x[map[o]]), or the w_s
+ * exponent of every coefficient of a TwiddleMul (with *s_out = s). */
+fftgen_status fftgen_plan_op_map(const fftgen_plan *plan, int idx, int64_t *map, int64_t *s_out);
+/* print_pipeline() text of the op list (rewrite.cpp:275-296). */
+fftgen_status fftgen_plan_pipeline_text(const fftgen_plan *plan, char *buf, size_t cap);
+/* The sm_100a execution: passes (radix R, cols, k) and launches. */
+int fftgen_plan_num_passes(const fftgen_plan *plan);
+fftgen_status fftgen_plan_pass(const fftgen_plan *plan, int idx, int64_t desc[4]);
+fftgen_status fftgen_plan_describe(const fftgen_plan *plan, char *buf, size_t cap);
+/* Kernel launches one fftgen_execute issues (for launch accounting). */
+int fftgen_plan_launches(const fftgen_plan *plan);
+size_t fftgen_plan_scratch_bytes(const fftgen_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTGEN_B200_H */

@@ -1,0 +1,58 @@
+// block_instances.cuh -- instantiates the K2 block kernel for every
+// N = 2^0 .. 2^14 at one (LAYOUT, DIR); included by block_<l>_<d>.cu so the
+// four variants compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fft_block.cuh"
+
+namespace fftgen_b200 {
+
+template <int N, int LAYOUT, int DIR>
+cudaError_t block_launch_n(const BlockArgs &a, cudaStream_t s) {
+  using G = BlockGeom<N>;
+  const int64_t grid = (a.batch + G::TPB - 1) / G::TPB;
+  constexpr int smem = SmemGeom<N>::BYTES;
+  if (grid <= 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  fft_block_kernel<N, LAYOUT, DIR><<<(unsigned)grid, G::THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N, int LAYOUT, int DIR>
+cudaError_t block_prepare_n() {
+  constexpr int smem = SmemGeom<N>::BYTES;
+  if (smem <= 48 * 1024) return cudaSuccess;
+  return cudaFuncSetAttribute(fft_block_kernel<N, LAYOUT, DIR>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+#define FFTGEN_BLOCK_SWITCH(FN, LAYOUT, DIR, ...)          \
+  switch (log2n) {                                         \
+  case 0: return FN<1, LAYOUT, DIR>(__VA_ARGS__);          \
+  case 1: return FN<2, LAYOUT, DIR>(__VA_ARGS__);          \
+  case 2: return FN<4, LAYOUT, DIR>(__VA_ARGS__);          \
+  case 3: return FN<8, LAYOUT, DIR>(__VA_ARGS__);          \
+  case 4: return FN<16, LAYOUT, DIR>(__VA_ARGS__);         \
+  case 5: return FN<32, LAYOUT, DIR>(__VA_ARGS__);         \
+  case 6: return FN<64, LAYOUT, DIR>(__VA_ARGS__);         \
+  case 7: return FN<128, LAYOUT, DIR>(__VA_ARGS__);        \
+  case 8: return FN<256, LAYOUT, DIR>(__VA_ARGS__);        \
+  case 9: return FN<512, LAYOUT, DIR>(__VA_ARGS__);        \
+  case 10: return FN<1024, LAYOUT, DIR>(__VA_ARGS__);      \
+  case 11: return FN<2048, LAYOUT, DIR>(__VA_ARGS__);      \
+  case 12: return FN<4096, LAYOUT, DIR>(__VA_ARGS__);      \
+  case 13: return FN<8192, LAYOUT, DIR>(__VA_ARGS__);      \
+  case 14: return FN<16384, LAYOUT, DIR>(__VA_ARGS__);     \
+  default: return cudaErrorInvalidValue;                   \
+  }
+
+#define FFTGEN_BLOCK_INSTANCES(SUFFIX, LAYOUT, DIR)                                      \
+  cudaError_t block_launch_##SUFFIX(int log2n, const BlockArgs &a, cudaStream_t s) {     \
+    FFTGEN_BLOCK_SWITCH(block_launch_n, LAYOUT, DIR, a, s)                               \
+  }                                                                                      \
+  cudaError_t block_prepare_##SUFFIX(int log2n) {                                        \
+    FFTGEN_BLOCK_SWITCH(block_prepare_n, LAYOUT, DIR)                                    \
+  }
+
+}  // namespace fftgen_b200

@@ -1,0 +1,432 @@
+// capi.cpp -- implementation of the C ABI declared in include/fftgen_b200.h.
+//
+// Host C++ only: validation (mirroring the reference's PlanError /
+// DimensionError / ExecError behaviour), plan construction, twiddle upload,
+// launch of the sm_100a kernels, and the chunked host<->device pipeline of
+// the host-buffer entry points.  No CPU fallback exists: without a usable
+// CUDA device every execute fails with FFTGEN_ERR_CUDA.
+#include "fftgen_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace fftgen_b200;
+
+namespace {
+thread_local std::string g_last_error;
+
+fftgen_status fail(fftgen_status st, const std::string &msg) {
+  g_last_error = msg;
+  return st;
+}
+
+fftgen_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(FFTGEN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class F> fftgen_status guarded(F &&f) {
+  try {
+    return f();
+  } catch (const PlanError &e) {
+    return fail(FFTGEN_ERR_PLAN, e.what());
+  } catch (const FuseError &e) {
+    return fail(FFTGEN_ERR_FUSE, e.what());
+  } catch (const DimensionError &e) {
+    return fail(FFTGEN_ERR_DIMENSION, e.what());
+  } catch (const ExecError &e) {
+    return fail(FFTGEN_ERR_EXEC, e.what());
+  } catch (const std::bad_alloc &) {
+    return fail(FFTGEN_ERR_NOMEM, "host allocation failed");
+  } catch (const std::exception &e) {
+    return fail(FFTGEN_ERR_EXEC, e.what());
+  }
+}
+}  // namespace
+
+struct fftgen_plan {
+  fftgen_config cfg{};
+  ExecPlan ex;
+  std::vector<int64_t> radices;
+  std::vector<RefOp> ops;
+  float2 *d_tw = nullptr;
+  // host-buffer pipeline scratch (lazily allocated, guarded by mu)
+  std::mutex mu;
+  void *d_stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t streams[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+fftgen_status validate_exec(const fftgen_plan *p, int direction, const void *in0, const void *in1,
+                            const void *out0, const void *out1, int64_t dist) {
+  if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
+  if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
+    return fail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
+  if (!in0 || !out0) return fail(FFTGEN_ERR_EXEC, "NULL data pointer");
+  if (p->cfg.layout == FFTGEN_LAYOUT_SPLIT && (!in1 || !out1))
+    return fail(FFTGEN_ERR_EXEC, "split layout needs both re (in0/out0) and im (in1/out1) pointers");
+  if (dist < p->cfg.n)
+    return fail(FFTGEN_ERR_DIMENSION, "dist " + std::to_string(dist) + " is smaller than n " +
+                                          std::to_string(p->cfg.n));
+  return FFTGEN_OK;
+}
+
+// Enqueue one execute over `batch` transforms on stream s (device pointers).
+cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const void *in1, void *out0,
+                    void *out1, int64_t dist, int64_t batch, cudaStream_t s) {
+  const int64_t n = p->cfg.n;
+  const int layout = p->cfg.layout;
+  switch (p->ex.strategy) {
+  case STRAT_IDENTITY: {
+    if (layout == FFTGEN_LAYOUT_INTERLEAVED)
+      return strided_copy((const float *)in0, (float *)out0, batch, 2, 2 * dist, 2 * dist, s);
+    cudaError_t e = strided_copy((const float *)in0, (float *)out0, batch, 1, dist, dist, s);
+    if (e != cudaSuccess) return e;
+    return strided_copy((const float *)in1, (float *)out1, batch, 1, dist, dist, s);
+  }
+  case STRAT_BLOCK: {
+    BlockArgs a{};
+    a.in0 = in0;
+    a.in1 = in1;
+    a.out0 = out0;
+    a.out1 = out1;
+    a.idist = dist;
+    a.odist = dist;
+    a.batch = batch;
+    a.tw = p->d_tw;
+    (void)n;
+    return block_launch(p->ex.log2n, layout, direction, a, s);
+  }
+  default:
+    return cudaErrorNotSupported;
+  }
+}
+
+size_t elem_bytes(const fftgen_plan *p) { return 8; }  // fp32 complex, either layout
+
+// Chunked host pipeline: `stage(chunk_first, count, slot_ptr, stream)`.
+template <class F>
+fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &&stage) {
+  const int64_t batch = p->cfg.batch;
+  const int64_t target = int64_t(64) << 20;  // ~64 MiB per chunk and slot
+  int64_t chunk = std::max<int64_t>(1, target / (int64_t)slot_bytes_per_transform);
+  chunk = std::min(chunk, batch);
+  const size_t slot = (size_t)chunk * slot_bytes_per_transform;
+  cudaError_t e;
+  if (p->stage_bytes < 2 * slot) {
+    if (p->d_stage) cudaFree(p->d_stage);
+    p->d_stage = nullptr;
+    p->stage_bytes = 0;
+    if ((e = cudaMalloc(&p->d_stage, 2 * slot)) != cudaSuccess)
+      return fail(FFTGEN_ERR_NOMEM, std::string("staging buffers: ") + cudaGetErrorString(e));
+    p->stage_bytes = 2 * slot;
+  }
+  for (auto &s : p->streams)
+    if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "cudaStreamCreate");
+  int i = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++i) {
+    const int64_t cnt = std::min(chunk, batch - b0);
+    char *slot_ptr = (char *)p->d_stage + (i & 1) * slot;
+    if ((e = stage(b0, cnt, slot_ptr, p->streams[i & 1])) != cudaSuccess) return cuda_fail(e, "host pipeline");
+  }
+  for (auto &s : p->streams)
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  return FFTGEN_OK;
+}
+
+fftgen_status copy_text(const std::string &s, char *buf, size_t cap) {
+  if (!buf || cap == 0) return fail(FFTGEN_ERR_INVALID, "NULL buffer");
+  const size_t k = std::min(cap - 1, s.size());
+  std::memcpy(buf, s.data(), k);
+  buf[k] = 0;
+  return s.size() < cap ? FFTGEN_OK : fail(FFTGEN_ERR_DIMENSION, "buffer too small");
+}
+
+}  // namespace
+
+extern "C" {
+
+void fftgen_config_init(fftgen_config *cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->n = 0;
+  cfg->algorithm = FFTGEN_ALG_COOLEY_TUKEY;  // PipelineConfig defaults (driver.hpp:26-35)
+  cfg->radix = 2;
+  cfg->layout = FFTGEN_LAYOUT_INTERLEAVED;
+  cfg->device = 0;
+  cfg->batch = 1;
+}
+
+int fftgen_abi_version(void) { return FFTGEN_B200_ABI_VERSION; }
+
+const char *fftgen_error_string(fftgen_status s) {
+  switch (s) {
+  case FFTGEN_OK: return "ok";
+  case FFTGEN_ERR_PLAN: return "PlanError";
+  case FFTGEN_ERR_DIMENSION: return "DimensionError";
+  case FFTGEN_ERR_EXEC: return "ExecError";
+  case FFTGEN_ERR_FUSE: return "FuseError";
+  case FFTGEN_ERR_INVALID: return "invalid argument";
+  case FFTGEN_ERR_CUDA: return "CUDA error";
+  case FFTGEN_ERR_NOMEM: return "out of device memory";
+  }
+  return "unknown status";
+}
+
+const char *fftgen_last_error(void) { return g_last_error.c_str(); }
+
+fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
+  if (!out || !cfg) return fail(FFTGEN_ERR_INVALID, "NULL plan pointer or config");
+  *out = nullptr;
+  return guarded([&]() -> fftgen_status {
+    if (cfg->layout != FFTGEN_LAYOUT_INTERLEAVED && cfg->layout != FFTGEN_LAYOUT_SPLIT)
+      throw ExecError("unknown complex layout " + std::to_string(cfg->layout));
+    if (cfg->algorithm != FFTGEN_ALG_COOLEY_TUKEY && cfg->algorithm != FFTGEN_ALG_STOCKHAM)
+      throw PlanError("unknown algorithm " + std::to_string(cfg->algorithm));
+    if (cfg->batch < 1) throw DimensionError("batch must be >= 1, got " + std::to_string(cfg->batch));
+    // same validation order as compile_pipeline -> plan_* -> fuse
+    auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);
+    auto radices = stockham_radices(cfg->n, cfg->radix);
+    ExecPlan ex = build_exec_plan(cfg->n);
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (cfg->device < 0 || cfg->device >= ndev)
+      return fail(FFTGEN_ERR_CUDA, "device " + std::to_string(cfg->device) + " not present (" +
+                                       std::to_string(ndev) + " visible)");
+    DeviceGuard g(cfg->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+
+    auto *p = new fftgen_plan();
+    p->cfg = *cfg;
+    p->ex = std::move(ex);
+    p->ops = std::move(ops);
+    p->radices = std::move(radices);
+    if (p->ex.strategy == STRAT_BLOCK) {
+      if ((e = block_prepare(p->ex.log2n)) != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaFuncSetAttribute");
+      }
+    }
+    const auto &tw = p->ex.tw_block;
+    if (!tw.empty()) {
+      if ((e = cudaMalloc(&p->d_tw, tw.size() * sizeof(float))) != cudaSuccess) {
+        delete p;
+        return fail(FFTGEN_ERR_NOMEM, std::string("twiddle table: ") + cudaGetErrorString(e));
+      }
+      if ((e = cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float), cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+        cudaFree(p->d_tw);
+        delete p;
+        return cuda_fail(e, "twiddle upload");
+      }
+    }
+    *out = p;
+    return FFTGEN_OK;
+  });
+}
+
+fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
+  if (!p) return FFTGEN_OK;
+  {
+    DeviceGuard g(p->cfg.device);
+    if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_stage) cudaFree(p->d_stage);
+    for (auto &s : p->streams)
+      if (s) cudaStreamDestroy(s);
+  }
+  delete p;
+  return FFTGEN_OK;
+}
+
+
+fftgen_status fftgen_execute(const fftgen_plan *p, int direction, const void *in0, const void *in1,
+                             void *out0, void *out1, int64_t dist, void *stream) {
+  fftgen_status st = validate_exec(p, direction, in0, in1, out0, out1, dist);
+  if (st != FFTGEN_OK) return st;
+  DeviceGuard g(p->cfg.device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = enqueue(p, direction, in0, in1, out0, out1, dist, p->cfg.batch, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return FFTGEN_OK;
+}
+
+fftgen_status fftgen_execute_host(const fftgen_plan *cp, int direction, const float *in0, const float *in1,
+                                  float *out0, float *out1, int64_t dist) {
+  fftgen_status st = validate_exec(cp, direction, in0, in1, out0, out1, dist);
+  if (st != FFTGEN_OK) return st;
+  auto *p = const_cast<fftgen_plan *>(cp);
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard g(p->cfg.device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  const int64_t n = p->cfg.n;
+  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+  const size_t per = 2 * (size_t)n * elem_bytes(p);  // device in + out, packed (dist = n)
+  return host_pipeline(p, per, [&](int64_t b0, int64_t cnt, char *slot, cudaStream_t s) {
+    cudaError_t e;
+    float *din = (float *)slot;
+    float *dout = din + 2 * n * cnt;
+    const size_t w = (split ? 1 : 2) * n * sizeof(float), hp = (split ? 1 : 2) * dist * sizeof(float);
+    const float *h0 = in0 + b0 * dist * (split ? 1 : 2);
+    if ((e = cudaMemcpy2DAsync(din, w, h0, hp, w, cnt, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    float *din1 = nullptr, *dout1 = nullptr;
+    if (split) {
+      din1 = din + n * cnt;
+      dout1 = dout + n * cnt;
+      if ((e = cudaMemcpy2DAsync(din1, w, in1 + b0 * dist, hp, w, cnt, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return e;
+    }
+    if ((e = enqueue(p, direction, din, din1, dout, dout1, n, cnt, s)) != cudaSuccess) return e;
+    float *ho0 = out0 + b0 * dist * (split ? 1 : 2);
+    if ((e = cudaMemcpy2DAsync(ho0, hp, dout, w, w, cnt, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if (split && (e = cudaMemcpy2DAsync(out1 + b0 * dist, hp, dout1, w, w, cnt, cudaMemcpyDeviceToHost, s)) !=
+                     cudaSuccess)
+      return e;
+    return cudaSuccess;
+  });
+}
+
+fftgen_status fftgen_interpret_f64(const fftgen_plan *cp, int direction, const double *in, double *out) {
+  if (!cp) return fail(FFTGEN_ERR_INVALID, "NULL plan");
+  if (!in || !out) return fail(FFTGEN_ERR_EXEC, "NULL data pointer");
+  if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
+    return fail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
+  auto *p = const_cast<fftgen_plan *>(cp);
+  std::lock_guard<std::mutex> lk(p->mu);
+  DeviceGuard g(p->cfg.device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  const int64_t n = p->cfg.n;
+  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+  // per transform: 2n doubles in, 2n floats in, 2n floats out, 2n doubles out
+  const size_t per = 2 * (size_t)n * (8 + 4 + 4 + 8);
+  return host_pipeline(p, per, [&](int64_t b0, int64_t cnt, char *slot, cudaStream_t s) {
+    cudaError_t e;
+    const int64_t cntf = 2 * n * cnt;
+    double *d64in = (double *)slot;
+    float *f32in = (float *)(d64in + cntf);
+    float *f32out = f32in + cntf;
+    double *d64out = (double *)(f32out + cntf);
+    if ((e = cudaMemcpyAsync(d64in, in + b0 * 2 * n, cntf * sizeof(double), cudaMemcpyHostToDevice, s)) !=
+        cudaSuccess)
+      return e;
+    if ((e = convert_f64_to_f32(d64in, f32in, cntf, s)) != cudaSuccess) return e;
+    if (split)  // reference ComplexBuffer split storage: [re n | im n] per transform
+      e = enqueue(p, direction, f32in, f32in + n, f32out, f32out + n, 2 * n, cnt, s);
+    else
+      e = enqueue(p, direction, f32in, nullptr, f32out, nullptr, n, cnt, s);
+    if (e != cudaSuccess) return e;
+    if ((e = convert_f32_to_f64(f32out, d64out, cntf, s)) != cudaSuccess) return e;
+    return cudaMemcpyAsync(out + b0 * 2 * n, d64out, cntf * sizeof(double), cudaMemcpyDeviceToHost, s);
+  });
+}
+
+// ---- introspection -------------------------------------------------------
+int fftgen_plan_radices(const fftgen_plan *p, int64_t *radices, int cap) {
+  if (!p) return -1;
+  const int cnt = (int)p->radices.size();
+  for (int i = 0; i < cnt && i < cap && radices; ++i) radices[i] = p->radices[i];
+  return cnt;
+}
+
+int fftgen_plan_num_ops(const fftgen_plan *p) { return p ? (int)p->ops.size() : -1; }
+
+fftgen_status fftgen_plan_op(const fftgen_plan *p, int idx, int64_t desc[4]) {
+  if (!p || !desc) return fail(FFTGEN_ERR_INVALID, "NULL argument");
+  if (idx < 0 || idx >= (int)p->ops.size()) return fail(FFTGEN_ERR_DIMENSION, "op index out of range");
+  const RefOp &op = p->ops[idx];
+  desc[0] = op.kind;
+  desc[1] = op.kind == OP_TWIDDLE ? p->cfg.n : op.p0;
+  desc[2] = op.kind == OP_TWIDDLE ? 0 : op.p1;
+  desc[3] = op.kind == OP_TWIDDLE ? 0 : op.p2;
+  return FFTGEN_OK;
+}
+
+fftgen_status fftgen_plan_op_map(const fftgen_plan *p, int idx, int64_t *map, int64_t *s_out) {
+  if (!p || !map) return fail(FFTGEN_ERR_INVALID, "NULL argument");
+  if (idx < 0 || idx >= (int)p->ops.size()) return fail(FFTGEN_ERR_DIMENSION, "op index out of range");
+  return guarded([&]() -> fftgen_status {
+    op_map(p->ops[idx], p->cfg.n, map, s_out);
+    return FFTGEN_OK;
+  });
+}
+
+
+fftgen_status fftgen_plan_pipeline_text(const fftgen_plan *p, char *buf, size_t cap) {
+  if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
+  return copy_text(pipeline_text(p->ops, p->cfg.n), buf, cap);
+}
+
+int fftgen_plan_num_passes(const fftgen_plan *p) { return p ? (int)p->ex.passes.size() : -1; }
+
+fftgen_status fftgen_plan_pass(const fftgen_plan *p, int idx, int64_t desc[4]) {
+  if (!p || !desc) return fail(FFTGEN_ERR_INVALID, "NULL argument");
+  if (idx < 0 || idx >= (int)p->ex.passes.size()) return fail(FFTGEN_ERR_DIMENSION, "pass index out of range");
+  const PassDesc &d = p->ex.passes[idx];
+  desc[0] = d.R;
+  desc[1] = d.cols;
+  desc[2] = d.k;
+  desc[3] = d.s;
+  return FFTGEN_OK;
+}
+
+int fftgen_plan_launches(const fftgen_plan *p) {
+  if (!p) return -1;
+  switch (p->ex.strategy) {
+  case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
+  case STRAT_BLOCK: return 1;
+  default: return 2;
+  }
+}
+
+size_t fftgen_plan_scratch_bytes(const fftgen_plan *p) { return p ? 0 : 0; }
+
+fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) {
+  if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
+  std::ostringstream o;
+  o << "n=" << p->cfg.n << " batch=" << p->cfg.batch
+    << " layout=" << (p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? "split" : "interleaved")
+    << " device=" << p->cfg.device << "\n";
+  o << "reference stages (radix " << p->cfg.radix << "):";
+  for (auto r : p->radices) o << " " << r;
+  o << "\n";
+  if (p->ex.strategy == STRAT_BLOCK) {
+    int64_t threads, tpb, smem;
+    block_launch_geom(p->ex.log2n, &threads, &tpb, &smem);
+    o << "kernel fft_block_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + tpb - 1) / tpb << "] block["
+      << threads << "] smem=" << smem << "B transforms/CTA=" << tpb << "\n";
+    for (size_t i = 0; i < p->ex.passes.size(); ++i) {
+      const auto &d = p->ex.passes[i];
+      o << "  pass " << i << ": radix " << d.R << " s=" << d.s << " cols=" << d.cols << " k=" << d.k
+        << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
+    }
+  } else if (p->ex.strategy == STRAT_IDENTITY) {
+    o << "identity copy\n";
+  }
+  return copy_text(o.str(), buf, cap);
+}
+
+}  // extern "C"

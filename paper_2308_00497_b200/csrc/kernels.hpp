@@ -1,0 +1,34 @@
+// kernels.hpp -- host-visible launch entry points of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fftgen_b200 {
+
+enum { LAYOUT_INTERLEAVED = 0, LAYOUT_SPLIT = 1 };
+
+// Arguments of the K2 block kernel (fft_block.cuh).
+struct BlockArgs {
+  const void *in0;
+  const void *in1;     // split: imaginary plane
+  void *out0;
+  void *out1;
+  int64_t idist;       // elements between consecutive transforms (input)
+  int64_t odist;
+  int64_t batch;
+  const float2 *tw;    // concatenated [A][m] pass tables, w_s^{A m} (forward)
+};
+
+// K2: one CTA per TPB whole transforms, N = 2^log2n <= 2^14.
+cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
+cudaError_t block_prepare(int log2n);
+void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);
+
+cudaError_t convert_f64_to_f32(const double *in, float *out, int64_t count, cudaStream_t s);
+cudaError_t convert_f32_to_f64(const float *in, double *out, int64_t count, cudaStream_t s);
+cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, int64_t istride,
+                         int64_t ostride, cudaStream_t s);
+
+}  // namespace fftgen_b200

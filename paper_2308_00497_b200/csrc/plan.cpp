@@ -1,0 +1,184 @@
+// plan.cpp -- host plan builder (see plan.hpp).
+#include "plan.hpp"
+
+#include <cmath>
+#include <sstream>
+
+namespace fftgen_b200 {
+
+namespace {
+bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
+int ilog2(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+void check_sizes(int64_t n, int64_t radix) {
+  if (!is_pow2(n))
+    throw PlanError("size must be a power of two, got " + std::to_string(n));
+  if (radix < 2 || !is_pow2(radix))
+    throw PlanError("radix must be a power of two >= 2, got " + std::to_string(radix));
+}
+void check_kernel_cap(int64_t size) {  // FuseOptions::kernel_cap (rewrite.hpp:66)
+  if (size > 64)
+    throw FuseError("DFT kernel of size " + std::to_string(size) +
+                    " exceeds the kernel cap 64; plan it into smaller factors first");
+}
+RefOp mk(int kind, int64_t a, int64_t b = 0, int64_t c = 0) { return RefOp{kind, a, b, c, 0, 0, 0}; }
+RefOp tw(int64_t total, int64_t block, int64_t repeat) {
+  return RefOp{OP_TWIDDLE, 0, 0, 0, total, block, repeat};
+}
+}  // namespace
+
+void unit_root(int64_t n, int64_t t, double *re, double *im) {
+  t %= n;
+  if (t < 0) t += n;
+  if (4 * t % n == 0) {
+    static const double qr[4] = {1.0, 0.0, -1.0, 0.0}, qi[4] = {0.0, -1.0, 0.0, 1.0};
+    *re = qr[4 * t / n];
+    *im = qi[4 * t / n];
+    return;
+  }
+  const double angle = -2.0 * M_PI * static_cast<double>(t) / static_cast<double>(n);
+  *re = std::cos(angle);
+  *im = std::sin(angle);
+}
+
+// plan_stockham's radix sequence in application order (formula.cpp:168-197):
+// r = min(radix, remaining) is pushed from the largest s down, so the
+// remainder radix is applied first.
+std::vector<int64_t> stockham_radices(int64_t n, int64_t radix) {
+  check_sizes(n, radix);
+  std::vector<int64_t> push;
+  for (int64_t remaining = n; remaining > 1;) {
+    const int64_t r = radix < remaining ? radix : remaining;
+    push.push_back(r);
+    remaining /= r;
+  }
+  return std::vector<int64_t>(push.rbegin(), push.rend());
+}
+
+namespace {
+// I_C (x) B = Pi^N_C (B (x) I_C) Pi^N_M  (emit_lifted, rewrite.cpp:60-75)
+void emit_lifted(std::vector<RefOp> &ops, int64_t copies, int64_t b_dim, RefOp lifted) {
+  if (copies == 1) {
+    ops.push_back(lifted);
+    return;
+  }
+  const int64_t n = copies * b_dim;
+  ops.push_back(mk(OP_PERMUTE, b_dim, n));
+  ops.push_back(lifted);
+  ops.push_back(mk(OP_PERMUTE, copies, n));
+}
+
+// Fuser::walk over plan_cooley_tukey(n_sub, radix) under I_copies
+// (formula.cpp:150-166, rewrite.cpp:94-170): factors apply right to left.
+void ct_walk(std::vector<RefOp> &ops, int64_t n_sub, int64_t radix, int64_t copies) {
+  if (n_sub <= radix) {
+    if (n_sub == 1) return;
+    check_kernel_cap(n_sub);
+    ops.push_back(mk(OP_IKMV, n_sub, copies));
+    return;
+  }
+  const int64_t k = radix, m = n_sub / radix;
+  if (copies == 1)
+    ops.push_back(mk(OP_PERMUTE, k, n_sub));
+  else
+    emit_lifted(ops, copies, n_sub, mk(OP_PKIV, k, n_sub, copies));
+  ct_walk(ops, m, radix, copies * k);
+  ops.push_back(tw(n_sub, m, 1));
+  check_kernel_cap(k);
+  emit_lifted(ops, copies, k * m, mk(OP_MKIV, k, m * copies));
+}
+}  // namespace
+
+std::vector<RefOp> fuse_ops(int64_t n, int algorithm, int64_t radix) {
+  check_sizes(n, radix);
+  std::vector<RefOp> ops;
+  if (algorithm == 0) {
+    ct_walk(ops, n, radix, 1);
+    return ops;
+  }
+  if (n == 1) return ops;
+  const auto rs = stockham_radices(n, radix);
+  int64_t s = 1;
+  for (size_t t = 0; t < rs.size(); ++t) {
+    const int64_t r = rs[t];
+    s *= r;
+    const int64_t k = n / s;
+    check_kernel_cap(r);
+    if (t > 0) {
+      // (Pi^s_r (x) I_k) then (D^s_{s/r} (x) I_k)   (formula.cpp:186-190)
+      ops.push_back(k == 1 ? mk(OP_PERMUTE, r, s) : mk(OP_PKIV, r, s, k));
+      ops.push_back(tw(s, s / r, k));
+    }
+    ops.push_back(n / r == 1 ? mk(OP_IKMV, r, 1) : mk(OP_MKIV, r, n / r));
+  }
+  return ops;
+}
+
+std::string pipeline_text(const std::vector<RefOp> &ops, int64_t n) {
+  std::ostringstream out;  // print_pipeline format (rewrite.cpp:275-296)
+  for (const RefOp &op : ops) {
+    switch (op.kind) {
+    case OP_MKIV: out << "FusedMKIV(m=" << op.p0 << ", copies=" << op.p1 << ")\n"; break;
+    case OP_IKMV: out << "FusedIKMV(n=" << op.p0 << ", copies=" << op.p1 << ")\n"; break;
+    case OP_PKIV:
+      out << "FusedPKIV(m=" << op.p0 << ", total=" << op.p1 << ", k=" << op.p2 << ")\n";
+      break;
+    case OP_TWIDDLE: out << "TwiddleMul(len=" << n << ")\n"; break;
+    default: out << "Permute(m=" << op.p0 << ", total=" << op.p1 << ")\n"; break;
+    }
+  }
+  return out.str();
+}
+
+void op_map(const RefOp &op, int64_t n, int64_t *map, int64_t *s_out) {
+  if (s_out) *s_out = 0;
+  if (op.kind == OP_PKIV) {  // y[k(i cols + j) + c] = x[k(j p + i) + c]  (rewrite.cpp:217-226)
+    const int64_t p = op.p0, cols = op.p1 / op.p0, k = op.p2;
+    for (int64_t i = 0; i < p; ++i)
+      for (int64_t j = 0; j < cols; ++j)
+        for (int64_t c = 0; c < k; ++c) map[k * (i * cols + j) + c] = k * (j * p + i) + c;
+  } else if (op.kind == OP_PERMUTE) {  // y[i cols + j] = x[j p + i]  (rewrite.cpp:232-239)
+    const int64_t p = op.p0, cols = op.p1 / op.p0;
+    for (int64_t i = 0; i < p; ++i)
+      for (int64_t j = 0; j < cols; ++j) map[i * cols + j] = j * p + i;
+  } else if (op.kind == OP_TWIDDLE) {
+    const int64_t period = op.tw_total * op.tw_repeat;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t b = (i % period) / op.tw_repeat;
+      map[i] = ((b / op.tw_block) * (b % op.tw_block)) % op.tw_total;
+    }
+    if (s_out) *s_out = op.tw_total;
+  } else {
+    throw DimensionError("op is a butterfly, not a data-movement or twiddle op");
+  }
+}
+
+ExecPlan build_exec_plan(int64_t n) {
+  if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
+  ExecPlan p;
+  p.n = n;
+  p.log2n = ilog2(n);
+  if (n == 1) {
+    p.strategy = STRAT_IDENTITY;
+    return p;
+  }
+  if (p.log2n <= 14) {
+    p.strategy = STRAT_BLOCK;
+    const int np = block_num_passes(p.log2n);
+    for (int q = 0; q < np; ++q) {
+      PassDesc d{};
+      block_pass(p.log2n, q, &d.R, &d.cols, &d.k);
+      d.s = d.R * d.cols;
+      p.passes.push_back(d);
+    }
+    p.tw_block = block_twiddles(p.log2n);
+    return p;
+  }
+  throw PlanError("size 2^" + std::to_string(p.log2n) +
+                  " exceeds the single-CTA path (2^14); four-step not built in this build");
+}
+
+}  // namespace fftgen_b200

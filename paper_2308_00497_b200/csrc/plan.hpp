@@ -1,0 +1,77 @@
+// plan.hpp -- host-side plan builder (C++), the B200 replacement for the
+// reference's compile_pipeline (proj/src/driver.cpp:11-34).
+//
+// It restates, for introspection and index parity, the reference planners
+// and sparse fusion (formula.cpp:150-197, rewrite.cpp:46-184) as a compact
+// operator list, and derives from N the sm_100a execution: either one
+// shared-memory-resident kernel (K2, N <= 2^14) or a four-step of two such
+// kernels (K3, 2^15 <= N <= 2^28).  Twiddles are generated in fp64 with the
+// reference's unit_root formula (matrix.cpp:14-35) and rounded to fp32 once,
+// at plan time.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fftgen_b200 {
+
+// Mirrors of the reference's error classes (error.hpp:16-71); the C ABI maps
+// them to fftgen_status codes and fftgen.hpp maps the codes back.
+struct PlanError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DimensionError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct FuseError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ExecError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+enum OpKind { OP_MKIV = 0, OP_IKMV = 1, OP_PKIV = 2, OP_TWIDDLE = 3, OP_PERMUTE = 4 };
+
+// One fused operator in the reference's application order (rewrite.hpp:24-52).
+// TwiddleMul coefficients are described, not stored: coefficient i is
+// unit_root(tw_total, kk*mm) with b = (i mod tw_total*tw_repeat) / tw_repeat,
+// kk = b / tw_block, mm = b mod tw_block.
+struct RefOp {
+  int kind;
+  int64_t p0, p1, p2;
+  int64_t tw_total, tw_block, tw_repeat;
+};
+
+// exp(-2 pi i t / n) in fp64, exact at quadrant multiples (matrix.cpp:14-35).
+void unit_root(int64_t n, int64_t t, double *re, double *im);
+
+std::vector<int64_t> stockham_radices(int64_t n, int64_t radix);
+std::vector<RefOp> fuse_ops(int64_t n, int algorithm, int64_t radix);
+std::string pipeline_text(const std::vector<RefOp> &ops, int64_t n);
+void op_map(const RefOp &op, int64_t n, int64_t *map, int64_t *s_out);
+
+// One execution pass: a radix-R Stockham stage over the whole transform.
+struct PassDesc {
+  int64_t R, cols, k, s;
+};
+
+enum Strategy { STRAT_IDENTITY = 0, STRAT_BLOCK = 1, STRAT_FOURSTEP = 2 };
+
+struct ExecPlan {
+  int64_t n = 0;
+  Strategy strategy = STRAT_BLOCK;
+  int log2n = 0;
+  // four-step: N = n1 * n2, column FFTs of size n1 (stride n2) then row FFTs
+  // of size n2 with the w_N^{e q} pre-twiddle and an n1-strided store.
+  int64_t n1 = 0, n2 = 0;
+  std::vector<PassDesc> passes;
+  // host copies of the fp32 twiddle tables (uploaded by the C ABI)
+  std::vector<float> tw_block;      // K2 pass tables of the single kernel / of n2
+  std::vector<float> tw_block_n1;   // K2 pass tables of the n1 column kernel
+  std::vector<float> tw_lo, tw_hi;  // four-step w_N^e = hi[e >> b] * lo[e & (2^b - 1)]
+  int tw_lo_bits = 0;
+};
+
+ExecPlan build_exec_plan(int64_t n);
+
+// K2 pass structure of an N-point block kernel (defined in kernels_common.cu
+// from the compile-time BlockPlan), and its [A][m] twiddle table in floats.
+int block_num_passes(int log2n);
+void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k);
+std::vector<float> block_twiddles(int log2n);
+
+}  // namespace fftgen_b200

@@ -1,0 +1,179 @@
+"""CPU: the product's host plan builder and C ABI surface (no GPU needed).
+
+* the library loads and exports every symbol include/fftgen_b200.h declares,
+* plan introspection (radices, fused op list, index maps, twiddle exponents,
+  print_pipeline text) is bit-exact against the reference's goldens,
+* the compile-time butterfly constants equal unit_root rounded to fp32,
+* the pass regrouping the kernels execute is restated in numpy and matches
+  the oracle,
+* the error behaviour at plan creation mirrors the reference's exceptions.
+Plan creation needs a CUDA device, so these tests exercise the host builder
+through a C++ test driver linked to the same objects (tests/cpp/).
+"""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "fftgen_b200.h")
+LIB = os.path.join(ROOT, "paper_2308_00497_b200", "lib", "libfftgen_b200.so")
+CSRC = os.path.join(ROOT, "paper_2308_00497_b200", "csrc")
+PLAN_TOOL = os.path.join(ROOT, "paper_2308_00497_b200", "build", "plan_tool")
+
+
+def declared_symbols():
+    text = open(HDR).read()
+    return sorted(set(re.findall(
+        r"^(?:fftgen_status|int|void|size_t|const char \*)\s*\*?(fftgen_[a-z0-9_]+)\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    import paper_2308_00497_b200 as fg
+    assert set(fg.ABI_SYMBOLS) == set(syms)
+    assert lib.fftgen_abi_version() == 1
+
+
+def test_error_strings_and_config_defaults():
+    import paper_2308_00497_b200 as fg
+    lib = fg.lib
+    assert lib.fftgen_error_string(1) == b"PlanError"
+    assert lib.fftgen_error_string(2) == b"DimensionError"
+    assert lib.fftgen_error_string(3) == b"ExecError"
+    c = fg._Config()
+    lib.fftgen_config_init(ctypes.byref(c))
+    # PipelineConfig defaults (driver.hpp:26-35): Cooley-Tukey, radix 2, interleaved
+    assert (c.algorithm, c.radix, c.layout, c.batch, c.device) == (0, 2, 0, 1, 0)
+
+
+@pytest.fixture(scope="module")
+def plan_tool():
+    """C++ driver over the host plan builder (plan.cpp), no CUDA device needed."""
+    src = os.path.join(ROOT, "tests", "cpp", "plan_tool.cpp")
+    if (not os.path.exists(PLAN_TOOL)) or os.path.getmtime(PLAN_TOOL) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(CSRC, "plan.cpp"))):
+        os.makedirs(os.path.dirname(PLAN_TOOL), exist_ok=True)
+        subprocess.run(["g++", "-std=c++17", "-O1", "-I", CSRC, "-o", PLAN_TOOL, src,
+                        os.path.join(CSRC, "plan.cpp"), os.path.join(CSRC, "geom.cpp")], check=True)
+    def run(*args):
+        p = subprocess.run([PLAN_TOOL, *map(str, args)], capture_output=True, text=True)
+        return p.returncode, p.stdout, p.stderr
+    return run
+
+
+def test_pipeline_text_matches_reference_goldens(plan_tool, golden_meta):
+    for key, text in golden_meta["pipelines"].items():
+        alg, n, radix = key.rsplit("_", 2)
+        rc, out, err = plan_tool("text", n, 0 if alg == "cooley-tukey" else 1, radix)
+        assert rc == 0, err
+        assert out == text, key
+
+
+def test_index_maps_bit_exact_vs_reference(plan_tool, golden, golden_meta):
+    checked = 0
+    for key in golden_meta["num_ops"]:
+        alg, n, radix = key.rsplit("_", 2)
+        a = 0 if alg == "cooley-tukey" else 1
+        rc, out, err = plan_tool("maps", n, a, radix)
+        assert rc == 0, err
+        for line in out.splitlines():
+            idx, kind, s, *vals = line.split()
+            vals = np.array([int(v) for v in vals])
+            if kind in ("2", "4"):
+                assert np.array_equal(vals, golden[f"map_{key}_{idx}"]), (key, idx)
+                checked += 1
+            elif kind == "3":
+                exps, ss = golden[f"tw_{key}_{idx}"]
+                assert int(s) == ss[0] and np.array_equal(vals, exps), (key, idx)
+                checked += 1
+    assert checked > 200
+
+
+def test_radices_reference_order(plan_tool):
+    for n, r, want in ((1024, 8, [2, 8, 8, 8]), (32, 4, [2, 4, 4]), (4096, 4, [4] * 6),
+                       (2048, 8, [4, 8, 8, 8]), (1, 2, [])):
+        rc, out, _ = plan_tool("radices", n, r)
+        assert rc == 0
+        assert [int(v) for v in out.split()] == want
+
+
+def test_plan_errors(plan_tool):
+    # formula.cpp:150-160 / rewrite.cpp:56-62 behaviour: PlanError / FuseError
+    assert plan_tool("text", 12, 1, 4)[0] == 1
+    assert plan_tool("text", 16, 1, 3)[0] == 1
+    assert plan_tool("text", 16, 1, 1)[0] == 1
+    assert plan_tool("text", 256, 1, 128)[0] == 4
+    assert plan_tool("text", 64, 1, 128)[0] == 0   # r = min(radix, n) = 64 fits the cap
+
+
+def test_exec_plan_passes_cover_all_sizes(plan_tool):
+    for l2 in range(0, 15):
+        rc, out, err = plan_tool("passes", 1 << l2)
+        assert rc == 0, err
+        passes = [tuple(int(v) for v in ln.split()) for ln in out.splitlines()]
+        prod = 1
+        for R, cols, k, s in passes:
+            assert cols == prod and s == R * cols and k * s == (1 << l2)
+            prod *= R
+        assert prod == 1 << l2
+
+
+def test_butterfly_constants_are_unit_root_fp32(orc):
+    text = open(os.path.join(CSRC, "roots64.cuh")).read()
+    def arr(name):
+        body = text.split(name + "[64] = {")[1].split("}")[0]
+        return [float.fromhex(v.strip().rstrip("f")) if "0x" in v else float(v.strip().rstrip("f"))
+                for v in body.split(",")]
+    re_, im_ = arr("kRoot64Re"), arr("kRoot64Im")
+    for j in range(64):
+        w = orc.unit_root(64, j)
+        assert np.float32(w.real) == np.float32(re_[j]) and np.float32(w.imag) == np.float32(im_[j]), j
+
+
+def _pass(x, R, cols, n, sign=-1):
+    s = cols * R
+    k = n // s
+    y = np.empty_like(x)
+    A = np.arange(R)
+    for m in range(cols):
+        for c in range(k):
+            v = x[(m * R + A) * k + c] * np.exp(sign * 2j * np.pi * A * m / s)
+            V = np.fft.fft(v) if sign < 0 else np.fft.ifft(v) * R
+            y[(A * cols + m) * k + c] = V
+    return y
+
+
+def test_pass_regrouping_restated_matches_oracle(plan_tool, orc):
+    """The kernels' pass formula (fft_block.cuh header) restated in numpy."""
+    for n in (16, 128, 1024, 2048, 8192):
+        rc, out, _ = plan_tool("passes", n)
+        passes = [tuple(int(v) for v in ln.split()) for ln in out.splitlines()]
+        x = orc.seeded_input(n, 2)
+        z = oracle.as_complex(x)
+        for R, cols, k, s in passes:
+            z = _pass(z, R, cols, n)
+        want = oracle.as_complex(orc.forward(x, "stockham", 2))
+        assert np.abs(z - want).max() / np.abs(want).max() < 1e-12, n
+
+
+def test_block_twiddle_tables_bit_exact(plan_tool, orc):
+    # fp32 tables = unit_root(s, A*m) rounded once (formula.cpp:199-206 values)
+    rc, out, _ = plan_tool("twiddles", 4096)
+    vals = np.array([float.fromhex(v) for v in out.split()], dtype=np.float64)
+    assert vals.size == 2 * 64 * 64
+    want = []
+    for A in range(64):
+        for m in range(64):
+            w = orc.unit_root(4096, A * m)
+            want += [w.real, w.imag]
+    assert np.array_equal(vals.astype(np.float32), np.array(want).astype(np.float32))
