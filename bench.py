@@ -37,8 +37,8 @@ METRIC = "batched 1-D complex FFT GFLOP/s (5N log2N) and % of HBM roofline at 1/
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--batch", type=int, default=65536)
@@ -65,58 +65,58 @@ def workload(a) -> dict:
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region via NVML
+    (B200_PROFILING.md clocks line); polls every 2 ms on a thread."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, dev: int):
         self.dev = dev
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._poll()  # one sample before the region starts
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # reported, not hidden
+            self.nv = None
+            self.err = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        reasons = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, self.max_sm, reasons))
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._poll()
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if getattr(self, "t", None):
+            self.t.join(timeout=1)
 
     def summary(self) -> dict:
-        sms, maxs, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sms.append(float(f[0]))
-                maxs.append(float(f[1]))
-            except ValueError:
-                continue
-            for name, v in zip(names, f[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        if not sms:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
-                "samples": len(sms)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "error": getattr(self, "err", "no samples")}
+        sms = [s[0] for s in self.samples]
+        reasons = sorted({name for _, _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": float(self.samples[0][1]),
+                "reasons": reasons, "samples": len(sms), "source": "nvml"}
 
 
 # ------------------------------------------------------------ CPU legs
@@ -272,7 +272,7 @@ def run_ours(a):
         "config": workload(a),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": f"fft_block_kernel<{n}>", "peak_source": peak_src,
+                     "kernel": plan.describe().splitlines()[2].split()[1], "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "kernel_ms_avg": round(kern_ms, 4)},
         "cpu_baseline": cpu,

@@ -1,4 +1,4 @@
-// block_geom.hpp -- compile-time geometry of the K2 block kernel, shared by
+// block_geom.hpp -- compile-time geometry of the K2 block kernels, shared by
 // the CUDA kernels (fft_block.cuh) and the host plan builder (geom.cpp).
 // Pure constexpr C++17; compiles with g++ and nvcc alike.
 #pragma once
@@ -14,7 +14,9 @@
 namespace fftgen_b200 {
 
 // -------------------------------------------------------------------------
-// Pass plans: radices per pass for each N handled by one CTA.
+// Pass plans: radices per pass for each N handled by one CTA.  Any grouping
+// of the reference's radix-2 Stockham stage list is a valid regrouping; the
+// register radix is capped at 64 (128 registers of float2 data per thread).
 template <int NP, int R0, int R1, int R2> struct PlanT {
   static constexpr int P = NP;
   FFTGEN_HD static constexpr int r(int p) { return p == 0 ? R0 : (p == 1 ? R1 : R2); }
@@ -36,16 +38,17 @@ template <> struct BlockPlan<4096> : PlanT<2, 64, 64, 1> {};
 template <> struct BlockPlan<8192> : PlanT<3, 32, 16, 16> {};
 template <> struct BlockPlan<16384> : PlanT<3, 32, 32, 16> {};
 
-template <int N> struct BlockGeom {
+// TP = transforms per CTA.  0 -> the direct kernel's default (128 threads).
+template <int N, int TP_ = 0> struct BlockGeom {
   using PL = BlockPlan<N>;
   static constexpr int P = PL::P;
   static constexpr int RMAX = PL::r(0) > PL::r(1) ? (PL::r(0) > PL::r(2) ? PL::r(0) : PL::r(2))
                                                   : (PL::r(1) > PL::r(2) ? PL::r(1) : PL::r(2));
-  static constexpr int T = N / RMAX;                           // threads per transform
-  static constexpr int TPB = T >= 128 ? 1 : 128 / T;           // transforms per CTA
+  static constexpr int T = N / RMAX;  // threads per transform
+  static constexpr int TPB = TP_ ? TP_ : (T >= 128 ? 1 : 128 / T);
   static constexpr int THREADS = T * TPB;
   FFTGEN_HD static constexpr int R(int p) { return PL::r(p); }
-  FFTGEN_HD static constexpr int S(int p) {          // cumulative size after pass p
+  FFTGEN_HD static constexpr int S(int p) {  // cumulative size after pass p
     int s = 1;
     for (int q = 0; q <= p; ++q) s *= PL::r(q);
     return s;
@@ -62,9 +65,12 @@ template <int N> struct BlockGeom {
 };
 
 // -------------------------------------------------------------------------
-// Shared-memory padding: padded(i) = i + K * (i / PP).  Chosen per pass
-// boundary at compile time by simulating warp 0's writer (pass p) and reader
-// (pass p+1) addresses and minimising the worst bank-conflict degree.
+// Shared-memory exchange buffers hold float2 (re, im) elements, accessed with
+// 64-bit LDS/STS: a warp access is served as two half-warp wavefronts, each
+// conflict-free when its 16 lanes hit 16 distinct 8-byte bank pairs.
+// padded(i) = i + K * (i / PP) is chosen per pass boundary at compile time by
+// simulating warp 0's writer (pass p) and reader (pass p+1) addresses and
+// minimising the wavefront count (ideal: 2 per access).
 struct Pad {
   int PP;
   int K;
@@ -73,10 +79,8 @@ FFTGEN_HD constexpr int padded(int i, Pad pd) { return pd.K ? i + pd.K * (i / pd
 
 template <int N> struct PadSearch {
   using G = BlockGeom<N>;
-  // worst conflict over the writer of pass p and the reader of pass p+1.
-  // Lanes of one access touch distinct elements, so the degree is the
-  // largest per-bank count.  Representative registers x and butterflies j
-  // suffice: the patterns are affine in both.
+  // Representative registers x and butterflies j suffice: the access
+  // patterns are affine in both.
   static constexpr int cost(int p, Pad pd) {
     const int T = G::T;
     int worst = 0;
@@ -88,24 +92,30 @@ template <int N> struct PadSearch {
       for (int jj = 0; jj < 2; ++jj)
         for (int xx = 0; xx < 4; ++xx) {
           const int j = js[jj], x = xs[xx];
-          int cnt[32] = {};
-          for (int l = 0; l < 32; ++l) {
-            const int t = l % T, f = l / T;  // T < 32: other transforms
-            const int u = t + j * T, m = u / k, c = u % k;
-            const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
-            const int b = (padded(idx, pd) + f * (padded(N - 1, pd) + 1)) & 31;
-            cnt[b]++;
-            worst = cnt[b] > worst ? cnt[b] : worst;
+          int wavefronts = 0;
+          for (int half = 0; half < 2; ++half) {
+            int cnt[16] = {};
+            int deg = 0;
+            for (int l = 16 * half; l < 16 * half + 16; ++l) {
+              const int t = l % T, f = l / T;  // T < 32: other transforms
+              const int u = t + j * T, m = u / k, c = u % k;
+              const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
+              const int b = (padded(idx, pd) + f * (padded(N - 1, pd) + 1)) & 15;
+              cnt[b]++;
+              deg = cnt[b] > deg ? cnt[b] : deg;
+            }
+            wavefronts += deg;
           }
+          worst = wavefronts > worst ? wavefronts : worst;
         }
     }
     return worst;
   }
   static constexpr Pad best(int p) {
-    Pad bestp{32, 0};
+    Pad bestp{16, 0};
     int bc = 1 << 30, bo = 1 << 30;
-    for (int PP = 32; PP <= N; PP *= 2)
-      for (int K = 0; K <= 32; K = K ? K * 2 : 1) {
+    for (int PP = 16; PP <= N; PP *= 2)
+      for (int K = 0; K <= 16; K = K ? K * 2 : 1) {
         const Pad pd{PP, K};
         const int c = cost(p, pd);
         const int o = K * (N / PP);
@@ -120,19 +130,38 @@ template <int N> struct PadSearch {
 };
 
 template <int N, int p> struct BoundaryPad {
-  static constexpr Pad value = BlockGeom<N>::P > 1 ? PadSearch<N>::best(p) : Pad{32, 0};
+  static constexpr Pad value = BlockGeom<N>::P > 1 ? PadSearch<N>::best(p) : Pad{16, 0};
   static constexpr int region = padded(N - 1, value) + 1;
+  static constexpr int wavefronts = BlockGeom<N>::P > 1 ? PadSearch<N>::cost(p, value) : 0;
 };
 
 template <int N> struct SmemGeom {
   using G = BlockGeom<N>;
   static constexpr int r0 = BoundaryPad<N, 0>::region;
   static constexpr int r1 = G::P > 2 ? BoundaryPad<N, 1>::region : 0;
-  static constexpr int REGION = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;  // floats per re/im plane
-  static constexpr int BYTES = G::TPB * REGION * 2 * 4;
+  static constexpr int REGION = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;  // float2 per transform
+  static constexpr int BYTES = G::TPB * REGION * 8;
 };
 
 // -------------------------------------------------------------------------
-
+// TMA-pipelined persistent variant: each CTA loops over groups of TP
+// transforms; the raw input of group i+1 is fetched by cp.async.bulk into one
+// of STAGES stage buffers while group i is computed.  After pass 0 has read a
+// stage's raw data, the same stage buffer holds the padded exchange.
+template <int N> struct TmaGeom {
+  static constexpr bool ENABLED = N >= 256 && N <= 8192;
+  static constexpr int T = BlockGeom<N>::T;
+  static constexpr int tp_threads = T >= 128 ? 1 : 128 / T;
+  static constexpr int tp_bytes = (32768 / (8 * N)) > 0 ? 32768 / (8 * N) : 1;
+  static constexpr int TP = tp_threads < tp_bytes ? tp_threads : tp_bytes;
+  using G = BlockGeom<N, TP>;
+  static constexpr int THREADS = G::THREADS;
+  static constexpr int STAGES = 2;
+  static constexpr int RAW = 8 * N;                                   // bytes per transform
+  static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes
+  static constexpr int SLOT = ((RAW > XCH ? RAW : XCH) + 127) / 128 * 128;
+  static constexpr int STAGE_BYTES = TP * SLOT;
+  static constexpr int BYTES = STAGES * STAGE_BYTES + 128;            // + mbarriers
+};
 
 }  // namespace fftgen_b200

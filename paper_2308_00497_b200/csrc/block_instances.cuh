@@ -1,4 +1,4 @@
-// block_instances.cuh -- instantiates the K2 block kernel for every
+// block_instances.cuh -- instantiates the K2 block kernels for every
 // N = 2^0 .. 2^14 at one (LAYOUT, DIR); included by block_<l>_<d>.cu so the
 // four variants compile in parallel.
 #pragma once
@@ -20,11 +20,33 @@ cudaError_t block_launch_n(const BlockArgs &a, cudaStream_t s) {
 }
 
 template <int N, int LAYOUT, int DIR>
-cudaError_t block_prepare_n() {
+cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
   constexpr int smem = SmemGeom<N>::BYTES;
-  if (smem <= 48 * 1024) return cudaSuccess;
-  return cudaFuncSetAttribute(fft_block_kernel<N, LAYOUT, DIR>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024)
+    e = cudaFuncSetAttribute(fft_block_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  *tma_blocks_per_sm = 0;
+  if constexpr (TmaGeom<N>::ENABLED) {
+    constexpr int tsmem = TmaGeom<N>::BYTES;
+    e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tsmem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma_kernel<N, LAYOUT, DIR>,
+                                                      TmaGeom<N>::THREADS, tsmem);
+  }
+  return e;
+}
+
+template <int N, int LAYOUT, int DIR>
+cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, cudaStream_t s) {
+  if constexpr (TmaGeom<N>::ENABLED) {
+    if (grid <= 0 || a.batch <= 0) return cudaSuccess;
+    fft_block_tma_kernel<N, LAYOUT, DIR><<<grid, TmaGeom<N>::THREADS, TmaGeom<N>::BYTES, s>>>(a);
+    return cudaGetLastError();
+  } else {
+    return cudaErrorNotSupported;
+  }
 }
 
 #define FFTGEN_BLOCK_SWITCH(FN, LAYOUT, DIR, ...)          \
@@ -47,12 +69,15 @@ cudaError_t block_prepare_n() {
   default: return cudaErrorInvalidValue;                   \
   }
 
-#define FFTGEN_BLOCK_INSTANCES(SUFFIX, LAYOUT, DIR)                                      \
-  cudaError_t block_launch_##SUFFIX(int log2n, const BlockArgs &a, cudaStream_t s) {     \
-    FFTGEN_BLOCK_SWITCH(block_launch_n, LAYOUT, DIR, a, s)                               \
-  }                                                                                      \
-  cudaError_t block_prepare_##SUFFIX(int log2n) {                                        \
-    FFTGEN_BLOCK_SWITCH(block_prepare_n, LAYOUT, DIR)                                    \
+#define FFTGEN_BLOCK_INSTANCES(SUFFIX, LAYOUT, DIR)                                           \
+  cudaError_t block_launch_##SUFFIX(int log2n, const BlockArgs &a, cudaStream_t s) {          \
+    FFTGEN_BLOCK_SWITCH(block_launch_n, LAYOUT, DIR, a, s)                                    \
+  }                                                                                           \
+  cudaError_t block_prepare_##SUFFIX(int log2n, int *tma_blocks_per_sm) {                     \
+    FFTGEN_BLOCK_SWITCH(block_prepare_n, LAYOUT, DIR, tma_blocks_per_sm)                      \
+  }                                                                                           \
+  cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, cudaStream_t s) { \
+    FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, s)                          \
   }
 
 }  // namespace fftgen_b200

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <sstream>
@@ -75,6 +77,9 @@ struct fftgen_plan {
   void *d_stage = nullptr;
   size_t stage_bytes = 0;
   cudaStream_t streams[2] = {nullptr, nullptr};
+  // persistent TMA variant: resident CTAs on the device (0 = unavailable)
+  int tma_grid = 0;
+  bool use_tma = true;
 };
 
 namespace {
@@ -117,6 +122,16 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     a.batch = batch;
     a.tw = p->d_tw;
     (void)n;
+    // cp.async.bulk needs 16-byte aligned sources and 16-byte multiples
+    const int64_t esz = layout == FFTGEN_LAYOUT_SPLIT ? 4 : 8;
+    const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
+                         (dist * esz) % 16 == 0;
+    if (p->use_tma && p->tma_grid > 0 && aligned) {
+      const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
+      const int64_t groups = (batch + tp - 1) / tp;
+      const int grid = (int)std::min<int64_t>(groups, p->tma_grid);
+      return block_tma_launch(p->ex.log2n, layout, direction, a, grid, s);
+    }
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
   default:
@@ -227,10 +242,14 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     p->ops = std::move(ops);
     p->radices = std::move(radices);
     if (p->ex.strategy == STRAT_BLOCK) {
-      if ((e = block_prepare(p->ex.log2n)) != cudaSuccess) {
+      int per_sm = 0, sms = 0;
+      if ((e = block_prepare(p->ex.log2n, &per_sm)) != cudaSuccess ||
+          (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess) {
         delete p;
-        return cuda_fail(e, "cudaFuncSetAttribute");
+        return cuda_fail(e, "kernel attributes");
       }
+      p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
+      if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
     }
     const auto &tw = p->ex.tw_block;
     if (!tw.empty()) {
@@ -415,9 +434,17 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
   o << "\n";
   if (p->ex.strategy == STRAT_BLOCK) {
     int64_t threads, tpb, smem;
-    block_launch_geom(p->ex.log2n, &threads, &tpb, &smem);
-    o << "kernel fft_block_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + tpb - 1) / tpb << "] block["
-      << threads << "] smem=" << smem << "B transforms/CTA=" << tpb << "\n";
+    if (p->use_tma && p->tma_grid > 0) {
+      block_tma_geom(p->ex.log2n, &threads, &tpb, &smem);
+      const int64_t groups = (p->cfg.batch + tpb - 1) / tpb;
+      o << "kernel fft_block_tma_kernel<" << p->cfg.n << "> grid[" << std::min<int64_t>(groups, p->tma_grid)
+        << "] block[" << threads << "] smem=" << smem << "B transforms/group=" << tpb
+        << " (persistent, cp.async.bulk double-buffered; direct kernel if unaligned)\n";
+    } else {
+      block_launch_geom(p->ex.log2n, &threads, &tpb, &smem);
+      o << "kernel fft_block_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + tpb - 1) / tpb << "] block["
+        << threads << "] smem=" << smem << "B transforms/CTA=" << tpb << "\n";
+    }
     for (size_t i = 0; i < p->ex.passes.size(); ++i) {
       const auto &d = p->ex.passes[i];
       o << "  pass " << i << ": radix " << d.R << " s=" << d.s << " cols=" << d.cols << " k=" << d.k

@@ -1,6 +1,6 @@
 // fft_block.cuh -- K2: batched, shared-memory-resident Stockham FFT (sm_100a).
 //
-// One CTA owns TPB whole transforms.  The reference's Stockham stage list
+// A CTA owns whole transforms.  The reference's Stockham stage list
 // (plan_stockham, proj/src/formula.cpp:168-197) is regrouped into P <= 3
 // register passes of radix R_p <= 64; pass p is one Stockham stage of radix
 // R_p with cumulative size s_p, cols_p = s_p / R_p, k_p = N / s_p:
@@ -14,12 +14,21 @@
 //   * the TwiddleMul of the pass is one multiply by w_s^{A m} from a
 //     coalesced [A][m] fp32 table (precomputed in fp64 at plan time, shared by
 //     both layouts and both directions),
-//   * the FusedMKIV butterflies are the register codelet (codelets.cuh),
+//   * the FusedMKIV butterflies are the packed fp32x2 register codelets
+//     (codelets.cuh),
 //   * HBM is touched exactly once on load (pass 0) and once on store (pass
 //     P-1): 16 N bytes per transform, the roofline's algorithmic traffic.
-// Between passes the data crosses shared memory once, in split re/im float
-// arrays with a padding chosen at compile time (pad_search) so that both
-// the writer's and the reader's 32-lane access patterns are conflict-free.
+// Between passes the data crosses shared memory once as float2 with a padding
+// chosen at compile time (block_geom.hpp) so writer and reader are
+// conflict-free.
+//
+// Two variants:
+//   fft_block_kernel      one CTA per TPB transforms, HBM -> registers directly
+//                         (any alignment / dist; all N <= 2^14)
+//   fft_block_tma_kernel  persistent; the next group's input is fetched by
+//                         cp.async.bulk (TMA) into a double-buffered stage while
+//                         the current group computes, so HBM latency is off the
+//                         critical path (16-byte aligned data, 256 <= N <= 8192)
 #pragma once
 
 #include <cstdint>
@@ -30,135 +39,220 @@
 
 namespace fftgen_b200 {
 
-
 template <int LAYOUT> struct GIO;
 template <> struct GIO<LAYOUT_INTERLEAVED> {
-  static __device__ __forceinline__ void load(const BlockArgs &a, int64_t off, float &re, float &im) {
-    const float2 v = __ldcs(reinterpret_cast<const float2 *>(a.in0) + off);
-    re = v.x;
-    im = v.y;
+  static FFTGEN_FI float2 load(const BlockArgs &a, int64_t off) {
+    return __ldcs(reinterpret_cast<const float2 *>(a.in0) + off);
   }
-  static __device__ __forceinline__ void store(const BlockArgs &a, int64_t off, float re, float im) {
-    __stcs(reinterpret_cast<float2 *>(a.out0) + off, make_float2(re, im));
+  static FFTGEN_FI void store(const BlockArgs &a, int64_t off, float2 v) {
+    __stcs(reinterpret_cast<float2 *>(a.out0) + off, v);
   }
 };
 template <> struct GIO<LAYOUT_SPLIT> {
-  static __device__ __forceinline__ void load(const BlockArgs &a, int64_t off, float &re, float &im) {
-    re = __ldcs(reinterpret_cast<const float *>(a.in0) + off);
-    im = __ldcs(reinterpret_cast<const float *>(a.in1) + off);
+  static FFTGEN_FI float2 load(const BlockArgs &a, int64_t off) {
+    return make_float2(__ldcs(reinterpret_cast<const float *>(a.in0) + off),
+                       __ldcs(reinterpret_cast<const float *>(a.in1) + off));
   }
-  static __device__ __forceinline__ void store(const BlockArgs &a, int64_t off, float re, float im) {
-    __stcs(reinterpret_cast<float *>(a.out0) + off, re);
-    __stcs(reinterpret_cast<float *>(a.out1) + off, im);
+  static FFTGEN_FI void store(const BlockArgs &a, int64_t off, float2 v) {
+    __stcs(reinterpret_cast<float *>(a.out0) + off, v.x);
+    __stcs(reinterpret_cast<float *>(a.out1) + off, v.y);
   }
 };
 
-template <int N, int p, int DIR>
-__device__ __forceinline__ void pass_twiddle(const float2 *__restrict__ tw, int m, int A, float &re, float &im) {
-  using G = BlockGeom<N>;
-  if (A == 0) return;
-  const float2 w = __ldg(tw + G::TW_OFF(p) + A * G::COLS(p) + m);
-  const float wi = DIR < 0 ? w.y : -w.y;
-  const float t = re * w.x - im * wi;
-  im = fmaf(re, wi, im * w.x);
-  re = t;
+// ---- pass building blocks (G = BlockGeom<N, TP>) -----------------------
+
+// pass 0 from an element accessor: v[j*R + A] = x[A*k + c], c = t + j*T
+template <class G, int DIR, class Load>
+FFTGEN_FI void pass0(int t, float2 *v, Load &&load) {
+  constexpr int R = G::R(0), k = G::K(0), J = G::RMAX / R;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int c = t + j * G::T;
+#pragma unroll
+    for (int A = 0; A < R; ++A) v[j * R + A] = load(A * k + c);
+    reg_fft<R, DIR>(v + j * R);
+  }
 }
 
-template <int N, int p>
-__device__ __forceinline__ void smem_write(float *sre, float *sim, int t, const float *re, const float *im) {
-  using G = BlockGeom<N>;
-  constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R, T = G::T;
+template <class G, int N, int p>
+FFTGEN_FI void smem_write(float2 *sx, int t, const float2 *v) {
+  constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R;
   constexpr Pad pd = BoundaryPad<N, p>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
-    const int u = t + j * T, m = u / k, c = u % k;
+    const int u = t + j * G::T, m = u / k, c = u % k;
 #pragma unroll
-    for (int B = 0; B < R; ++B) {
-      const int idx = padded((B * cols + m) * k + c, pd);
-      sre[idx] = re[j * R + B];
-      sim[idx] = im[j * R + B];
+    for (int B = 0; B < R; ++B) sx[padded((B * cols + m) * k + c, pd)] = v[j * R + B];
+  }
+}
+
+template <class G, int N, int p, int DIR>
+FFTGEN_FI void smem_read_pass(const float2 *sx, int t, const float2 *__restrict__ tw, float2 *v) {
+  constexpr int R = G::R(p), k = G::K(p), cols = G::COLS(p), J = G::RMAX / R;
+  constexpr Pad pd = BoundaryPad<N, p - 1>::value;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+    const float2 *twp = tw + G::TW_OFF(p) + m;
+    v[j * R] = sx[padded((m * R) * k + c, pd)];
+#pragma unroll
+    for (int A = 1; A < R; ++A)
+      v[j * R + A] = mul_tw<DIR>(sx[padded((m * R + A) * k + c, pd)], __ldg(twp + A * cols));
+    reg_fft<R, DIR>(v + j * R);
+  }
+}
+
+// last pass: k == 1 so lanes over m are coalesced in HBM
+template <class G, int LAYOUT>
+FFTGEN_FI void store_last(const BlockArgs &a, int64_t obase, int t, const float2 *v) {
+  constexpr int q = G::P - 1;
+  constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / R;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+#pragma unroll
+    for (int B = 0; B < R; ++B) GIO<LAYOUT>::store(a, obase + (B * cols + m) * k + c, v[j * R + B]);
+  }
+}
+
+// passes 1..P-1 through the exchange buffer sx
+template <class G, int N, int DIR>
+FFTGEN_FI void middle_passes(float2 *sx, int t, const float2 *__restrict__ tw, float2 *v) {
+  if constexpr (G::P > 1) {
+    smem_write<G, N, 0>(sx, t, v);
+    __syncthreads();
+    smem_read_pass<G, N, 1, DIR>(sx, t, tw, v);
+    if constexpr (G::P > 2) {
+      __syncthreads();
+      smem_write<G, N, 1>(sx, t, v);
+      __syncthreads();
+      smem_read_pass<G, N, 2, DIR>(sx, t, tw, v);
     }
   }
 }
 
-template <int N, int p, int DIR>
-__device__ __forceinline__ void smem_read_pass(const float *sre, const float *sim, int t,
-                                               const float2 *__restrict__ tw, float *re, float *im) {
+// ---- variant 1: direct ---------------------------------------------------
+template <int N, int LAYOUT, int DIR>
+__global__ void __launch_bounds__(BlockGeom<N>::THREADS) fft_block_kernel(const BlockArgs args) {
   using G = BlockGeom<N>;
-  constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R, T = G::T;
-  constexpr Pad pd = BoundaryPad<N, p - 1>::value;
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    const int u = t + j * T, m = u / k, c = u % k;
-#pragma unroll
-    for (int A = 0; A < R; ++A) {
-      const int idx = padded((m * R + A) * k + c, pd);
-      re[j * R + A] = sre[idx];
-      im[j * R + A] = sim[idx];
-      pass_twiddle<N, p, DIR>(tw, m, A, re[j * R + A], im[j * R + A]);
+  extern __shared__ float4 smem_f4[];
+  const int tid = threadIdx.x;
+  const int f = tid / G::T;
+  const int t = tid - f * G::T;
+  const int64_t b = (int64_t)blockIdx.x * G::TPB + f;
+  const bool live = b < args.batch;
+  const int64_t ibase = b * args.idist;
+
+  float2 v[G::RMAX];
+  pass0<G, DIR>(t, v, [&](int e) { return live ? GIO<LAYOUT>::load(args, ibase + e) : make_float2(0.f, 0.f); });
+  float2 *sx = reinterpret_cast<float2 *>(smem_f4) + f * SmemGeom<N>::REGION;
+  middle_passes<G, N, DIR>(sx, t, args.tw, v);
+  if (live) store_last<G, LAYOUT>(args, b * args.odist, t, v);
+}
+
+// ---- variant 2: persistent, TMA double-buffered --------------------------
+FFTGEN_FI uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+FFTGEN_FI void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+FFTGEN_FI void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+FFTGEN_FI void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// 1-D bulk copy global -> shared (TMA), completion counted on `bar`
+FFTGEN_FI void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+FFTGEN_FI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int N, int LAYOUT>
+FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t group) {
+  using TG = TmaGeom<N>;
+  const int64_t b0 = group * TG::TP;
+  const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
+  constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
+  mbar_expect_tx(bar, (uint32_t)cnt * 8 * N);
+  for (int f = 0; f < cnt; ++f) {
+    char *dst = stage + f * TG::SLOT;
+    const int64_t b = b0 + f;
+    if (LAYOUT == LAYOUT_SPLIT) {
+      bulk_g2s(dst, reinterpret_cast<const float *>(a.in0) + b * a.idist, plane, bar);
+      bulk_g2s(dst + plane, reinterpret_cast<const float *>(a.in1) + b * a.idist, plane, bar);
+    } else {
+      bulk_g2s(dst, reinterpret_cast<const float2 *>(a.in0) + b * a.idist, plane, bar);
     }
-    reg_fft<R, DIR>(re + j * R, im + j * R);
   }
 }
 
 template <int N, int LAYOUT, int DIR>
-__global__ void __launch_bounds__(BlockGeom<N>::THREADS)
-fft_block_kernel(const BlockArgs args) {
-  using G = BlockGeom<N>;
-  constexpr int T = G::T, TPB = G::TPB, RM = G::RMAX, P = G::P;
-  extern __shared__ float smem[];
+__global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
+  using TG = TmaGeom<N>;
+  using G = typename TG::G;
+  extern __shared__ float4 smem_f4[];
+  char *smem = reinterpret_cast<char *>(smem_f4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TG::STAGES * TG::STAGE_BYTES);
   const int tid = threadIdx.x;
-  const int f = tid / T;
-  const int t = tid - f * T;
-  const int64_t b = (int64_t)blockIdx.x * TPB + f;
-  const bool live = b < args.batch;
-  const int64_t ibase = b * args.idist, obase = b * args.odist;
+  const int f = tid / G::T;
+  const int t = tid - f * G::T;
+  const int64_t groups = (args.batch + TG::TP - 1) / TG::TP;
+  const int64_t stride = gridDim.x;
 
-  float re[RM], im[RM];
-  // ---- pass 0: HBM -> registers (coalesced across t), codelet ----------
-  {
-    constexpr int R = G::R(0), k = G::K(0), J = RM / R;
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int c = t + j * T;
-#pragma unroll
-      for (int A = 0; A < R; ++A) {
-        if (live) {
-          GIO<LAYOUT>::load(args, ibase + A * k + c, re[j * R + A], im[j * R + A]);
-        } else {
-          re[j * R + A] = 0.f;
-          im[j * R + A] = 0.f;
-        }
-      }
-      reg_fft<R, DIR>(re + j * R, im + j * R);
+  if (tid == 0) {
+    for (int s = 0; s < TG::STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < TG::STAGES; ++s) {
+      const int64_t g = blockIdx.x + s * stride;
+      if (g < groups) tma_issue<N, LAYOUT>(args, smem + s * TG::STAGE_BYTES, &bars[s], g);
     }
   }
-  if constexpr (P > 1) {
-    float *sre = smem + f * (2 * SmemGeom<N>::REGION);
-    float *sim = sre + SmemGeom<N>::REGION;
-    smem_write<N, 0>(sre, sim, t, re, im);
-    __syncthreads();
-    smem_read_pass<N, 1, DIR>(sre, sim, t, args.tw, re, im);
-    if constexpr (P > 2) {
-      __syncthreads();
-      smem_write<N, 1>(sre, sim, t, re, im);
-      __syncthreads();
-      smem_read_pass<N, 2, DIR>(sre, sim, t, args.tw, re, im);
+
+  int it = 0;
+  for (int64_t g = blockIdx.x; g < groups; g += stride, ++it) {
+    const int s = it % TG::STAGES;
+    char *stage = smem + s * TG::STAGE_BYTES;
+    char *slot = stage + f * TG::SLOT;
+    mbar_wait(&bars[s], (it / TG::STAGES) & 1);
+
+    float2 v[G::RMAX];
+    if constexpr (LAYOUT == LAYOUT_SPLIT) {
+      const float *re = reinterpret_cast<const float *>(slot), *im = re + N;
+      pass0<G, DIR>(t, v, [&](int e) { return make_float2(re[e], im[e]); });
+    } else {
+      const float2 *x = reinterpret_cast<const float2 *>(slot);
+      pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
-  }
-  // ---- last pass: registers -> HBM, k == 1 so lanes over m coalesce -----
-  {
-    constexpr int q = P - 1;
-    constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = RM / R;
-    if (live) {
-#pragma unroll
-      for (int j = 0; j < J; ++j) {
-        const int u = t + j * T, m = u / k, c = u % k;
-#pragma unroll
-        for (int B = 0; B < R; ++B)
-          GIO<LAYOUT>::store(args, obase + (B * cols + m) * k + c, re[j * R + B], im[j * R + B]);
+    __syncthreads();  // raw stage fully consumed; reuse it as the exchange
+    middle_passes<G, N, DIR>(reinterpret_cast<float2 *>(slot), t, args.tw, v);
+    __syncthreads();  // exchange fully consumed; the stage may be refilled
+    if (tid == 0) {
+      const int64_t gn = g + TG::STAGES * stride;
+      if (gn < groups) {
+        fence_proxy_async();
+        tma_issue<N, LAYOUT>(args, stage, &bars[s], gn);
       }
     }
+    const int64_t b = g * TG::TP + f;
+    if (b < args.batch) store_last<G, LAYOUT>(args, b * args.odist, t, v);
   }
 }
 

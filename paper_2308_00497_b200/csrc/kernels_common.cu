@@ -3,6 +3,8 @@
 // fp32 conversion kernels used by fftgen_interpret_f64.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "fft_block.cuh"
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -13,10 +15,14 @@ cudaError_t block_launch_i_f(int, const BlockArgs &, cudaStream_t);
 cudaError_t block_launch_i_b(int, const BlockArgs &, cudaStream_t);
 cudaError_t block_launch_s_f(int, const BlockArgs &, cudaStream_t);
 cudaError_t block_launch_s_b(int, const BlockArgs &, cudaStream_t);
-cudaError_t block_prepare_i_f(int);
-cudaError_t block_prepare_i_b(int);
-cudaError_t block_prepare_s_f(int);
-cudaError_t block_prepare_s_b(int);
+cudaError_t block_prepare_i_f(int, int *);
+cudaError_t block_prepare_i_b(int, int *);
+cudaError_t block_prepare_s_f(int, int *);
+cudaError_t block_prepare_s_b(int, int *);
+cudaError_t block_tma_launch_i_f(int, const BlockArgs &, int, cudaStream_t);
+cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, cudaStream_t);
+cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, cudaStream_t);
+cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, cudaStream_t);
 
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
@@ -24,12 +30,58 @@ cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cud
   return dir < 0 ? block_launch_s_f(log2n, a, s) : block_launch_s_b(log2n, a, s);
 }
 
-cudaError_t block_prepare(int log2n) {
+cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, cudaStream_t s) {
+  if (layout == LAYOUT_INTERLEAVED)
+    return dir < 0 ? block_tma_launch_i_f(log2n, a, grid, s) : block_tma_launch_i_b(log2n, a, grid, s);
+  return dir < 0 ? block_tma_launch_s_f(log2n, a, grid, s) : block_tma_launch_s_b(log2n, a, grid, s);
+}
+
+// Sets the smem attributes of all four (layout, direction) instances and
+// returns the TMA variant's resident CTAs per SM (min over instances; 0 if
+// the size has no TMA variant).
+cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
   cudaError_t e;
-  if ((e = block_prepare_i_f(log2n)) != cudaSuccess) return e;
-  if ((e = block_prepare_i_b(log2n)) != cudaSuccess) return e;
-  if ((e = block_prepare_s_f(log2n)) != cudaSuccess) return e;
-  return block_prepare_s_b(log2n);
+  int b[4] = {0, 0, 0, 0};
+  if ((e = block_prepare_i_f(log2n, &b[0])) != cudaSuccess) return e;
+  if ((e = block_prepare_i_b(log2n, &b[1])) != cudaSuccess) return e;
+  if ((e = block_prepare_s_f(log2n, &b[2])) != cudaSuccess) return e;
+  if ((e = block_prepare_s_b(log2n, &b[3])) != cudaSuccess) return e;
+  *tma_blocks_per_sm = std::min(std::min(b[0], b[1]), std::min(b[2], b[3]));
+  return cudaSuccess;
+}
+
+bool block_tma_enabled(int log2n) {
+  switch (log2n) {
+  case 8: return TmaGeom<256>::ENABLED;
+  case 9: return TmaGeom<512>::ENABLED;
+  case 10: return TmaGeom<1024>::ENABLED;
+  case 11: return TmaGeom<2048>::ENABLED;
+  case 12: return TmaGeom<4096>::ENABLED;
+  case 13: return TmaGeom<8192>::ENABLED;
+  default: return false;
+  }
+}
+
+void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem) {
+  *threads = *tp = *smem = 0;
+  switch (log2n) {
+#define FFTGEN_TG(L, NN) case L: *threads = TmaGeom<NN>::THREADS; *tp = TmaGeom<NN>::TP; *smem = TmaGeom<NN>::BYTES; return;
+  FFTGEN_TG(8, 256) FFTGEN_TG(9, 512) FFTGEN_TG(10, 1024) FFTGEN_TG(11, 2048) FFTGEN_TG(12, 4096) FFTGEN_TG(13, 8192)
+#undef FFTGEN_TG
+  default: return;
+  }
+}
+
+int block_tma_transforms_per_cta(int log2n) {
+  switch (log2n) {
+  case 8: return TmaGeom<256>::TP;
+  case 9: return TmaGeom<512>::TP;
+  case 10: return TmaGeom<1024>::TP;
+  case 11: return TmaGeom<2048>::TP;
+  case 12: return TmaGeom<4096>::TP;
+  case 13: return TmaGeom<8192>::TP;
+  default: return 0;
+  }
 }
 
 // ---- fp64 <-> fp32 for the interpret() drop-in ---------------------------

@@ -272,4 +272,4 @@ def test_introspection_matches_reference_goldens(golden, golden_meta):
     assert p.radices() == [2] * 12
     assert [d[0] for d in p.passes()] == [64, 64]
     assert p.launches() == 1
-    assert "fft_block_kernel<4096>" in p.describe()
+    assert "fft_block_tma_kernel<4096>" in p.describe()
