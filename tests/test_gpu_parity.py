@@ -273,3 +273,39 @@ def test_introspection_matches_reference_goldens(golden, golden_meta):
     assert [d[0] for d in p.passes()] == [64, 64]
     assert p.launches() == 1
     assert "fft_block_tma_kernel<4096>" in p.describe()
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096, 8192])
+def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
+    """The persistent TMA variant and the direct variant run the same passes."""
+    x = seeded_batch(orc, n, 37)
+    for layout in ("interleaved", "split"):
+        a = run(n, layout, -1, x)
+        monkeypatch.setenv("FFTGEN_DISABLE_TMA", "1")
+        b = run(n, layout, -1, x)
+        monkeypatch.delenv("FFTGEN_DISABLE_TMA")
+        assert np.array_equal(a, b), layout
+        check(a, orc.forward(x, "stockham", 4), n)
+
+
+def test_unaligned_dist_uses_direct_path(orc):
+    # dist*4 bytes not a multiple of 16 -> no cp.async.bulk; still correct
+    n = 4096
+    x = seeded_batch(orc, n, 5)
+    check(run(n, "split", -1, x, dist=n + 3), orc.forward(x, "stockham", 4), n)
+    check(run(n, "interleaved", 1, x, dist=n + 1), orc.forward(x, "stockham", 4, inverse=True), n)
+
+
+def test_large_batch_persistent_grid(orc):
+    """More groups than resident CTAs: every transform visited exactly once."""
+    n, batch = 1024, 20000
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
+    y = torch.full_like(x, float("nan"))
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    plan.execute(x, y)
+    torch.cuda.synchronize()
+    assert not torch.isnan(y).any()
+    for b in (0, 777, batch - 1):
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        assert oracle.rel_l2(y[b].reshape(-1).double().cpu().numpy(), orc.forward(xi, "stockham", 4)) < 2e-6
