@@ -29,20 +29,31 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
   *tma_blocks_per_sm = 0;
   if constexpr (TmaGeom<N>::ENABLED) {
     constexpr int tsmem = TmaGeom<N>::BYTES;
-    e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tsmem);
+    e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma_kernel<N, LAYOUT, DIR>,
+    e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+    if (e != cudaSuccess) return e;
+    int b0 = 0, b1 = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, fft_block_tma_kernel<N, LAYOUT, DIR, false>,
                                                       TmaGeom<N>::THREADS, tsmem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, fft_block_tma_kernel<N, LAYOUT, DIR, true>,
+                                                      TmaGeom<N>::THREADS, tsmem);
+    *tma_blocks_per_sm = b0 < b1 ? b0 : b1;
   }
   return e;
 }
 
 template <int N, int LAYOUT, int DIR>
-cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, cudaStream_t s) {
+cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, bool store_tma, cudaStream_t s) {
   if constexpr (TmaGeom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
-    fft_block_tma_kernel<N, LAYOUT, DIR><<<grid, TmaGeom<N>::THREADS, TmaGeom<N>::BYTES, s>>>(a);
+    if (store_tma)
+      fft_block_tma_kernel<N, LAYOUT, DIR, true><<<grid, TmaGeom<N>::THREADS, TmaGeom<N>::BYTES, s>>>(a);
+    else
+      fft_block_tma_kernel<N, LAYOUT, DIR, false><<<grid, TmaGeom<N>::THREADS, TmaGeom<N>::BYTES, s>>>(a);
     return cudaGetLastError();
   } else {
     return cudaErrorNotSupported;
@@ -76,8 +87,9 @@ cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, cudaStream_t s) {
   cudaError_t block_prepare_##SUFFIX(int log2n, int *tma_blocks_per_sm) {                     \
     FFTGEN_BLOCK_SWITCH(block_prepare_n, LAYOUT, DIR, tma_blocks_per_sm)                      \
   }                                                                                           \
-  cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, cudaStream_t s) { \
-    FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, s)                          \
+  cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, bool store_tma, \
+                                        cudaStream_t s) {                                     \
+    FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, store_tma, s)               \
   }
 
 }  // namespace fftgen_b200

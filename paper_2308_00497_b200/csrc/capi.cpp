@@ -80,6 +80,7 @@ struct fftgen_plan {
   // persistent TMA variant: resident CTAs on the device (0 = unavailable)
   int tma_grid = 0;
   bool use_tma = true;
+  bool use_tma_store = true;
 };
 
 namespace {
@@ -126,11 +127,12 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const int64_t esz = layout == FFTGEN_LAYOUT_SPLIT ? 4 : 8;
     const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                          (dist * esz) % 16 == 0;
+    const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
     if (p->use_tma && p->tma_grid > 0 && aligned) {
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
       const int64_t groups = (batch + tp - 1) / tp;
       const int grid = (int)std::min<int64_t>(groups, p->tma_grid);
-      return block_tma_launch(p->ex.log2n, layout, direction, a, grid, s);
+      return block_tma_launch(p->ex.log2n, layout, direction, a, grid, p->use_tma_store && out_aligned, s);
     }
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
@@ -250,6 +252,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       }
       p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
+      if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
     }
     const auto &tw = p->ex.tw_block;
     if (!tw.empty()) {

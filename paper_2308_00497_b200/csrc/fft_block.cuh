@@ -102,6 +102,40 @@ FFTGEN_FI void smem_read_pass(const float2 *sx, int t, const float2 *__restrict_
   }
 }
 
+// Factored pass twiddles for a 2-pass plan: pass 1 has k == 1 and J == 1, so
+// thread t always owns butterfly m = t and needs w_s^{A m} for A < R only.
+// With A = a*RLO + b:  w^{A m} = Q[a] * P[b],  P[b] = w^{b m},  Q[a] = w^{RLO a m},
+// loaded once per thread from the [A][m] table (RLO-1 + RHI-1 values).
+template <class G> struct TwPQ {
+  static constexpr int R = G::R(1);
+  static constexpr int RLO = R >= 16 ? 8 : (R >= 4 ? 4 : R);
+  static constexpr int RHI = R / RLO;
+  float2 p[RLO], q[RHI];
+  FFTGEN_FI void load(const float2 *__restrict__ tw, int m) {
+    const float2 *base = tw + G::TW_OFF(1) + m;
+#pragma unroll
+    for (int b = 1; b < RLO; ++b) p[b] = __ldg(base + b * G::COLS(1));
+#pragma unroll
+    for (int a = 1; a < RHI; ++a) q[a] = __ldg(base + a * RLO * G::COLS(1));
+  }
+  template <int DIR> FFTGEN_FI float2 apply(float2 x, int A) const {
+    const int a = A / RLO, b = A % RLO;
+    if (b) x = mul_tw<DIR>(x, p[b]);
+    if (a) x = mul_tw<DIR>(x, q[a]);
+    return x;
+  }
+};
+
+template <class G, int N, int DIR>
+FFTGEN_FI void smem_read_pass1_pq(const float2 *sx, int t, const TwPQ<G> &w, float2 *v) {
+  constexpr int R = G::R(1);
+  constexpr Pad pd = BoundaryPad<N, 0>::value;
+  static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == R, "factored twiddles need a 2-pass plan");
+#pragma unroll
+  for (int A = 0; A < R; ++A) v[A] = w.template apply<DIR>(sx[padded(t * R + A, pd)], A);
+  reg_fft<R, DIR>(v);
+}
+
 // last pass: k == 1 so lanes over m are coalesced in HBM
 template <class G, int LAYOUT>
 FFTGEN_FI void store_last(const BlockArgs &a, int64_t obase, int t, const float2 *v) {
@@ -146,7 +180,15 @@ __global__ void __launch_bounds__(BlockGeom<N>::THREADS) fft_block_kernel(const 
   float2 v[G::RMAX];
   pass0<G, DIR>(t, v, [&](int e) { return live ? GIO<LAYOUT>::load(args, ibase + e) : make_float2(0.f, 0.f); });
   float2 *sx = reinterpret_cast<float2 *>(smem_f4) + f * SmemGeom<N>::REGION;
-  middle_passes<G, N, DIR>(sx, t, args.tw, v);
+  if constexpr (G::P == 2) {
+    TwPQ<G> pq;
+    pq.load(args.tw, t);
+    smem_write<G, N, 0>(sx, t, v);
+    __syncthreads();
+    smem_read_pass1_pq<G, N, DIR>(sx, t, pq, v);
+  } else {
+    middle_passes<G, N, DIR>(sx, t, args.tw, v);
+  }
   if (live) store_last<G, LAYOUT>(args, b * args.odist, t, v);
 }
 
@@ -201,10 +243,63 @@ FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t
   }
 }
 
-template <int N, int LAYOUT, int DIR>
+// 1-D bulk copy shared -> global (TMA store), tracked by the bulk group
+FFTGEN_FI void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+FFTGEN_FI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+FFTGEN_FI void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+FFTGEN_FI void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Stage the last pass's outputs in the slot (raw layout) for a bulk store.
+template <class G, int N, int LAYOUT>
+FFTGEN_FI void smem_write_out(char *slot, int t, const float2 *v) {
+  constexpr int q = G::P - 1;
+  constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / R;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+#pragma unroll
+    for (int B = 0; B < R; ++B) {
+      const int e = (B * cols + m) * k + c;
+      if constexpr (LAYOUT == LAYOUT_SPLIT) {
+        reinterpret_cast<float *>(slot)[e] = v[j * R + B].x;
+        reinterpret_cast<float *>(slot)[N + e] = v[j * R + B].y;
+      } else {
+        reinterpret_cast<float2 *>(slot)[e] = v[j * R + B];
+      }
+    }
+  }
+}
+
+template <int N, int LAYOUT>
+FFTGEN_FI void tma_store(const BlockArgs &a, char *stage, int64_t group) {
+  using TG = TmaGeom<N>;
+  const int64_t b0 = group * TG::TP;
+  const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
+  constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
+  for (int f = 0; f < cnt; ++f) {
+    char *src = stage + f * TG::SLOT;
+    const int64_t b = b0 + f;
+    if (LAYOUT == LAYOUT_SPLIT) {
+      bulk_s2g(reinterpret_cast<float *>(a.out0) + b * a.odist, src, plane);
+      bulk_s2g(reinterpret_cast<float *>(a.out1) + b * a.odist, src + plane, plane);
+    } else {
+      bulk_s2g(reinterpret_cast<float2 *>(a.out0) + b * a.odist, src, plane);
+    }
+  }
+  bulk_commit();
+}
+
+// STORE_TMA: outputs go smem -> HBM by cp.async.bulk (needs 16-byte aligned
+// output rows) instead of per-thread coalesced st.global.
+template <int N, int LAYOUT, int DIR, bool STORE_TMA>
 __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
   using TG = TmaGeom<N>;
   using G = typename TG::G;
+  static_assert(TG::STAGES == 2, "refill schedule assumes double buffering");
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TG::STAGES * TG::STAGE_BYTES);
@@ -225,13 +320,25 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       if (g < groups) tma_issue<N, LAYOUT>(args, smem + s * TG::STAGE_BYTES, &bars[s], g);
     }
   }
+  // 2-pass plans: this thread's pass-1 twiddle bases live in registers
+  TwPQ<G> pq;
+  if constexpr (G::P == 2) pq.load(args.tw, t);
 
   int it = 0;
   for (int64_t g = blockIdx.x; g < groups; g += stride, ++it) {
-    const int s = it % TG::STAGES;
+    const int s = it & 1;
     char *stage = smem + s * TG::STAGE_BYTES;
     char *slot = stage + f * TG::SLOT;
-    mbar_wait(&bars[s], (it / TG::STAGES) & 1);
+    if (STORE_TMA && tid == 0 && it >= 1) {
+      // the other stage held group it-1, now being bulk-stored: refill it
+      // with group it+1 once the store has finished reading shared memory
+      const int64_t gn = g + stride;
+      if (gn < groups) {
+        bulk_wait_read0();
+        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[s ^ 1], gn);
+      }
+    }
+    mbar_wait(&bars[s], (it >> 1) & 1);
 
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
@@ -242,18 +349,34 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
-    middle_passes<G, N, DIR>(reinterpret_cast<float2 *>(slot), t, args.tw, v);
-    __syncthreads();  // exchange fully consumed; the stage may be refilled
-    if (tid == 0) {
-      const int64_t gn = g + TG::STAGES * stride;
-      if (gn < groups) {
-        fence_proxy_async();
-        tma_issue<N, LAYOUT>(args, stage, &bars[s], gn);
-      }
+    float2 *sx = reinterpret_cast<float2 *>(slot);
+    if constexpr (G::P == 2) {
+      smem_write<G, N, 0>(sx, t, v);
+      __syncthreads();
+      smem_read_pass1_pq<G, N, DIR>(sx, t, pq, v);
+    } else {
+      middle_passes<G, N, DIR>(sx, t, args.tw, v);
     }
+    __syncthreads();  // exchange fully consumed
     const int64_t b = g * TG::TP + f;
-    if (b < args.batch) store_last<G, LAYOUT>(args, b * args.odist, t, v);
+    if constexpr (STORE_TMA) {
+      smem_write_out<G, N, LAYOUT>(slot, t, v);
+      fence_proxy_async();  // make generic-proxy writes visible to the bulk copy
+      __syncthreads();
+      if (tid == 0) tma_store<N, LAYOUT>(args, stage, g);
+      (void)b;
+    } else {
+      if (tid == 0) {
+        const int64_t gn = g + TG::STAGES * stride;
+        if (gn < groups) {
+          fence_proxy_async();
+          tma_issue<N, LAYOUT>(args, stage, &bars[s], gn);
+        }
+      }
+      if (b < args.batch) store_last<G, LAYOUT>(args, b * args.odist, t, v);
+    }
   }
+  if (STORE_TMA && tid == 0) bulk_wait0();
 }
 
 }  // namespace fftgen_b200

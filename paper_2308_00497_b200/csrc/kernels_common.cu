@@ -19,10 +19,10 @@ cudaError_t block_prepare_i_f(int, int *);
 cudaError_t block_prepare_i_b(int, int *);
 cudaError_t block_prepare_s_f(int, int *);
 cudaError_t block_prepare_s_b(int, int *);
-cudaError_t block_tma_launch_i_f(int, const BlockArgs &, int, cudaStream_t);
-cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, cudaStream_t);
-cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, cudaStream_t);
-cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, cudaStream_t);
+cudaError_t block_tma_launch_i_f(int, const BlockArgs &, int, bool, cudaStream_t);
+cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, bool, cudaStream_t);
+cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, bool, cudaStream_t);
+cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, bool, cudaStream_t);
 
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
@@ -30,10 +30,13 @@ cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cud
   return dir < 0 ? block_launch_s_f(log2n, a, s) : block_launch_s_b(log2n, a, s);
 }
 
-cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, cudaStream_t s) {
+cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, bool store_tma,
+                             cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
-    return dir < 0 ? block_tma_launch_i_f(log2n, a, grid, s) : block_tma_launch_i_b(log2n, a, grid, s);
-  return dir < 0 ? block_tma_launch_s_f(log2n, a, grid, s) : block_tma_launch_s_b(log2n, a, grid, s);
+    return dir < 0 ? block_tma_launch_i_f(log2n, a, grid, store_tma, s)
+                   : block_tma_launch_i_b(log2n, a, grid, store_tma, s);
+  return dir < 0 ? block_tma_launch_s_f(log2n, a, grid, store_tma, s)
+                 : block_tma_launch_s_b(log2n, a, grid, store_tma, s);
 }
 
 // Sets the smem attributes of all four (layout, direction) instances and

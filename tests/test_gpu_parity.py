@@ -284,7 +284,10 @@ def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
         monkeypatch.setenv("FFTGEN_DISABLE_TMA", "1")
         b = run(n, layout, -1, x)
         monkeypatch.delenv("FFTGEN_DISABLE_TMA")
-        assert np.array_equal(a, b), layout
+        monkeypatch.setenv("FFTGEN_DISABLE_TMA_STORE", "1")
+        c = run(n, layout, -1, x)
+        monkeypatch.delenv("FFTGEN_DISABLE_TMA_STORE")
+        assert np.array_equal(a, b) and np.array_equal(a, c), layout
         check(a, orc.forward(x, "stockham", 4), n)
 
 
