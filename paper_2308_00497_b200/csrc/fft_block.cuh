@@ -329,15 +329,6 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
     const int s = it & 1;
     char *stage = smem + s * TG::STAGE_BYTES;
     char *slot = stage + f * TG::SLOT;
-    if (STORE_TMA && tid == 0 && it >= 1) {
-      // the other stage held group it-1, now being bulk-stored: refill it
-      // with group it+1 once the store has finished reading shared memory
-      const int64_t gn = g + stride;
-      if (gn < groups) {
-        bulk_wait_read0();
-        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[s ^ 1], gn);
-      }
-    }
     mbar_wait(&bars[s], (it >> 1) & 1);
 
     float2 v[G::RMAX];
@@ -349,6 +340,16 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
+    if (STORE_TMA && tid == 0 && it >= 1) {
+      // the other stage held group it-1, bulk-stored at the end of the last
+      // iteration: refill it with group it+1 once that store has drained
+      // shared memory (pass 0 above overlapped the drain)
+      const int64_t gn = g + stride;
+      if (gn < groups) {
+        bulk_wait_read0();
+        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[s ^ 1], gn);
+      }
+    }
     float2 *sx = reinterpret_cast<float2 *>(slot);
     if constexpr (G::P == 2) {
       smem_write<G, N, 0>(sx, t, v);
