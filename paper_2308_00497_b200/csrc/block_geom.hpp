@@ -164,4 +164,21 @@ template <int N> struct TmaGeom {
   static constexpr int BYTES = STAGES * STAGE_BYTES + 128;            // + mbarriers
 };
 
+// -------------------------------------------------------------------------
+// K3 group kernel tile: TC adjacent transforms of size NS per CTA (~64 KB of
+// float2 in shared memory, <= 512 threads); odd per-transform stride REG so
+// lanes walking over the tile index f hit distinct bank pairs.
+template <int NS> struct GroupGeom {
+  static constexpr int T = BlockGeom<NS>::T;
+  static constexpr int TC_BYTES = 65536 / (8 * NS);                 // ~64 KB tiles
+  static constexpr int TC = TC_BYTES * T > 512 ? 512 / T : TC_BYTES;  // <= 512 threads
+  using G = BlockGeom<NS, TC>;
+  static constexpr int THREADS = G::THREADS;
+  static constexpr int EX = SmemGeom<NS>::REGION > NS ? SmemGeom<NS>::REGION : NS;
+  static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
+  static constexpr int BYTES = TC * REG * 8;
+  static constexpr int R0 = G::R(0);
+  static constexpr int K0 = NS / R0;
+};
+
 }  // namespace fftgen_b200

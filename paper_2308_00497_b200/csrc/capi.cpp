@@ -72,6 +72,10 @@ struct fftgen_plan {
   std::vector<int64_t> radices;
   std::vector<RefOp> ops;
   float2 *d_tw = nullptr;
+  // K3 four-step: device-generated group twiddles and intermediate buffers
+  float2 *d_twg = nullptr;
+  float2 *d_scratch = nullptr;
+  size_t scratch_bytes = 0;
   // host-buffer pipeline scratch (lazily allocated, guarded by mu)
   std::mutex mu;
   void *d_stage = nullptr;
@@ -136,6 +140,35 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     }
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
+  case STRAT_FOURSTEP: {
+    // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
+    const auto &gs = p->ex.groups;
+    const size_t per = (size_t)p->cfg.batch * (size_t)n;  // float2 per scratch buffer
+    for (size_t g = 0; g < gs.size(); ++g) {
+      const GroupDesc &d = gs[g];
+      const bool first = g == 0, last = g + 1 == gs.size();
+      float2 *src = first ? nullptr : p->d_scratch + ((g - 1) % p->ex.scratch_buffers) * per;
+      float2 *dst = last ? nullptr : p->d_scratch + (g % p->ex.scratch_buffers) * per;
+      GroupArgs a{};
+      a.in0 = first ? in0 : src;
+      a.in1 = first ? in1 : nullptr;
+      a.out0 = last ? out0 : dst;
+      a.out1 = last ? out1 : nullptr;
+      a.cols = d.cols;
+      a.k = d.k;
+      a.idist = first ? dist : n;
+      a.odist = last ? dist : n;
+      a.tiles_per_outer = (d.cols * d.k) / d.tc;
+      a.tw_local = p->d_tw + d.local_off;
+      a.tw_q = d.cols > 1 ? p->d_twg + d.q_off : nullptr;
+      a.tw_p = d.cols > 1 ? p->d_twg + d.p_off : nullptr;
+      const bool split = layout == FFTGEN_LAYOUT_SPLIT;
+      const int shape = last ? (split ? 3 : 2) : (first && split ? 1 : 0);
+      cudaError_t e = group_launch(d.log2ns, shape, direction, a, batch, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   default:
     return cudaErrorNotSupported;
   }
@@ -167,7 +200,9 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
   for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++i) {
     const int64_t cnt = std::min(chunk, batch - b0);
     char *slot_ptr = (char *)p->d_stage + (i & 1) * slot;
-    if ((e = stage(b0, cnt, slot_ptr, p->streams[i & 1])) != cudaSuccess) return cuda_fail(e, "host pipeline");
+    // four-step plans share one scratch buffer: keep their chunks stream-ordered
+    const int sid = p->ex.strategy == STRAT_FOURSTEP ? 0 : (i & 1);
+    if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) return cuda_fail(e, "host pipeline");
   }
   for (auto &s : p->streams)
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
@@ -254,19 +289,39 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
     }
+    auto bail = [&](fftgen_status st, const std::string &msg) {
+      fftgen_plan_destroy(p);
+      return fail(st, msg);
+    };
+    if (p->ex.strategy == STRAT_FOURSTEP) {
+      for (const GroupDesc &d : p->ex.groups)
+        if ((e = group_prepare(d.log2ns)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, std::string("group kernel attributes: ") + cudaGetErrorString(e));
+      // K4: Q[A0][m] = w_s^{A0 (NS/R0) m}, P[c][m] = w_s^{c m}, generated on the device in fp64
+      if (p->ex.tw_group_len > 0) {
+        if ((e = cudaMalloc(&p->d_twg, p->ex.tw_group_len * sizeof(float2))) != cudaSuccess)
+          return bail(FFTGEN_ERR_NOMEM, std::string("group twiddles: ") + cudaGetErrorString(e));
+        for (const GroupDesc &d : p->ex.groups) {
+          if (d.cols <= 1) continue;
+          if ((e = gen_twiddles(p->d_twg + d.q_off, d.r0, d.cols, d.ns / d.r0, d.s, 0)) != cudaSuccess ||
+              (e = gen_twiddles(p->d_twg + d.p_off, d.ns / d.r0, d.cols, 1, d.s, 0)) != cudaSuccess)
+            return bail(FFTGEN_ERR_CUDA, std::string("twiddle generation: ") + cudaGetErrorString(e));
+        }
+      }
+      p->scratch_bytes = (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n * sizeof(float2);
+      if ((e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
+        return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
+                                          " bytes): " + cudaGetErrorString(e));
+    }
     const auto &tw = p->ex.tw_block;
     if (!tw.empty()) {
-      if ((e = cudaMalloc(&p->d_tw, tw.size() * sizeof(float))) != cudaSuccess) {
-        delete p;
-        return fail(FFTGEN_ERR_NOMEM, std::string("twiddle table: ") + cudaGetErrorString(e));
-      }
-      if ((e = cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float), cudaMemcpyHostToDevice)) !=
-          cudaSuccess) {
-        cudaFree(p->d_tw);
-        delete p;
-        return cuda_fail(e, "twiddle upload");
-      }
+      if ((e = cudaMalloc(&p->d_tw, tw.size() * sizeof(float))) != cudaSuccess)
+        return bail(FFTGEN_ERR_NOMEM, std::string("twiddle table: ") + cudaGetErrorString(e));
+      if ((e = cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(FFTGEN_ERR_CUDA, std::string("twiddle upload: ") + cudaGetErrorString(e));
     }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess)
+      return bail(FFTGEN_ERR_CUDA, std::string("plan creation: ") + cudaGetErrorString(e));
     *out = p;
     return FFTGEN_OK;
   });
@@ -277,6 +332,8 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
   {
     DeviceGuard g(p->cfg.device);
     if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_twg) cudaFree(p->d_twg);
+    if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_stage) cudaFree(p->d_stage);
     for (auto &s : p->streams)
       if (s) cudaStreamDestroy(s);
@@ -420,11 +477,11 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return 2;
+  default: return (int)p->ex.groups.size();
   }
 }
 
-size_t fftgen_plan_scratch_bytes(const fftgen_plan *p) { return p ? 0 : 0; }
+size_t fftgen_plan_scratch_bytes(const fftgen_plan *p) { return p ? p->scratch_bytes : 0; }
 
 fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) {
   if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
@@ -452,6 +509,18 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
       const auto &d = p->ex.passes[i];
       o << "  pass " << i << ": radix " << d.R << " s=" << d.s << " cols=" << d.cols << " k=" << d.k
         << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
+    }
+  } else if (p->ex.strategy == STRAT_FOURSTEP) {
+    o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
+      << " B\n";
+    for (size_t i = 0; i < p->ex.groups.size(); ++i) {
+      const GroupDesc &d = p->ex.groups[i];
+      int64_t threads, tc, smem, r0;
+      group_geom(d.log2ns, &threads, &tc, &smem, &r0);
+      o << "  group " << i << ": fft_group_kernel<" << d.ns << "> radix " << d.ns << " s=" << d.s
+        << " cols=" << d.cols << " k=" << d.k << (d.rows ? " rows (transposed store)" : " columns")
+        << " grid[" << p->cfg.batch * (d.cols * d.k / tc) << "] block[" << threads << "] smem=" << smem
+        << "B tile=" << tc << "\n";
     }
   } else if (p->ex.strategy == STRAT_IDENTITY) {
     o << "identity copy\n";

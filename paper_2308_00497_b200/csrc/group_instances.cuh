@@ -1,0 +1,72 @@
+// group_instances.cuh -- instantiates the K3 group kernel (fft_group.cuh)
+// for NS = 2^6 .. 2^10 and the (input layout, output layout, rows) shapes a
+// multi-group plan uses: first group (user -> interleaved scratch, columns),
+// middle groups (scratch -> scratch, columns), last group (scratch -> user,
+// rows with the transposed store).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fft_group.cuh"
+
+namespace fftgen_b200 {
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+cudaError_t group_launch_t(const GroupArgs &a, int64_t grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  fft_group_kernel<NS, LIN, LOUT, DIR, ROWS><<<(unsigned)grid, GroupGeom<NS>::THREADS, GroupGeom<NS>::BYTES, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+cudaError_t group_prepare_t() {
+  return cudaFuncSetAttribute(fft_group_kernel<NS, LIN, LOUT, DIR, ROWS>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, GroupGeom<NS>::BYTES);
+}
+
+// shape: 0 = (interleaved -> interleaved, columns), 1 = (split -> interleaved, columns),
+//        2 = (interleaved -> interleaved, rows),    3 = (interleaved -> split, rows)
+template <int NS, int DIR>
+cudaError_t group_launch_ns(int shape, const GroupArgs &a, int64_t grid, cudaStream_t s) {
+  switch (shape) {
+  case 0: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, false>(a, grid, s);
+  case 1: return group_launch_t<NS, LAYOUT_SPLIT, LAYOUT_INTERLEAVED, DIR, false>(a, grid, s);
+  case 2: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, true>(a, grid, s);
+  case 3: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SPLIT, DIR, true>(a, grid, s);
+  default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int NS, int DIR>
+cudaError_t group_prepare_ns() {
+  cudaError_t e;
+  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, false>()) != cudaSuccess) return e;
+  if ((e = group_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_INTERLEAVED, DIR, false>()) != cudaSuccess) return e;
+  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, true>()) != cudaSuccess) return e;
+  return group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SPLIT, DIR, true>();
+}
+
+#define FFTGEN_GROUP_INSTANCES(SUFFIX, DIR)                                                          \
+  cudaError_t group_launch_##SUFFIX(int log2ns, int shape, const GroupArgs &a, int64_t grid,        \
+                                    cudaStream_t s) {                                               \
+    switch (log2ns) {                                                                               \
+    case 6: return group_launch_ns<64, DIR>(shape, a, grid, s);                                     \
+    case 7: return group_launch_ns<128, DIR>(shape, a, grid, s);                                    \
+    case 8: return group_launch_ns<256, DIR>(shape, a, grid, s);                                    \
+    case 9: return group_launch_ns<512, DIR>(shape, a, grid, s);                                    \
+    case 10: return group_launch_ns<1024, DIR>(shape, a, grid, s);                                  \
+    default: return cudaErrorInvalidValue;                                                          \
+    }                                                                                               \
+  }                                                                                                 \
+  cudaError_t group_prepare_##SUFFIX(int log2ns) {                                                  \
+    switch (log2ns) {                                                                               \
+    case 6: return group_prepare_ns<64, DIR>();                                                     \
+    case 7: return group_prepare_ns<128, DIR>();                                                    \
+    case 8: return group_prepare_ns<256, DIR>();                                                    \
+    case 9: return group_prepare_ns<512, DIR>();                                                    \
+    case 10: return group_prepare_ns<1024, DIR>();                                                  \
+    default: return cudaErrorInvalidValue;                                                          \
+    }                                                                                               \
+  }
+
+}  // namespace fftgen_b200

@@ -32,6 +32,30 @@ int block_tma_transforms_per_cta(int log2n);
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem);
 void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);
 
+// Arguments of the K3 group kernel (fft_group.cuh): one radix-NS Stockham
+// stage of the whole transform with global (cols, k).
+struct GroupArgs {
+  const void *in0;
+  const void *in1;
+  void *out0;
+  void *out1;
+  int64_t cols, k;         // global Stockham parameters of the group
+  int64_t idist, odist;    // elements between consecutive transforms
+  int64_t tiles_per_outer; // CTAs per transform
+  const float2 *tw_local;  // NS-point block-plan pass tables
+  const float2 *tw_q;      // [A0][m] = w_s^{A0 (NS/R0) m}   (cols > 1)
+  const float2 *tw_p;      // [c][m]  = w_s^{c m}
+};
+
+// shape: 0 interleaved->interleaved columns, 1 split->interleaved columns,
+//        2 interleaved->interleaved rows,    3 interleaved->split rows
+cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);
+cudaError_t group_prepare(int log2ns);
+void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
+
+// K4: out[x*cols + m] = w_s^{x*row_scale*m}, fp64-accurate, rounded to fp32
+cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_scale, int64_t s, cudaStream_t st);
+
 cudaError_t convert_f64_to_f32(const double *in, float *out, int64_t count, cudaStream_t s);
 cudaError_t convert_f32_to_f64(const float *in, double *out, int64_t count, cudaStream_t s);
 cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, int64_t istride,

@@ -129,3 +129,62 @@ cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, i
 }
 
 }  // namespace fftgen_b200
+
+// ---- K3 group kernels ------------------------------------------------------
+#include "fft_group.cuh"
+
+namespace fftgen_b200 {
+
+cudaError_t group_launch_f(int, int, const GroupArgs &, int64_t, cudaStream_t);
+cudaError_t group_launch_b(int, int, const GroupArgs &, int64_t, cudaStream_t);
+cudaError_t group_prepare_f(int);
+cudaError_t group_prepare_b(int);
+
+cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s) {
+  const int64_t grid = batch * a.tiles_per_outer;
+  return dir < 0 ? group_launch_f(log2ns, shape, a, grid, s) : group_launch_b(log2ns, shape, a, grid, s);
+}
+
+cudaError_t group_prepare(int log2ns) {
+  cudaError_t e = group_prepare_f(log2ns);
+  return e != cudaSuccess ? e : group_prepare_b(log2ns);
+}
+
+}  // namespace fftgen_b200
+
+// ---- K4: device twiddle-table generation -----------------------------------
+namespace fftgen_b200 {
+
+// out[x * cols + m] = w_s^{x * row_scale * m}, computed in fp64 (sincospi of an
+// exact argument, exact at quadrant multiples like unit_root, matrix.cpp:14-35)
+// and rounded once to fp32.
+__global__ void gen_twiddles_kernel(float2 *__restrict__ out, int64_t rows, int64_t cols, int64_t row_scale,
+                                    int64_t s) {
+  const int64_t total = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = i / cols, m = i - x * cols;
+    const int64_t e = (x * row_scale % s) * m % s;
+    float2 w;
+    if ((4 * e) % s == 0) {
+      const int q = (int)(4 * e / s);
+      w = q == 0 ? make_float2(1.f, 0.f) : q == 1 ? make_float2(0.f, -1.f) : q == 2 ? make_float2(-1.f, 0.f)
+                                                                                     : make_float2(0.f, 1.f);
+    } else {
+      double sn, cs;
+      sincospi(-2.0 * (double)e / (double)s, &sn, &cs);
+      w = make_float2((float)cs, (float)sn);
+    }
+    out[i] = w;
+  }
+}
+
+cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_scale, int64_t s, cudaStream_t st) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  gen_twiddles_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, rows, cols, row_scale, s);
+  return cudaGetLastError();
+}
+
+}  // namespace fftgen_b200

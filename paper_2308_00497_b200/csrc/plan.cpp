@@ -177,8 +177,57 @@ ExecPlan build_exec_plan(int64_t n) {
     p.tw_block = block_twiddles(p.log2n);
     return p;
   }
-  throw PlanError("size 2^" + std::to_string(p.log2n) +
-                  " exceeds the single-CTA path (2^14); four-step not built in this build");
+  if (p.log2n > 30)
+    throw PlanError("size 2^" + std::to_string(p.log2n) + " exceeds the single-GPU limit 2^30");
+  // K3 four-step: groups of consecutive Stockham stages, each one kernel
+  p.strategy = STRAT_FOURSTEP;
+  const std::vector<int> split = group_split(p.log2n);
+  int64_t s = 1;
+  std::vector<int> seen_local;
+  for (size_t g = 0; g < split.size(); ++g) {
+    GroupDesc d;
+    d.log2ns = split[g];
+    d.ns = int64_t(1) << d.log2ns;
+    d.cols = s;
+    s *= d.ns;
+    d.s = s;
+    d.k = n / s;
+    d.rows = g + 1 == split.size();
+    int64_t threads, smem;
+    group_geom(d.log2ns, &threads, &d.tc, &smem, &d.r0);
+    if (d.tc == 0) throw PlanError("no group kernel for 2^" + std::to_string(d.log2ns));
+    // local NS-point pass tables, shared by groups of the same NS
+    bool found = false;
+    for (const GroupDesc &e : p.groups)
+      if (e.log2ns == d.log2ns) {
+        d.local_off = e.local_off;
+        found = true;
+      }
+    if (!found) {
+      d.local_off = (int64_t)p.tw_block.size() / 2;
+      const auto t = block_twiddles(d.log2ns);
+      p.tw_block.insert(p.tw_block.end(), t.begin(), t.end());
+    }
+    if (d.cols > 1) {
+      d.q_off = p.tw_group_len;
+      p.tw_group_len += d.r0 * d.cols;
+      d.p_off = p.tw_group_len;
+      p.tw_group_len += (d.ns / d.r0) * d.cols;
+    }
+    p.passes.push_back(PassDesc{d.ns, d.cols, d.k, d.s});
+    p.groups.push_back(d);
+  }
+  p.scratch_buffers = split.size() >= 3 ? 2 : 1;
+  return p;
+}
+
+std::vector<int> group_split(int log2n) {
+  // 2 groups up to 2^20 (NS <= 2^10), 3 groups up to 2^27 (NS <= 2^9),
+  // 4 groups up to 2^30; sizes as even as possible, larger ones last
+  int g = log2n <= 20 ? 2 : (log2n <= 27 ? 3 : 4);
+  std::vector<int> out(g, log2n / g);
+  for (int i = 0; i < log2n % g; ++i) out[g - 1 - i] += 1;
+  return out;
 }
 
 }  // namespace fftgen_b200

@@ -51,20 +51,35 @@ struct PassDesc {
 
 enum Strategy { STRAT_IDENTITY = 0, STRAT_BLOCK = 1, STRAT_FOURSTEP = 2 };
 
+// One K3 group (fft_group.cuh): a radix-NS Stockham stage of the whole
+// transform with global (cols, k); `rows` for the last group (k == 1).
+struct GroupDesc {
+  int log2ns = 0;
+  int64_t ns = 0, cols = 0, k = 0, s = 0;
+  int64_t r0 = 0;           // first pass radix of the NS-point sub-FFT
+  int64_t tc = 0;           // transforms per CTA tile
+  bool rows = false;
+  int64_t local_off = 0;    // float2 offset of the NS-point pass tables
+  int64_t q_off = 0, p_off = 0;  // float2 offsets of Q[A0][m], P[c][m] (cols > 1)
+};
+
 struct ExecPlan {
   int64_t n = 0;
   Strategy strategy = STRAT_BLOCK;
   int log2n = 0;
-  // four-step: N = n1 * n2, column FFTs of size n1 (stride n2) then row FFTs
-  // of size n2 with the w_N^{e q} pre-twiddle and an n1-strided store.
-  int64_t n1 = 0, n2 = 0;
   std::vector<PassDesc> passes;
   // host copies of the fp32 twiddle tables (uploaded by the C ABI)
-  std::vector<float> tw_block;      // K2 pass tables of the single kernel / of n2
-  std::vector<float> tw_block_n1;   // K2 pass tables of the n1 column kernel
-  std::vector<float> tw_lo, tw_hi;  // four-step w_N^e = hi[e >> b] * lo[e & (2^b - 1)]
-  int tw_lo_bits = 0;
+  std::vector<float> tw_block;   // K2 pass tables of the single kernel / per-NS group tables
+  // K3: groups and the device-generated Q/P table size (float2 count)
+  std::vector<GroupDesc> groups;
+  int64_t tw_group_len = 0;
+  int scratch_buffers = 0;       // intermediate N-element buffers per transform
 };
+
+// The group split of log2 N used by the four-step path (2..4 groups of
+// 2^6..2^10 points).
+std::vector<int> group_split(int log2n);
+void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
 ExecPlan build_exec_plan(int64_t n);
 

@@ -1,0 +1,152 @@
+"""GPU parity of the K3 four-step path (2^15 <= N <= 2^30) vs the CPU oracle.
+
+Same contract as tests/test_gpu_parity.py: fp32-rounded seeded inputs, the
+pinned fp64 oracle (oracle/fftgen_oracle.c) on the same values, relative L2
+<= 1e-5 log2 N per transform.  At sizes where a full oracle transform is too
+slow, size-independent properties are used instead: single tones and
+delta (analytic), sampled bins of the O(N)-per-bin dft_oracle restatement,
+Parseval, and the inverse(forward) round trip.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fg():
+    assert torch.cuda.is_available()
+    import paper_2308_00497_b200 as m
+    return m
+
+
+def tol(n):
+    return 1e-5 * math.log2(n)
+
+
+def seeded_batch(orc, n, batch, seed0=1):
+    x = np.stack([orc.seeded_input(n, seed0 + b) for b in range(batch)])
+    return x.astype(np.float32).astype(np.float64)
+
+
+def run(fg, n, layout, direction, x):
+    batch = x.shape[0]
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, algorithm="stockham"))
+    if layout == "interleaved":
+        src = torch.from_numpy(x.astype(np.float32)).cuda()
+        dst = torch.full_like(src, float("nan"))
+        plan.execute(src, dst, direction=direction)
+        torch.cuda.synchronize()
+        return dst.double().cpu().numpy()
+    re = torch.from_numpy(np.ascontiguousarray(x[:, 0::2]).astype(np.float32)).cuda()
+    im = torch.from_numpy(np.ascontiguousarray(x[:, 1::2]).astype(np.float32)).cuda()
+    ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+    plan.execute(re, ore, im, oim, direction=direction)
+    torch.cuda.synchronize()
+    out = np.empty_like(x)
+    out[:, 0::2] = ore.double().cpu().numpy()
+    out[:, 1::2] = oim.double().cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+@pytest.mark.parametrize("direction", [-1, 1])
+@pytest.mark.parametrize("l2", [15, 16, 17, 18, 19, 20])
+def test_fourstep_matches_oracle(fg, orc, l2, layout, direction):
+    n = 1 << l2
+    batch = 3 if l2 <= 17 else 1
+    x = seeded_batch(orc, n, batch)
+    got = run(fg, n, layout, direction, x)
+    want = orc.forward(x, "stockham", 4, inverse=direction > 0, threads=4)
+    for b in range(batch):
+        err = oracle.rel_l2(got[b], want[b])
+        assert err <= tol(n) and err < 3e-6, (n, b, err)
+
+
+@pytest.mark.parametrize("l2", [21, 22, 24])
+def test_three_group_sizes_vs_oracle(fg, orc, l2):
+    n = 1 << l2
+    x = seeded_batch(orc, n, 1, seed0=5)
+    got = run(fg, n, "split", -1, x)
+    want = orc.forward(x, "stockham", 4)
+    err = oracle.rel_l2(got[0], want[0])
+    assert err <= tol(n) and err < 4e-6, err
+
+
+def test_fourstep_plan_shape(fg):
+    p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 24, layout="split", batch=1))
+    assert [d[0] for d in p.passes()] == [256, 256, 256]
+    assert p.launches() == 3
+    assert p.scratch_bytes() == 2 * (1 << 24) * 8
+    assert "transposed store" in p.describe()
+    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, batch=4))
+    assert [d[0] for d in q.passes()] == [256, 256] and q.scratch_bytes() == 4 * (1 << 16) * 8
+
+
+def test_fourstep_host_and_interpret_paths(fg, orc):
+    n, batch = 1 << 15, 5
+    x = seeded_batch(orc, n, batch)
+    want = orc.forward(x, "stockham", 4, threads=4)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="split", batch=batch))
+    re = np.ascontiguousarray(x[:, 0::2].astype(np.float32))
+    im = np.ascontiguousarray(x[:, 1::2].astype(np.float32))
+    ore, oim = np.empty_like(re), np.empty_like(im)
+    plan.execute_host(re, ore, im, oim)
+    got = np.empty_like(x)
+    got[:, 0::2], got[:, 1::2] = ore, oim
+    for b in range(batch):
+        assert oracle.rel_l2(got[b], want[b]) < 3e-6
+    y = fg.interpret(plan, oracle.relayout_to_split(x))
+    assert oracle.rel_l2(oracle.split_to_interleaved(y), want) < 3e-6
+
+
+@pytest.mark.parametrize("l2", [26, 30])
+def test_huge_single_transform_tones(fg, l2):
+    """N = 2^26 .. 2^30: x = e^{2 pi i k1 n/N} + 0.5 e^{-2 pi i k2 n/N}
+    -> X = N delta[k - k1] + N/2 delta[k + k2] (forward), exact analytic answer."""
+    n = 1 << l2
+    k1, k2 = 12345, 987654 % n
+    idx = torch.arange(n, device="cuda", dtype=torch.int64)
+    ph1 = ((idx * k1) % n).double() * (2 * math.pi / n)
+    ph2 = ((idx * k2) % n).double() * (-2 * math.pi / n)
+    re = (torch.cos(ph1) + 0.5 * torch.cos(ph2)).float()
+    im = (torch.sin(ph1) + 0.5 * torch.sin(ph2)).float()
+    del idx, ph1, ph2
+    ore, oim = torch.empty_like(re), torch.empty_like(im)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="split", batch=1))
+    plan.execute(re, ore, im, oim)
+    torch.cuda.synchronize()
+    ore[k1] -= n
+    ore[(n - k2) % n] -= n / 2
+    err = torch.sqrt((ore.double() ** 2 + oim.double() ** 2).max()).item() / n
+    assert err < 1e-5, err
+    plan.close()
+
+
+def test_2p26_random_sampled_bins_and_roundtrip(fg, orc):
+    n = 1 << 26
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.rand(n, 2, device="cuda", generator=g) * 2 - 1).contiguous()
+    y = torch.empty_like(x)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=1))
+    plan.execute(x, y)
+    z = torch.empty_like(x)
+    plan.execute(y, z, direction=fg.INVERSE)
+    torch.cuda.synchronize()
+    assert torch.linalg.norm((z / n - x).double()) / torch.linalg.norm(x.double()) < 1e-6
+    # Parseval
+    ex = (x.double() ** 2).sum()
+    ey = (y.double() ** 2).sum()
+    assert abs(ey / (n * ex) - 1) < 1e-6
+    # sampled bins of the O(N)-per-bin oracle restatement
+    xh = x.reshape(-1).double().cpu().numpy()
+    bins = [0, 1, 777, n // 2, n - 1]
+    want = orc.dft_bins(xh, bins)
+    got = np.concatenate([y[b].double().cpu().numpy() for b in bins])
+    scale = math.sqrt(n)  # typical |X| for unit-variance random input
+    assert np.abs(got - want).max() / scale < 1e-4

@@ -128,6 +128,42 @@ def test_exec_plan_passes_cover_all_sizes(plan_tool):
         assert prod == 1 << l2
 
 
+def test_fourstep_groups_cover_large_sizes(plan_tool):
+    """K3 groups: each a radix-NS Stockham stage with cols = prior product,
+    k = N / s; inner groups need k >= tile, the last group has k == 1."""
+    for l2 in range(15, 31):
+        rc, out, err = plan_tool("passes", 1 << l2)
+        assert rc == 0, err
+        groups = [tuple(int(v) for v in ln.split()) for ln in out.splitlines()]
+        assert 2 <= len(groups) <= 4
+        prod = 1
+        for R, cols, k, s in groups:
+            assert 64 <= R <= 1024 and cols == prod and s == R * cols and k * s == 1 << l2
+            prod *= R
+        assert prod == 1 << l2 and groups[-1][2] == 1
+    assert plan_tool("passes", 1 << 31)[0] == 1  # PlanError above 2^30
+
+
+def test_fourstep_regrouping_restated_matches_oracle(plan_tool, orc):
+    for n in (1 << 15, 1 << 16):
+        rc, out, _ = plan_tool("passes", n)
+        groups = [tuple(int(v) for v in ln.split()) for ln in out.splitlines()]
+        x = orc.seeded_input(n, 3)
+        z = oracle.as_complex(x)
+        for R, cols, k, s in groups:
+            # vectorised radix-R Stockham stage over the whole transform
+            m = np.arange(cols)[:, None, None]
+            A = np.arange(R)[None, :, None]
+            c = np.arange(k)[None, None, :]
+            v = z[(m * R + A) * k + c] * np.exp(-2j * np.pi * A * m / s)
+            V = np.fft.fft(v, axis=1)
+            y = np.empty_like(z)
+            y[(A * cols + m) * k + c] = V
+            z = y
+        want = oracle.as_complex(orc.forward(x, "stockham", 4))
+        assert np.abs(z - want).max() / np.abs(want).max() < 1e-12
+
+
 def test_butterfly_constants_are_unit_root_fp32(orc):
     text = open(os.path.join(CSRC, "roots64.cuh")).read()
     def arr(name):
