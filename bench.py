@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON)")
+    ap.add_argument("--workload", choices=["batched", "distributed"], default="batched",
+                    help="distributed: one N-point transform over all ranks (config C5, e.g. --n 1073741824)")
     return ap.parse_args()
 
 
@@ -328,10 +330,61 @@ def run_reference(a):
     return line
 
 
+def run_distributed(a):
+    """Config C5: one N-point transform block-distributed over all ranks,
+    three NCCL all-to-alls (paper_2308_00497_b200.distributed)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2308_00497_b200.distributed import DistributedFFT
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world)
+    dev = torch.device("cuda", local)
+    n = a.n
+    m = n // world
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    x = torch.complex(torch.rand(m, device=dev, generator=g) * 2 - 1, torch.rand(m, device=dev, generator=g) * 2 - 1)
+    d = DistributedFFT(n, device=local)
+    for _ in range(a.warmup):
+        y = d.execute(x)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        s.record()
+        for _ in range(a.steps):
+            y = d.execute(x)
+        e.record()
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    t = torch.tensor([s.elapsed_time(e) / a.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    del y
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": round(gflop(n, 1) / (ms / 1e3), 2), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: uniform [-1,1) re/im on device", "impl": "ours",
+            "config": {"workload": f"single c2c fp32 FFT N={n} distributed over {world} GPU(s), "
+                                   f"{d.n1}x{d.n2} four-step, 3 all-to-alls", "n": n, "n1": d.n1, "n2": d.n2},
+            "clocks": clk.summary()}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "distributed":
+        run_distributed(a)
     else:
         run_ours(a)
 

@@ -110,6 +110,15 @@ fftgen_status fftgen_execute_host(const fftgen_plan *plan, int direction,
 fftgen_status fftgen_interpret_f64(const fftgen_plan *plan, int direction,
                                    const double *in, double *out);
 
+/* Distributed four-step helper (the twiddle diagonal D^N of Eq. 1,
+ * formula.hpp:44-49, applied to one rank's block): for an interleaved fp32
+ * block of `rows` x `cols` complex values with leading dimension `ld`,
+ *   data[r*ld + c] *= w_n^{(row_offset + r) * (col_offset + c)}
+ * (w_n = exp(-2 pi i / n); conjugated for FFTGEN_INVERSE), twiddles
+ * computed in fp64 on the device, exact at quadrant multiples. */
+fftgen_status fftgen_twiddle_multiply(int direction, void *data, int64_t rows, int64_t cols, int64_t ld,
+                                      int64_t row_offset, int64_t col_offset, int64_t n, void *stream);
+
 const char *fftgen_error_string(fftgen_status status);
 /* Detail message of the most recent failure on the calling thread. */
 const char *fftgen_last_error(void);

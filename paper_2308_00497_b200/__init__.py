@@ -43,6 +43,7 @@ ABI_SYMBOLS = (
     "fftgen_abi_version", "fftgen_plan_radices", "fftgen_plan_num_ops", "fftgen_plan_op",
     "fftgen_plan_op_map", "fftgen_plan_pipeline_text", "fftgen_plan_num_passes", "fftgen_plan_pass",
     "fftgen_plan_describe", "fftgen_plan_launches", "fftgen_plan_scratch_bytes",
+    "fftgen_twiddle_multiply",
 )
 
 
@@ -109,6 +110,7 @@ def _load() -> C.CDLL:
     L.fftgen_plan_launches.argtypes = [vp]
     L.fftgen_plan_scratch_bytes.argtypes = [vp]
     L.fftgen_plan_scratch_bytes.restype = C.c_size_t
+    L.fftgen_twiddle_multiply.argtypes = [C.c_int, vp, i64, i64, i64, i64, i64, i64, vp]
     return L
 
 
@@ -270,6 +272,20 @@ def compile_pipeline(cfg: PipelineConfig) -> Plan:
 def interpret(plan: Plan, x: np.ndarray, direction: int = FORWARD) -> np.ndarray:
     """interpret(final_ir, ComplexBuffer) analogue on fp64 reference storage."""
     return plan.interpret(x, direction)
+
+
+def twiddle_multiply(block, row_offset: int, col_offset: int, n: int, direction: int = FORWARD,
+                     stream=None) -> None:
+    """In place on a CUDA complex64 (rows, cols) block (or float32 (rows, cols, 2)):
+    block[r, c] *= w_n^{(row_offset + r)(col_offset + c)} -- the four-step
+    twiddle diagonal D^N (formula.hpp:44-49) on one rank's block."""
+    rows, cols = block.shape[0], block.shape[1]
+    ld = block.stride(0) if block.dtype.is_complex else block.stride(0) // 2
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream(block.device).cuda_stream
+    _check(lib.fftgen_twiddle_multiply(direction, _ptr(block), rows, cols, ld, row_offset, col_offset, n,
+                                       int(stream)))
 
 
 def flops(n: int, batch: int = 1) -> float:

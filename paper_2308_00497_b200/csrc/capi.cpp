@@ -529,3 +529,15 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
 }
 
 }  // extern "C"
+
+extern "C" fftgen_status fftgen_twiddle_multiply(int direction, void *data, int64_t rows, int64_t cols, int64_t ld,
+                                                 int64_t row_offset, int64_t col_offset, int64_t n, void *stream) {
+  if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
+    return fail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
+  if (!data) return fail(FFTGEN_ERR_EXEC, "NULL data pointer");
+  if (rows < 0 || cols < 0 || ld < cols || n < 1 || row_offset < 0 || col_offset < 0)
+    return fail(FFTGEN_ERR_DIMENSION, "bad twiddle block geometry");
+  cudaError_t e = twiddle_block((float2 *)data, rows, cols, ld, row_offset, col_offset, n, direction,
+                                (cudaStream_t)stream);
+  return e == cudaSuccess ? FFTGEN_OK : cuda_fail(e, "twiddle kernel");
+}

@@ -56,6 +56,10 @@ void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_
 // K4: out[x*cols + m] = w_s^{x*row_scale*m}, fp64-accurate, rounded to fp32
 cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_scale, int64_t s, cudaStream_t st);
 
+// distributed four-step twiddle diagonal on a local (rows x cols, ld) block
+cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, int64_t row_offset,
+                          int64_t col_offset, int64_t n, int dir, cudaStream_t s);
+
 cudaError_t convert_f64_to_f32(const double *in, float *out, int64_t count, cudaStream_t s);
 cudaError_t convert_f32_to_f64(const float *in, double *out, int64_t count, cudaStream_t s);
 cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, int64_t istride,

@@ -188,3 +188,44 @@ cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_sc
 }
 
 }  // namespace fftgen_b200
+
+// ---- distributed four-step: twiddle diagonal on a local block --------------
+namespace fftgen_b200 {
+
+// data[r * ld + c] *= w_n^{(row_offset + r) (col_offset + c)}  (conj for DIR > 0)
+__global__ void twiddle_block_kernel(float2 *__restrict__ data, int64_t rows, int64_t cols, int64_t ld,
+                                     int64_t row_offset, int64_t col_offset, int64_t n, int dir) {
+  const int64_t total = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const unsigned __int128 prod = (unsigned __int128)(row_offset + r) * (unsigned __int128)(col_offset + c);
+    const int64_t e = (int64_t)(prod % (unsigned __int128)n);
+    float wr, wi;
+    if ((4 * e) % n == 0) {
+      const int q = (int)(4 * e / n);
+      wr = q == 0 ? 1.f : (q == 2 ? -1.f : 0.f);
+      wi = q == 1 ? -1.f : (q == 3 ? 1.f : 0.f);
+    } else {
+      double sn, cs;
+      sincospi(-2.0 * (double)e / (double)n, &sn, &cs);
+      wr = (float)cs;
+      wi = (float)sn;
+    }
+    if (dir > 0) wi = -wi;
+    float2 *p = data + r * ld + c;
+    const float2 x = *p;
+    *p = make_float2(x.x * wr - x.y * wi, fmaf(x.x, wi, x.y * wr));
+  }
+}
+
+cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, int64_t row_offset,
+                          int64_t col_offset, int64_t n, int dir, cudaStream_t s) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  twiddle_block_kernel<<<(unsigned)blocks, 256, 0, s>>>(data, rows, cols, ld, row_offset, col_offset, n, dir);
+  return cudaGetLastError();
+}
+
+}  // namespace fftgen_b200
