@@ -76,6 +76,11 @@ struct fftgen_plan {
   float2 *d_twg = nullptr;
   float2 *d_scratch = nullptr;
   size_t scratch_bytes = 0;
+  // L2-resident chunked execution of 2-group plans (0 = off)
+  int64_t chunk = 0;
+  cudaStream_t xs[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_a[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr},
+              ev_join[2] = {nullptr, nullptr};
   // host-buffer pipeline scratch (lazily allocated, guarded by mu)
   std::mutex mu;
   void *d_stage = nullptr;
@@ -101,6 +106,30 @@ fftgen_status validate_exec(const fftgen_plan *p, int direction, const void *in0
     return fail(FFTGEN_ERR_DIMENSION, "dist " + std::to_string(dist) + " is smaller than n " +
                                           std::to_string(p->cfg.n));
   return FFTGEN_OK;
+}
+
+// One K3 group launch: the first group reads the user layout, the last writes
+// it, intermediates are interleaved scratch.
+cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void *in0, const void *in1,
+                         void *out0, void *out1, int64_t idist, int64_t odist, int64_t batch, cudaStream_t s) {
+  const GroupDesc &d = p->ex.groups[g];
+  const bool first = g == 0, last = g + 1 == (int)p->ex.groups.size();
+  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+  GroupArgs a{};
+  a.in0 = in0;
+  a.in1 = in1;
+  a.out0 = out0;
+  a.out1 = out1;
+  a.cols = d.cols;
+  a.k = d.k;
+  a.idist = idist;
+  a.odist = odist;
+  a.tiles_per_outer = (d.cols * d.k) / d.tc;
+  a.tw_local = p->d_tw + d.local_off;
+  a.tw_q = d.cols > 1 ? p->d_twg + d.q_off : nullptr;
+  a.tw_p = d.cols > 1 ? p->d_twg + d.p_off : nullptr;
+  const int shape = last ? (split ? 3 : 2) : (first && split ? 1 : 0);
+  return group_launch(d.log2ns, shape, direction, a, batch, s);
 }
 
 // Enqueue one execute over `batch` transforms on stream s (device pointers).
@@ -141,30 +170,49 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
   case STRAT_FOURSTEP: {
-    // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
     const auto &gs = p->ex.groups;
+    const bool split = layout == FFTGEN_LAYOUT_SPLIT;
+    if (gs.size() == 2 && p->chunk > 0 && batch >= 2 * p->chunk) {
+      // L2-resident chunking: group 0 of chunk c on xs[0], group 1 on xs[1];
+      // the intermediate of a chunk (<= 2 slots live) is read back from L2.
+      cudaError_t e;
+      if ((e = cudaEventRecord(p->ev_fork, s)) != cudaSuccess) return e;
+      for (auto &x : p->xs)
+        if ((e = cudaStreamWaitEvent(x, p->ev_fork, 0)) != cudaSuccess) return e;
+      const int64_t esz = split ? 1 : 2;  // floats per element of a user plane
+      int64_t c = 0;
+      for (int64_t b0 = 0; b0 < batch; b0 += p->chunk, ++c) {
+        const int64_t cnt = std::min<int64_t>(p->chunk, batch - b0);
+        const int slot = (int)(c & 1);
+        float2 *buf = p->d_scratch + (size_t)slot * p->chunk * n;
+        if (c >= 2 && (e = cudaStreamWaitEvent(p->xs[0], p->ev_b[slot], 0)) != cudaSuccess) return e;
+        const float *i0 = (const float *)in0 + b0 * dist * esz;
+        const float *i1 = in1 ? (const float *)in1 + b0 * dist : nullptr;
+        if ((e = launch_group(p, 0, direction, i0, i1, buf, nullptr, dist, n, cnt, p->xs[0])) != cudaSuccess)
+          return e;
+        if ((e = cudaEventRecord(p->ev_a[slot], p->xs[0])) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(p->xs[1], p->ev_a[slot], 0)) != cudaSuccess) return e;
+        float *o0 = (float *)out0 + b0 * dist * esz;
+        float *o1 = out1 ? (float *)out1 + b0 * dist : nullptr;
+        if ((e = launch_group(p, 1, direction, buf, nullptr, o0, o1, n, dist, cnt, p->xs[1])) != cudaSuccess)
+          return e;
+        if ((e = cudaEventRecord(p->ev_b[slot], p->xs[1])) != cudaSuccess) return e;
+      }
+      for (int i = 0; i < 2; ++i) {
+        if ((e = cudaEventRecord(p->ev_join[i], p->xs[i])) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s, p->ev_join[i], 0)) != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+    // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
     const size_t per = (size_t)p->cfg.batch * (size_t)n;  // float2 per scratch buffer
     for (size_t g = 0; g < gs.size(); ++g) {
-      const GroupDesc &d = gs[g];
       const bool first = g == 0, last = g + 1 == gs.size();
       float2 *src = first ? nullptr : p->d_scratch + ((g - 1) % p->ex.scratch_buffers) * per;
       float2 *dst = last ? nullptr : p->d_scratch + (g % p->ex.scratch_buffers) * per;
-      GroupArgs a{};
-      a.in0 = first ? in0 : src;
-      a.in1 = first ? in1 : nullptr;
-      a.out0 = last ? out0 : dst;
-      a.out1 = last ? out1 : nullptr;
-      a.cols = d.cols;
-      a.k = d.k;
-      a.idist = first ? dist : n;
-      a.odist = last ? dist : n;
-      a.tiles_per_outer = (d.cols * d.k) / d.tc;
-      a.tw_local = p->d_tw + d.local_off;
-      a.tw_q = d.cols > 1 ? p->d_twg + d.q_off : nullptr;
-      a.tw_p = d.cols > 1 ? p->d_twg + d.p_off : nullptr;
-      const bool split = layout == FFTGEN_LAYOUT_SPLIT;
-      const int shape = last ? (split ? 3 : 2) : (first && split ? 1 : 0);
-      cudaError_t e = group_launch(d.log2ns, shape, direction, a, batch, s);
+      cudaError_t e = launch_group(p, (int)g, direction, first ? in0 : src, first ? in1 : nullptr,
+                                   last ? out0 : dst, last ? out1 : nullptr, first ? dist : n, last ? dist : n,
+                                   batch, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -308,6 +356,25 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
             return bail(FFTGEN_ERR_CUDA, std::string("twiddle generation: ") + cudaGetErrorString(e));
         }
       }
+      if (p->ex.groups.size() == 2) {
+        // chunk of ~L2/4 of intermediate per slot; two slots live in L2
+        int64_t chunk_bytes = int64_t(32) << 20;
+        if (const char *env = std::getenv("FFTGEN_L2_CHUNK_BYTES")) chunk_bytes = std::atoll(env);
+        const int64_t per_tf = cfg->n * (int64_t)sizeof(float2);
+        p->chunk = chunk_bytes > 0 ? std::max<int64_t>(1, chunk_bytes / per_tf) : 0;
+        if (p->chunk > 0 && cfg->batch >= 2 * p->chunk) {
+          for (auto &x : p->xs)
+            if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess)
+              return bail(FFTGEN_ERR_CUDA, "stream creation");
+          cudaEvent_t *evs[] = {&p->ev_fork, &p->ev_a[0], &p->ev_a[1], &p->ev_b[0], &p->ev_b[1],
+                                &p->ev_join[0], &p->ev_join[1]};
+          for (cudaEvent_t *ev : evs)
+            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
+              return bail(FFTGEN_ERR_CUDA, "event creation");
+        } else {
+          p->chunk = 0;
+        }
+      }
       p->scratch_bytes = (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n * sizeof(float2);
       if ((e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
@@ -334,6 +401,10 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    for (auto &x : p->xs)
+      if (x) cudaStreamDestroy(x);
+    for (cudaEvent_t ev : {p->ev_fork, p->ev_a[0], p->ev_a[1], p->ev_b[0], p->ev_b[1], p->ev_join[0], p->ev_join[1]})
+      if (ev) cudaEventDestroy(ev);
     if (p->d_stage) cudaFree(p->d_stage);
     for (auto &s : p->streams)
       if (s) cudaStreamDestroy(s);

@@ -74,17 +74,30 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
   const int64_t ib = b * a.idist, ob = b * a.odist;
 
   // ---- cooperative, coalesced tile load (HBM -> smem) --------------------
-  if (ROWS) {  // k == 1: transform f is the contiguous row m0 + f
-#pragma unroll 4
-    for (int i = tid; i < TC * NS; i += THREADS) {
-      const int f = i / NS, A = i % NS;
-      stage[f * REG + A] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 + f) * NS + A);
+  // All ITER loads of a thread are issued before the first shared store so
+  // each thread keeps ITER independent HBM requests in flight.
+  constexpr int ITER = TC * NS / THREADS;
+  static_assert(ITER * THREADS == TC * NS, "tile must divide evenly");
+  {
+    float2 ld[ITER];
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int i = tid + it * THREADS;
+      if (ROWS) {  // k == 1: transform f is the contiguous row m0 + f
+        const int f = i / NS, A = i % NS;
+        ld[it] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 + f) * NS + A);
+      } else {     // columns: element A of transform f at (m0 NS + A) k + c0 + f
+        const int f = i % TC, A = i / TC;
+        ld[it] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 * NS + A) * a.k + c0 + f);
+      }
     }
-  } else {     // columns: element A of transform f at (m0 NS + A) k + c0 + f
-#pragma unroll 4
-    for (int i = tid; i < TC * NS; i += THREADS) {
-      const int f = i % TC, A = i / TC;
-      stage[f * REG + A] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 * NS + A) * a.k + c0 + f);
+#pragma unroll
+    for (int it = 0; it < ITER; ++it) {
+      const int i = tid + it * THREADS;
+      if (ROWS)
+        stage[(i / NS) * REG + i % NS] = ld[it];
+      else
+        stage[(i % TC) * REG + i / TC] = ld[it];
     }
   }
   __syncthreads();
@@ -138,8 +151,9 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
   __syncthreads();
 
   // ---- cooperative, coalesced tile store (smem -> HBM), lanes over f ------
-#pragma unroll 4
-  for (int i = tid; i < TC * NS; i += THREADS) {
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int i = tid + it * THREADS;
     const int ff = i % TC, B = i / TC;
     const int64_t off = ROWS ? (int64_t)B * a.cols + m0 + ff : ((int64_t)B * a.cols + m0) * a.k + c0 + ff;
     SIO<LOUT>::store(a.out0, a.out1, ob + off, stage[ff * REG + B]);
