@@ -14,15 +14,18 @@
 // A CTA owns a tile of TC transforms that are ADJACENT in memory:
 //   inner groups (k >= TC): same m, consecutive c  -> columns of stride k
 //   last group  (k == 1):   consecutive m          -> contiguous rows
-// The tile is staged through shared memory so that every HBM access covers
-// TC consecutive elements (TC*8 bytes interleaved, TC*4 per split plane):
-//   load:  lanes over c (columns) or over A (rows)
-//   store: lanes over c or m -- the transposed store of the last group
-// In between, the NS-point sub-FFT runs on the block-kernel machinery
-// (registers + padded smem exchange, fft_block.cuh), and the global twiddle
-// w_s^{A m} = w_s^{A0 (NS/R0) m} * w_s^{c m} (A = A0 (NS/R0) + c, R0 = the
-// sub-FFT's first pass radix) comes from two fp64-exact fp32 tables
-// Q[A0][m], P[c][m] built at plan time.
+// The NS-point sub-FFT is two register passes with one padded shared-memory
+// exchange (block_geom.hpp).  HBM is read by pass 0 and written by pass 1
+// straight from registers; coalescing comes from the thread mapping, which
+// is chosen per side of the exchange:
+//   columns: lanes over the tile index f on both sides (TC*8-byte segments)
+//   rows:    pass 0 lanes over the row (contiguous loads); pass 1 lanes over
+//            f, so the last group's transposed natural-order store covers TC
+//            consecutive m per segment.
+// The global twiddle w_s^{A m} = w_s^{A0 (NS/R0) m} * w_s^{c m}
+// (A = A0 (NS/R0) + c, R0 = the sub-FFT's first pass radix) comes from two
+// fp64-exact fp32 tables Q[A0][m], P[c][m] (generated on the device at plan
+// time), read once per thread into registers.
 #pragma once
 
 #include <cstdint>
@@ -55,9 +58,12 @@ template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
 __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const GroupArgs a) {
   using GG = GroupGeom<NS>;
   using G = typename GG::G;
-  constexpr int TC = GG::TC, REG = GG::REG, THREADS = GG::THREADS;
+  constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
+  static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == G::R(1), "group sub-FFTs are 2-pass plans");
+  constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
+  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
   extern __shared__ float4 smem_f4[];
-  float2 *stage = reinterpret_cast<float2 *>(smem_f4);
+  float2 *smem = reinterpret_cast<float2 *>(smem_f4);
   const int tid = threadIdx.x;
 
   const int64_t b = blockIdx.x / a.tiles_per_outer;
@@ -73,90 +79,52 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
   }
   const int64_t ib = b * a.idist, ob = b * a.odist;
 
-  // ---- cooperative, coalesced tile load (HBM -> smem) --------------------
-  // All ITER loads of a thread are issued before the first shared store so
-  // each thread keeps ITER independent HBM requests in flight.
-  constexpr int ITER = TC * NS / THREADS;
-  static_assert(ITER * THREADS == TC * NS, "tile must divide evenly");
-  {
-    float2 ld[ITER];
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int i = tid + it * THREADS;
-      if (ROWS) {  // k == 1: transform f is the contiguous row m0 + f
-        const int f = i / NS, A = i % NS;
-        ld[it] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 + f) * NS + A);
-      } else {     // columns: element A of transform f at (m0 NS + A) k + c0 + f
-        const int f = i % TC, A = i / TC;
-        ld[it] = SIO<LIN>::load(a.in0, a.in1, ib + (m0 * NS + A) * a.k + c0 + f);
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < ITER; ++it) {
-      const int i = tid + it * THREADS;
-      if (ROWS)
-        stage[(i / NS) * REG + i % NS] = ld[it];
-      else
-        stage[(i % TC) * REG + i / TC] = ld[it];
-    }
-  }
-  __syncthreads();
-
-  // ---- pass 0 with the global twiddle w_s^{A m}, then the local passes ----
-  const int f = tid / G::T;
-  const int t = tid - f * G::T;
-  const int64_t m = ROWS ? m0 + f : m0;
-  float2 *sx = stage + f * REG;
+  // ---- pass 0: HBM -> registers, global twiddle, radix-R0 codelets --------
   float2 v[G::RMAX];
   {
-    constexpr int R = G::R(0), k = G::K(0), J = G::RMAX / R;
+    const int f = ROWS ? tid / T : tid % TC;
+    const int t = ROWS ? tid % T : tid / TC;
+    const int64_t m = ROWS ? m0 + f : m0;
+    const bool tw = a.cols > 1;
+    float2 q[R0];
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int c = t + j * G::T;
-      float2 pw = make_float2(1.f, 0.f);
-      if (a.cols > 1) pw = __ldg(a.tw_p + c * a.cols + m);
+    for (int A0 = 0; A0 < R0; ++A0) q[A0] = tw && A0 ? __ldg(a.tw_q + A0 * a.cols + m) : make_float2(1.f, 0.f);
 #pragma unroll
-      for (int A0 = 0; A0 < R; ++A0) {
-        float2 x = sx[A0 * k + c];
-        if (a.cols > 1) {
-          x = mul_tw<DIR>(x, pw);
-          if (A0) x = mul_tw<DIR>(x, __ldg(a.tw_q + A0 * a.cols + m));
-        }
-        v[j * R + A0] = x;
+    for (int j = 0; j < J0; ++j) {
+      const int c = t + j * T;
+#pragma unroll
+      for (int A0 = 0; A0 < R0; ++A0) {
+        const int A = A0 * K0 + c;
+        const int64_t off = ROWS ? ib + (m0 + f) * NS + A : ib + (m0 * NS + A) * a.k + c0 + f;
+        v[j * R0 + A0] = SIO<LIN>::load(a.in0, a.in1, off);
       }
-      reg_fft<R, DIR>(v + j * R);
-    }
-  }
-  __syncthreads();  // staged input consumed; the region becomes the exchange
-  if constexpr (G::P == 2) {
-    TwPQ<G> pq;
-    pq.load(a.tw_local, t);
-    smem_write<G, NS, 0>(sx, t, v);
-    __syncthreads();
-    smem_read_pass1_pq<G, NS, DIR>(sx, t, pq, v);
-  } else {
-    middle_passes<G, NS, DIR>(sx, t, a.tw_local, v);
-  }
-  __syncthreads();  // exchange consumed; stage the outputs in natural order
-  {
-    constexpr int q = G::P - 1;
-    constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / R;
+      if (tw) {
+        const float2 pw = __ldg(a.tw_p + c * a.cols + m);
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      const int u = t + j * G::T, mm = u / k, c = u % k;
-#pragma unroll
-      for (int B = 0; B < R; ++B) sx[(B * cols + mm) * k + c] = v[j * R + B];
+        for (int A0 = 0; A0 < R0; ++A0) {
+          float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
+          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, q[A0]) : x;
+        }
+      }
+      reg_fft<R0, DIR>(v + j * R0);
     }
+    smem_write<G, NS, 0>(smem + f * REG, t, v);
   }
   __syncthreads();
 
-  // ---- cooperative, coalesced tile store (smem -> HBM), lanes over f ------
+  // ---- pass 1: smem -> registers (lanes over f), codelet, HBM store ------
+  {
+    const int f = tid % TC;
+    const int t = tid / TC;  // pass-1 butterfly m1 = t (k == 1, J == 1)
+    TwPQ<G> pq;
+    pq.load(a.tw_local, t);
+    smem_read_pass1_pq<G, NS, DIR>(smem + f * REG, t, pq, v);
 #pragma unroll
-  for (int it = 0; it < ITER; ++it) {
-    const int i = tid + it * THREADS;
-    const int ff = i % TC, B = i / TC;
-    const int64_t off = ROWS ? (int64_t)B * a.cols + m0 + ff : ((int64_t)B * a.cols + m0) * a.k + c0 + ff;
-    SIO<LOUT>::store(a.out0, a.out1, ob + off, stage[ff * REG + B]);
+    for (int B = 0; B < R1; ++B) {
+      const int64_t e = B * COLS1 + t;  // local output index
+      const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
+      SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+    }
   }
 }
 
