@@ -81,7 +81,7 @@ void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_
     *smem = GroupGeom<NN>::BYTES;      \
     *r0 = GroupGeom<NN>::R0;           \
     return;
-    FFTGEN_GG(6, 64) FFTGEN_GG(7, 128) FFTGEN_GG(8, 256) FFTGEN_GG(9, 512) FFTGEN_GG(10, 1024)
+    FFTGEN_GG(7, 128) FFTGEN_GG(8, 256) FFTGEN_GG(9, 512) FFTGEN_GG(10, 1024)
 #undef FFTGEN_GG
   default:
     *threads = *tc = *smem = *r0 = 0;

@@ -50,7 +50,6 @@ cudaError_t group_prepare_ns() {
   cudaError_t group_launch_##SUFFIX(int log2ns, int shape, const GroupArgs &a, int64_t grid,        \
                                     cudaStream_t s) {                                               \
     switch (log2ns) {                                                                               \
-    case 6: return group_launch_ns<64, DIR>(shape, a, grid, s);                                     \
     case 7: return group_launch_ns<128, DIR>(shape, a, grid, s);                                    \
     case 8: return group_launch_ns<256, DIR>(shape, a, grid, s);                                    \
     case 9: return group_launch_ns<512, DIR>(shape, a, grid, s);                                    \
@@ -60,7 +59,6 @@ cudaError_t group_prepare_ns() {
   }                                                                                                 \
   cudaError_t group_prepare_##SUFFIX(int log2ns) {                                                  \
     switch (log2ns) {                                                                               \
-    case 6: return group_prepare_ns<64, DIR>();                                                     \
     case 7: return group_prepare_ns<128, DIR>();                                                    \
     case 8: return group_prepare_ns<256, DIR>();                                                    \
     case 9: return group_prepare_ns<512, DIR>();                                                    \
