@@ -177,6 +177,8 @@ template <int NS> struct GroupGeom {
   static constexpr int EX = SmemGeom<NS>::REGION > NS ? SmemGeom<NS>::REGION : NS;
   static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
   static constexpr int BYTES = TC * REG * 8;
+  // resident CTAs the register budget must allow (smem allows 3 at ~66 KB)
+  static constexpr int MIN_BLOCKS = THREADS >= 512 ? 2 : 3;
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };

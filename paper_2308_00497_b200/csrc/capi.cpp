@@ -128,7 +128,7 @@ cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void 
   a.tw_local = p->d_tw + d.local_off;
   a.tw_q = d.cols > 1 ? p->d_twg + d.q_off : nullptr;
   a.tw_p = d.cols > 1 ? p->d_twg + d.p_off : nullptr;
-  const int shape = last ? (split ? 3 : 2) : (first && split ? 1 : 0);
+  const int shape = last ? (split ? 3 : 2) : (first ? (split ? 1 : 0) : 4);
   return group_launch(d.log2ns, shape, direction, a, batch, s);
 }
 

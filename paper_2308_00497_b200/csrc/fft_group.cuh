@@ -34,6 +34,11 @@
 
 namespace fftgen_b200 {
 
+// User buffers stream through L2 (evict-first); interleaved scratch between
+// groups is written with the normal policy and read back as last use, so a
+// chunk's intermediate can be consumed from the 126 MB L2 (LAYOUT_SCRATCH).
+constexpr int LAYOUT_SCRATCH = 2;
+
 template <int L> struct SIO;
 template <> struct SIO<LAYOUT_INTERLEAVED> {
   static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
@@ -41,6 +46,14 @@ template <> struct SIO<LAYOUT_INTERLEAVED> {
   }
   static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
     __stcs(reinterpret_cast<float2 *>(p0) + off, v);
+  }
+};
+template <> struct SIO<LAYOUT_SCRATCH> {
+  static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
+    return __ldlu(reinterpret_cast<const float2 *>(p0) + off);
+  }
+  static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
+    reinterpret_cast<float2 *>(p0)[off] = v;
   }
 };
 template <> struct SIO<LAYOUT_SPLIT> {
@@ -55,7 +68,7 @@ template <> struct SIO<LAYOUT_SPLIT> {
 };
 
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
-__global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const GroupArgs a) {
+__global__ void __launch_bounds__(GroupGeom<NS>::THREADS, GroupGeom<NS>::MIN_BLOCKS) fft_group_kernel(const GroupArgs a) {
   using GG = GroupGeom<NS>;
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
@@ -86,9 +99,8 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
     const int t = ROWS ? tid % T : tid / TC;
     const int64_t m = ROWS ? m0 + f : m0;
     const bool tw = a.cols > 1;
-    float2 q[R0];
-#pragma unroll
-    for (int A0 = 0; A0 < R0; ++A0) q[A0] = tw && A0 ? __ldg(a.tw_q + A0 * a.cols + m) : make_float2(1.f, 0.f);
+    // Q[A0][m]: one address per warp (m is shared by the lanes) -> L1 broadcast
+    const float2 *qm = a.tw_q + m;
 #pragma unroll
     for (int j = 0; j < J0; ++j) {
       const int c = t + j * T;
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
 #pragma unroll
         for (int A0 = 0; A0 < R0; ++A0) {
           float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, q[A0]) : x;
+          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
         }
       }
       reg_fft<R0, DIR>(v + j * R0);
@@ -116,9 +128,8 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS) fft_group_kernel(const
   {
     const int f = tid % TC;
     const int t = tid / TC;  // pass-1 butterfly m1 = t (k == 1, J == 1)
-    TwPQ<G> pq;
-    pq.load(a.tw_local, t);
-    smem_read_pass1_pq<G, NS, DIR>(smem + f * REG, t, pq, v);
+    // local pass-1 twiddles w^{A t}: lanes share t -> L1 broadcast loads
+    smem_read_pass<G, NS, 1, DIR>(smem + f * REG, t, a.tw_local, v);
 #pragma unroll
     for (int B = 0; B < R1; ++B) {
       const int64_t e = B * COLS1 + t;  // local output index

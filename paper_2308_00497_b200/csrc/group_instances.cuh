@@ -24,15 +24,17 @@ cudaError_t group_prepare_t() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, GroupGeom<NS>::BYTES);
 }
 
-// shape: 0 = (interleaved -> interleaved, columns), 1 = (split -> interleaved, columns),
-//        2 = (interleaved -> interleaved, rows),    3 = (interleaved -> split, rows)
+// shape: 0 = (interleaved -> scratch, columns), 1 = (split -> scratch, columns),
+//        2 = (scratch -> interleaved, rows),     3 = (scratch -> split, rows),
+//        4 = (scratch -> scratch, columns)
 template <int NS, int DIR>
 cudaError_t group_launch_ns(int shape, const GroupArgs &a, int64_t grid, cudaStream_t s) {
   switch (shape) {
-  case 0: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, false>(a, grid, s);
-  case 1: return group_launch_t<NS, LAYOUT_SPLIT, LAYOUT_INTERLEAVED, DIR, false>(a, grid, s);
-  case 2: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, true>(a, grid, s);
-  case 3: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SPLIT, DIR, true>(a, grid, s);
+  case 0: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SCRATCH, DIR, false>(a, grid, s);
+  case 1: return group_launch_t<NS, LAYOUT_SPLIT, LAYOUT_SCRATCH, DIR, false>(a, grid, s);
+  case 2: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>(a, grid, s);
+  case 3: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>(a, grid, s);
+  case 4: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>(a, grid, s);
   default: return cudaErrorInvalidValue;
   }
 }
@@ -40,10 +42,11 @@ cudaError_t group_launch_ns(int shape, const GroupArgs &a, int64_t grid, cudaStr
 template <int NS, int DIR>
 cudaError_t group_prepare_ns() {
   cudaError_t e;
-  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, false>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_INTERLEAVED, DIR, false>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_INTERLEAVED, DIR, true>()) != cudaSuccess) return e;
-  return group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SPLIT, DIR, true>();
+  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SCRATCH, DIR, false>()) != cudaSuccess) return e;
+  if ((e = group_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_SCRATCH, DIR, false>()) != cudaSuccess) return e;
+  if ((e = group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>()) != cudaSuccess) return e;
+  if ((e = group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>()) != cudaSuccess) return e;
+  return group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>();
 }
 
 #define FFTGEN_GROUP_INSTANCES(SUFFIX, DIR)                                                          \

@@ -47,8 +47,8 @@ struct GroupArgs {
   const float2 *tw_p;      // [c][m]  = w_s^{c m}
 };
 
-// shape: 0 interleaved->interleaved columns, 1 split->interleaved columns,
-//        2 interleaved->interleaved rows,    3 interleaved->split rows
+// shape: 0 interleaved->scratch columns, 1 split->scratch columns,
+//        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
 cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);
 cudaError_t group_prepare(int log2ns);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
