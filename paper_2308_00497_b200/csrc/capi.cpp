@@ -357,8 +357,8 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         }
       }
       if (p->ex.groups.size() == 2) {
-        // chunk of ~L2/4 of intermediate per slot; two slots live in L2
-        int64_t chunk_bytes = int64_t(32) << 20;
+        // opt-in: chunk of intermediate per slot; two slots live in L2
+        int64_t chunk_bytes = 0;
         if (const char *env = std::getenv("FFTGEN_L2_CHUNK_BYTES")) chunk_bytes = std::atoll(env);
         const int64_t per_tf = cfg->n * (int64_t)sizeof(float2);
         p->chunk = chunk_bytes > 0 ? std::max<int64_t>(1, chunk_bytes / per_tf) : 0;

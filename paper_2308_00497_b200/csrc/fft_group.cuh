@@ -25,7 +25,8 @@
 // The global twiddle w_s^{A m} = w_s^{A0 (NS/R0) m} * w_s^{c m}
 // (A = A0 (NS/R0) + c, R0 = the sub-FFT's first pass radix) comes from two
 // fp64-exact fp32 tables Q[A0][m], P[c][m] (generated on the device at plan
-// time), read once per thread into registers.
+// time); the lanes of a warp share m, so the Q reads are L1 broadcasts.
+// Registers are capped (MIN_BLOCKS) so two 512-thread CTAs stay resident.
 #pragma once
 
 #include <cstdint>
@@ -34,9 +35,9 @@
 
 namespace fftgen_b200 {
 
-// User buffers stream through L2 (evict-first); interleaved scratch between
-// groups is written with the normal policy and read back as last use, so a
-// chunk's intermediate can be consumed from the 126 MB L2 (LAYOUT_SCRATCH).
+// Interleaved scratch between groups (LAYOUT_SCRATCH) streams like the user
+// buffers: measured on B200, keeping it L2-resident through chunked
+// execution (FFTGEN_L2_CHUNK_BYTES) lost to the extra launches and tails.
 constexpr int LAYOUT_SCRATCH = 2;
 
 template <int L> struct SIO;
@@ -50,10 +51,10 @@ template <> struct SIO<LAYOUT_INTERLEAVED> {
 };
 template <> struct SIO<LAYOUT_SCRATCH> {
   static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
-    return __ldlu(reinterpret_cast<const float2 *>(p0) + off);
+    return __ldcs(reinterpret_cast<const float2 *>(p0) + off);
   }
   static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
-    reinterpret_cast<float2 *>(p0)[off] = v;
+    __stcs(reinterpret_cast<float2 *>(p0) + off, v);
   }
 };
 template <> struct SIO<LAYOUT_SPLIT> {
