@@ -1,0 +1,119 @@
+"""GPU edge cases across the execution strategies: in-place execution,
+CUDA-graph capture and replay, ragged batches and padded dist on the
+four-step path, unaligned pointers, and plan reuse across batch sizes."""
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fg():
+    import paper_2308_00497_b200 as m
+    return m
+
+
+def rand(shape, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.rand(*shape, device="cuda", generator=g) * 2 - 1
+
+
+def check_rows(orc, x, y, n, inverse=False, rows=(0, -1)):
+    """x, y: (batch, n, 2) float32 device tensors."""
+    for b in rows:
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        got = y[b].reshape(-1).double().cpu().numpy()
+        assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4, inverse=inverse)) < 3e-6, b
+
+
+@pytest.mark.parametrize("n", [1024, 4096, 16384, 1 << 16, 1 << 21])
+def test_in_place_execution(fg, orc, n):
+    batch = 4 if n <= 1 << 16 else 1
+    x = rand((batch, n, 2), 1)
+    ref = x.clone()
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    plan.execute(x, x)  # out == in
+    torch.cuda.synchronize()
+    check_rows(orc, ref, x, n)
+    re, im = ref[..., 0].contiguous(), ref[..., 1].contiguous()
+    ps = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout="split"))
+    ps.execute(re, re, im, im, direction=fg.INVERSE)
+    torch.cuda.synchronize()
+    check_rows(orc, ref, torch.stack([re, im], -1), n, inverse=True)
+
+
+@pytest.mark.parametrize("n", [4096, 1 << 16])
+def test_cuda_graph_capture_and_replay(fg, orc, n):
+    batch = 64
+    x = rand((batch, n, 2), 2)
+    y = torch.empty_like(x)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.execute(x, y, stream=s)  # warm-up outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.execute(x, y, stream=s)
+    y.zero_()
+    x.copy_(rand((batch, n, 2), 3))
+    g.replay()
+    torch.cuda.synchronize()
+    check_rows(orc, x, y, n, rows=(0, 17, batch - 1))
+
+
+@pytest.mark.parametrize("n", [1 << 15, 1 << 17])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_fourstep_ragged_batch_and_padded_dist(fg, orc, n, layout):
+    batch, dist = 3, n + 64
+    x = rand((batch, dist, 2), 4)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout=layout))
+    if layout == "interleaved":
+        y = torch.full_like(x, float("nan"))
+        plan.execute(x, y, dist=dist)
+    else:
+        re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+        ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+        plan.execute(re, ore, im, oim, dist=dist)
+        y = torch.stack([ore, oim], -1)
+    torch.cuda.synchronize()
+    assert torch.isnan(y[:, n:]).all()  # padding untouched
+    check_rows(orc, x[:, :n], y[:, :n], n, rows=(0, 1, 2))
+
+
+def test_unaligned_pointers_fall_back_to_direct_kernel(fg, orc):
+    n, batch = 4096, 5
+    buf = rand((batch * n * 2 + 2,), 5)
+    x = buf[1:1 + batch * n * 2].view(batch, n, 2)  # 4-byte aligned only
+    out = torch.empty(batch * n * 2 + 2, device="cuda")
+    y = out[1:1 + batch * n * 2].view(batch, n, 2)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    plan.execute(x, y)
+    torch.cuda.synchronize()
+    check_rows(orc, x, y, n, rows=(0, 4))
+
+
+def test_smaller_batch_than_planned_via_host_path(fg, orc):
+    """execute_host chunks a plan's batch; the last chunk is ragged."""
+    n, batch = 1 << 16, 257  # 64 MiB staging -> chunk 64 transforms, last chunk of 1
+    x = np.random.default_rng(0).uniform(-1, 1, (batch, n * 2)).astype(np.float32)
+    y = np.empty_like(x)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    plan.execute_host(x, y)
+    for b in (0, 63, 64, 256):
+        assert oracle.rel_l2(y[b], orc.forward(x[b].astype(np.float64), "stockham", 4)) < 3e-6
+
+
+def test_many_plans_and_destroy(fg):
+    plans = [fg.compile_pipeline(fg.PipelineConfig(n=1 << l, batch=2)) for l in range(1, 21)]
+    for p in plans:
+        assert p.launches() >= 1
+        p.close()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(5):
+        p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 20, batch=16))
+        p.close()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)  # no leak of scratch/tables
