@@ -76,6 +76,12 @@ struct fftgen_plan {
   float2 *d_twg = nullptr;
   float2 *d_scratch = nullptr;
   size_t scratch_bytes = 0;
+  // K3 dataflow (both groups in one persistent launch, L2 ring of slots)
+  bool use_flow = false;
+  int flow_grid = 0;
+  int64_t flow_lag = 0, flow_ring = 0;
+  char *d_counters = nullptr;
+  size_t counter_bytes = 0;
   // L2-resident chunked execution of 2-group plans (0 = off)
   int64_t chunk = 0;
   cudaStream_t xs[2] = {nullptr, nullptr};
@@ -105,16 +111,19 @@ fftgen_status validate_exec(const fftgen_plan *p, int direction, const void *in0
   if (dist < p->cfg.n)
     return fail(FFTGEN_ERR_DIMENSION, "dist " + std::to_string(dist) + " is smaller than n " +
                                           std::to_string(p->cfg.n));
+  // element alignment: float2 for interleaved, float for split
+  const uintptr_t al = p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 4 : 8;
+  for (const void *q : {in0, in1, out0, out1})
+    if (q && (uintptr_t)q % al != 0)
+      return fail(FFTGEN_ERR_EXEC, "data pointer not aligned to its " + std::to_string(al) + "-byte element");
   return FFTGEN_OK;
 }
 
 // One K3 group launch: the first group reads the user layout, the last writes
 // it, intermediates are interleaved scratch.
-cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void *in0, const void *in1,
-                         void *out0, void *out1, int64_t idist, int64_t odist, int64_t batch, cudaStream_t s) {
+GroupArgs make_group_args(const fftgen_plan *p, int g, const void *in0, const void *in1, void *out0, void *out1,
+                          int64_t idist, int64_t odist) {
   const GroupDesc &d = p->ex.groups[g];
-  const bool first = g == 0, last = g + 1 == (int)p->ex.groups.size();
-  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
   GroupArgs a{};
   a.in0 = in0;
   a.in1 = in1;
@@ -128,6 +137,15 @@ cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void 
   a.tw_local = p->d_tw + d.local_off;
   a.tw_q = d.cols > 1 ? p->d_twg + d.q_off : nullptr;
   a.tw_p = d.cols > 1 ? p->d_twg + d.p_off : nullptr;
+  return a;
+}
+
+cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void *in0, const void *in1,
+                         void *out0, void *out1, int64_t idist, int64_t odist, int64_t batch, cudaStream_t s) {
+  const GroupDesc &d = p->ex.groups[g];
+  const bool first = g == 0, last = g + 1 == (int)p->ex.groups.size();
+  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+  const GroupArgs a = make_group_args(p, g, in0, in1, out0, out1, idist, odist);
   const int shape = last ? (split ? 3 : 2) : (first ? (split ? 1 : 0) : 4);
   return group_launch(d.log2ns, shape, direction, a, batch, s);
 }
@@ -172,6 +190,26 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
   case STRAT_FOURSTEP: {
     const auto &gs = p->ex.groups;
     const bool split = layout == FFTGEN_LAYOUT_SPLIT;
+    if (p->use_flow) {
+      // one persistent launch for both groups, intermediate in the L2 ring
+      cudaError_t e = cudaMemsetAsync(p->d_counters, 0, p->counter_bytes, s);
+      if (e != cudaSuccess) return e;
+      FlowArgs f{};
+      f.g0 = make_group_args(p, 0, in0, in1, p->d_scratch, nullptr, dist, n);
+      f.g1 = make_group_args(p, 1, p->d_scratch, nullptr, out0, out1, n, dist);
+      f.n = n;
+      f.batch = batch;
+      f.lag = std::min<int64_t>(p->flow_lag, batch);
+      f.ring_slots = p->flow_ring;
+      f.tiles0 = f.g0.tiles_per_outer;
+      f.tiles1 = f.g1.tiles_per_outer;
+      f.work = reinterpret_cast<unsigned long long *>(p->d_counters);
+      f.done0 = reinterpret_cast<int *>(p->d_counters + 8);
+      f.done1 = f.done0 + p->flow_ring;
+      const int64_t items = batch * (f.tiles0 + f.tiles1);
+      const int grid = (int)std::min<int64_t>(items, p->flow_grid);
+      return flow_launch(gs[0].log2ns, gs[1].log2ns, layout, direction, f, grid, s);
+    }
     if (gs.size() == 2 && p->chunk > 0 && batch >= 2 * p->chunk) {
       // L2-resident chunking: group 0 of chunk c on xs[0], group 1 on xs[1];
       // the intermediate of a chunk (<= 2 slots live) is read back from L2.
@@ -375,7 +413,32 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           p->chunk = 0;
         }
       }
-      p->scratch_bytes = (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n * sizeof(float2);
+      const auto &gs = p->ex.groups;
+      const char *no_flow = std::getenv("FFTGEN_DISABLE_FLOW");
+      if (gs.size() == 2 && flow_supported(gs[0].log2ns, gs[1].log2ns) && !(no_flow && no_flow[0] != '0') &&
+          p->chunk == 0) {
+        int bps = 0, smem = 0, sms = 0;
+        if ((e = flow_prepare(gs[0].log2ns, gs[1].log2ns, &bps, &smem)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, std::string("dataflow kernel attributes: ") + cudaGetErrorString(e));
+        if (bps > 0) {
+          const int64_t resident = (int64_t)bps * sms;
+          const int64_t t0 = cfg->n / gs[0].ns / gs[0].tc, t1 = cfg->n / gs[1].ns / gs[1].tc;
+          // group 1 of b is dispatched LAG transforms after group 0 of b: far
+          // enough that the resident CTAs have finished it; a slot is reused
+          // R transforms later, after group 1 has drained it
+          p->flow_lag = std::min<int64_t>(cfg->batch, (resident + t0 + t1 - 1) / (t0 + t1) + 1);
+          p->flow_ring = std::min<int64_t>(cfg->batch, 2 * p->flow_lag + 1);
+          p->flow_grid = (int)resident;
+          p->use_flow = true;
+          p->counter_bytes = 8 + 2 * (size_t)p->flow_ring * sizeof(int);
+          if ((e = cudaMalloc(&p->d_counters, p->counter_bytes)) != cudaSuccess)
+            return bail(FFTGEN_ERR_NOMEM, "dataflow counters");
+        }
+      }
+      p->scratch_bytes = p->use_flow ? (size_t)p->flow_ring * (size_t)cfg->n * sizeof(float2)
+                                     : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
+                                           sizeof(float2);
       if ((e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
                                           " bytes): " + cudaGetErrorString(e));
@@ -401,6 +464,7 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_counters) cudaFree(p->d_counters);
     for (auto &x : p->xs)
       if (x) cudaStreamDestroy(x);
     for (cudaEvent_t ev : {p->ev_fork, p->ev_a[0], p->ev_a[1], p->ev_b[0], p->ev_b[1], p->ev_join[0], p->ev_join[1]})
@@ -548,7 +612,7 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return (int)p->ex.groups.size();
+  default: return p->use_flow ? 1 : (int)p->ex.groups.size();
   }
 }
 
@@ -582,8 +646,13 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_FOURSTEP) {
-    o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
-      << " B\n";
+    if (p->use_flow)
+      o << "four-step: 1 fft_flow_kernel<" << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
+        << "> launch (persistent dataflow, grid " << p->flow_grid << ", lag " << p->flow_lag << ", L2 ring "
+        << p->flow_ring << " slots = " << p->scratch_bytes << " B)\n";
+    else
+      o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
+        << " B\n";
     for (size_t i = 0; i < p->ex.groups.size(); ++i) {
       const GroupDesc &d = p->ex.groups[i];
       int64_t threads, tc, smem, r0;

@@ -39,6 +39,7 @@ namespace fftgen_b200 {
 // buffers: measured on B200, keeping it L2-resident through chunked
 // execution (FFTGEN_L2_CHUNK_BYTES) lost to the extra launches and tails.
 constexpr int LAYOUT_SCRATCH = 2;
+constexpr int LAYOUT_RING = 3;
 
 template <int L> struct SIO;
 template <> struct SIO<LAYOUT_INTERLEAVED> {
@@ -68,20 +69,17 @@ template <> struct SIO<LAYOUT_SPLIT> {
   }
 };
 
+// One tile of one group: TC adjacent transforms (tile index tt) of the
+// transform whose input / output start at element offsets ib / ob.
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
-__global__ void __launch_bounds__(GroupGeom<NS>::THREADS, GroupGeom<NS>::MIN_BLOCKS) fft_group_kernel(const GroupArgs a) {
+FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
   using GG = GroupGeom<NS>;
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
   static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == G::R(1), "group sub-FFTs are 2-pass plans");
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
   constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
-  extern __shared__ float4 smem_f4[];
-  float2 *smem = reinterpret_cast<float2 *>(smem_f4);
   const int tid = threadIdx.x;
-
-  const int64_t b = blockIdx.x / a.tiles_per_outer;
-  const int64_t tt = blockIdx.x - b * a.tiles_per_outer;
   int64_t m0, c0;
   if (ROWS) {
     m0 = tt * TC;
@@ -91,7 +89,6 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS, GroupGeom<NS>::MIN_BLO
     m0 = u0 / a.k;
     c0 = u0 - m0 * a.k;
   }
-  const int64_t ib = b * a.idist, ob = b * a.odist;
 
   // ---- pass 0: HBM -> registers, global twiddle, radix-R0 codelets --------
   float2 v[G::RMAX];
@@ -137,6 +134,96 @@ __global__ void __launch_bounds__(GroupGeom<NS>::THREADS, GroupGeom<NS>::MIN_BLO
       const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
       SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
     }
+  }
+}
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+__global__ void __launch_bounds__(GroupGeom<NS>::THREADS, GroupGeom<NS>::MIN_BLOCKS)
+fft_group_kernel(const GroupArgs a) {
+  extern __shared__ float4 smem_f4[];
+  const int64_t b = blockIdx.x / a.tiles_per_outer;
+  const int64_t tt = blockIdx.x - b * a.tiles_per_outer;
+  group_tile<NS, LIN, LOUT, DIR, ROWS>(a, b * a.idist, b * a.odist, tt, reinterpret_cast<float2 *>(smem_f4));
+}
+
+// ---- K3 dataflow: both groups of a 2-group plan in ONE persistent launch ----
+//
+// Work items (one tile each) are handed out in a fixed global order by an
+// atomic counter: group 0 of transform s, interleaved with group 1 of
+// transform s - LAG.  The intermediate of transform b lives in slot b % R of
+// a ring small enough to stay in the 126 MB L2, so HBM only sees the input
+// read and the output write (16 N bytes per transform) instead of 32 N.
+// Dependencies are per-slot tile counters (release / acquire at gpu scope):
+//   group 1 of b waits for all group-0 tiles of b,
+//   group 0 of b waits until group 1 of b - R has drained the slot.
+// Every wait targets an item dispatched earlier, and the grid never exceeds
+// the co-resident CTA count, so the schedule cannot deadlock.
+FFTGEN_FI int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FFTGEN_FI void red_release_gpu(int *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ring traffic: plain (write-back) stores, L2-only loads (the slot of an
+// earlier generation may still sit in this SM's L1)
+template <> struct SIO<LAYOUT_RING> {
+  static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
+    return __ldcg(reinterpret_cast<const float2 *>(p0) + off);
+  }
+  static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
+    reinterpret_cast<float2 *>(p0)[off] = v;
+  }
+};
+
+template <int NS0, int NS1, int LIN, int LOUT, int DIR>
+__global__ void __launch_bounds__(GroupGeom<NS0>::THREADS, GroupGeom<NS0>::MIN_BLOCKS)
+fft_flow_kernel(const FlowArgs f) {
+  static_assert(GroupGeom<NS0>::THREADS == GroupGeom<NS1>::THREADS, "both groups share the CTA shape");
+  extern __shared__ float4 smem_f4[];
+  float2 *smem = reinterpret_cast<float2 *>(smem_f4);
+  __shared__ int64_t item_s;
+  const int64_t t0 = f.tiles0, t1 = f.tiles1, D = f.lag, batch = f.batch, R = f.ring_slots;
+  const int64_t p1 = D * t0, p2 = p1 + (batch - D) * (t0 + t1), p3 = p2 + D * t1;
+  int *done0 = f.done0, *done1 = f.done1;
+  for (;;) {
+    if (threadIdx.x == 0) item_s = (int64_t)atomicAdd(f.work, 1ull);
+    __syncthreads();
+    const int64_t idx = item_s;
+    __syncthreads();
+    if (idx >= p3) break;
+    bool first;
+    int64_t b, tile;
+    if (idx < p1) {
+      first = true, b = idx / t0, tile = idx % t0;
+    } else if (idx < p2) {
+      const int64_t r = idx - p1, s = D + r / (t0 + t1), q = r % (t0 + t1);
+      first = q < t0;
+      b = first ? s : s - D;
+      tile = first ? q : q - t0;
+    } else {
+      const int64_t r = idx - p2;
+      first = false, b = batch - D + r / t1, tile = r % t1;
+    }
+    const int64_t slot = b % R, gen = b / R;
+    if (threadIdx.x == 0) {
+      if (first) {
+        if (gen > 0)
+          while (ld_acquire_gpu(done1 + slot) < gen * t1) __nanosleep(32);
+      } else {
+        while (ld_acquire_gpu(done0 + slot) < (gen + 1) * t0) __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    if (first)
+      group_tile<NS0, LIN, LAYOUT_RING, DIR, false>(f.g0, b * f.g0.idist, slot * f.n, tile, smem);
+    else
+      group_tile<NS1, LAYOUT_RING, LOUT, DIR, true>(f.g1, slot * f.n, b * f.g1.odist, tile, smem);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) red_release_gpu((first ? done0 : done1) + slot, 1);
   }
 }
 

@@ -47,6 +47,18 @@ struct GroupArgs {
   const float2 *tw_p;      // [c][m]  = w_s^{c m}
 };
 
+// Both groups of a 2-group plan in one persistent launch (fft_flow_kernel):
+// group-0 output goes to slot b % ring_slots of an L2-resident ring.
+struct FlowArgs {
+  GroupArgs g0, g1;        // g0: user in -> ring; g1: ring -> user out
+  int64_t n, batch, lag, ring_slots, tiles0, tiles1;
+  unsigned long long *work;  // work-item counter (zeroed per launch)
+  int *done0, *done1;        // per-slot completed tiles of group 0 / group 1
+};
+bool flow_supported(int log2ns0, int log2ns1);
+cudaError_t flow_prepare(int log2ns0, int log2ns1, int *blocks_per_sm, int *smem_bytes);
+cudaError_t flow_launch(int log2ns0, int log2ns1, int layout, int dir, const FlowArgs &f, int grid, cudaStream_t s);
+
 // shape: 0 interleaved->scratch columns, 1 split->scratch columns,
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
 cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);

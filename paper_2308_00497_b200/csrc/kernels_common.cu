@@ -229,3 +229,43 @@ cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, 
 }
 
 }  // namespace fftgen_b200
+
+// ---- K3 dataflow dispatch ---------------------------------------------------
+#include "flow_instances.cuh"
+
+namespace fftgen_b200 {
+
+cudaError_t flow_launch_f(int, int, int, const FlowArgs &, int, cudaStream_t);
+cudaError_t flow_launch_b(int, int, int, const FlowArgs &, int, cudaStream_t);
+cudaError_t flow_prepare_f(int, int, int *);
+cudaError_t flow_prepare_b(int, int, int *);
+
+bool flow_supported(int l0, int l1) {
+  switch (l0 * 16 + l1) {
+  case 7 * 16 + 7: case 7 * 16 + 8: case 8 * 16 + 8: case 9 * 16 + 9: case 9 * 16 + 10: case 10 * 16 + 10:
+    return true;
+  default:
+    return false;
+  }
+}
+
+cudaError_t flow_prepare(int l0, int l1, int *bps, int *smem) {
+  int a = 0, b = 0;
+  cudaError_t e = flow_prepare_f(l0, l1, &a);
+  if (e == cudaSuccess) e = flow_prepare_b(l0, l1, &b);
+  *bps = std::min(a, b);
+  switch (l0 * 16 + l1) {
+#define FFTGEN_FS(A, B, NA, NB) case A * 16 + B: *smem = FlowShape<NA, NB>::SMEM; break;
+    FFTGEN_FS(7, 7, 128, 128) FFTGEN_FS(7, 8, 128, 256) FFTGEN_FS(8, 8, 256, 256)
+    FFTGEN_FS(9, 9, 512, 512) FFTGEN_FS(9, 10, 512, 1024) FFTGEN_FS(10, 10, 1024, 1024)
+#undef FFTGEN_FS
+  default: *smem = 0;
+  }
+  return e;
+}
+
+cudaError_t flow_launch(int l0, int l1, int layout, int dir, const FlowArgs &f, int grid, cudaStream_t s) {
+  return dir < 0 ? flow_launch_f(l0, l1, layout, f, grid, s) : flow_launch_b(l0, l1, layout, f, grid, s);
+}
+
+}  // namespace fftgen_b200

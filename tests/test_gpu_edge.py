@@ -86,14 +86,17 @@ def test_fourstep_ragged_batch_and_padded_dist(fg, orc, n, layout):
 
 def test_unaligned_pointers_fall_back_to_direct_kernel(fg, orc):
     n, batch = 4096, 5
-    buf = rand((batch * n * 2 + 2,), 5)
-    x = buf[1:1 + batch * n * 2].view(batch, n, 2)  # 4-byte aligned only
-    out = torch.empty(batch * n * 2 + 2, device="cuda")
-    y = out[1:1 + batch * n * 2].view(batch, n, 2)
+    buf = rand((batch * n * 2 + 4,), 5)
+    x = buf[2:2 + batch * n * 2].view(batch, n, 2)  # 8-byte aligned, not 16: no cp.async.bulk
+    out = torch.empty(batch * n * 2 + 4, device="cuda")
+    y = out[2:2 + batch * n * 2].view(batch, n, 2)
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
     plan.execute(x, y)
     torch.cuda.synchronize()
     check_rows(orc, x, y, n, rows=(0, 4))
+    # a float2 stream that is not even 8-byte aligned is rejected, not faulted
+    with pytest.raises(fg.ExecError):
+        plan.execute(buf[1:1 + batch * n * 2], y)
 
 
 def test_smaller_batch_than_planned_via_host_path(fg, orc):

@@ -152,6 +152,44 @@ def test_2p26_random_sampled_bins_and_roundtrip(fg, orc):
     assert np.abs(got - want).max() / scale < 1e-4
 
 
+@pytest.mark.parametrize("l2,batch", [(14, 700), (15, 400), (16, 200), (18, 40), (19, 20), (20, 9)])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_dataflow_kernel_matches_two_launch_path(fg, orc, l2, batch, layout, monkeypatch):
+    """The persistent dataflow kernel (both groups, L2 ring of slots reused
+    several times over the batch) is bitwise the two-launch path."""
+    n = 1 << l2
+    if l2 == 14:  # 2^14 runs on the block kernel by default; force the group split
+        pytest.skip("2^14 is planned on the K2 block kernel")
+    g = torch.Generator(device="cuda").manual_seed(l2)
+    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
+
+    def run_once(direction):
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+        if layout == "interleaved":
+            y = torch.full_like(x, float("nan"))
+            plan.execute(x, y, direction=direction)
+        else:
+            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+            plan.execute(re, ore, im, oim, direction=direction)
+            y = torch.stack([ore, oim], dim=-1)
+        torch.cuda.synchronize()
+        return y, plan
+
+    for direction in (-1, 1):
+        flow, plan = run_once(direction)
+        assert "dataflow" in plan.describe()
+        monkeypatch.setenv("FFTGEN_DISABLE_FLOW", "1")
+        plain, plan2 = run_once(direction)
+        monkeypatch.delenv("FFTGEN_DISABLE_FLOW")
+        assert "dataflow" not in plan2.describe()
+        assert torch.equal(flow, plain), direction
+    for b in (0, batch // 2, batch - 1):
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        got = plain[b].reshape(-1).double().cpu().numpy()
+        assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4, inverse=True)) < 3e-6, b
+
+
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
     """Batched 2-group plans run in L2-sized chunks on two internal streams;
