@@ -414,9 +414,13 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         }
       }
       const auto &gs = p->ex.groups;
+      // opt-in: measured on B200 the dataflow kernel keeps the intermediate
+      // in L2 (DRAM bytes == 16 N) but its per-tile fence/atomic/dependency
+      // serialization makes it ~8% slower than the two-launch path at 2^16
+      const char *flow_env = std::getenv("FFTGEN_ENABLE_FLOW");
       const char *no_flow = std::getenv("FFTGEN_DISABLE_FLOW");
-      if (gs.size() == 2 && flow_supported(gs[0].log2ns, gs[1].log2ns) && !(no_flow && no_flow[0] != '0') &&
-          p->chunk == 0) {
+      const bool want_flow = flow_env && flow_env[0] != '0' && !(no_flow && no_flow[0] != '0');
+      if (gs.size() == 2 && flow_supported(gs[0].log2ns, gs[1].log2ns) && want_flow && p->chunk == 0) {
         int bps = 0, smem = 0, sms = 0;
         if ((e = flow_prepare(gs[0].log2ns, gs[1].log2ns, &bps, &smem)) != cudaSuccess ||
             (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
@@ -427,7 +431,10 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           // group 1 of b is dispatched LAG transforms after group 0 of b: far
           // enough that the resident CTAs have finished it; a slot is reused
           // R transforms later, after group 1 has drained it
-          p->flow_lag = std::min<int64_t>(cfg->batch, (resident + t0 + t1 - 1) / (t0 + t1) + 1);
+          double lag_mult = 2.0;
+          if (const char *env = std::getenv("FFTGEN_FLOW_LAG_MULT")) lag_mult = std::atof(env);
+          p->flow_lag = std::min<int64_t>(
+              cfg->batch, (int64_t)(lag_mult * (double)((resident + t0 + t1 - 1) / (t0 + t1))) + 1);
           p->flow_ring = std::min<int64_t>(cfg->batch, 2 * p->flow_lag + 1);
           p->flow_grid = (int)resident;
           p->use_flow = true;

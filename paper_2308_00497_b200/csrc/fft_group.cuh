@@ -184,16 +184,17 @@ fft_flow_kernel(const FlowArgs f) {
   static_assert(GroupGeom<NS0>::THREADS == GroupGeom<NS1>::THREADS, "both groups share the CTA shape");
   extern __shared__ float4 smem_f4[];
   float2 *smem = reinterpret_cast<float2 *>(smem_f4);
-  __shared__ int64_t item_s;
+  __shared__ int64_t item_s[2];
   const int64_t t0 = f.tiles0, t1 = f.tiles1, D = f.lag, batch = f.batch, R = f.ring_slots;
   const int64_t p1 = D * t0, p2 = p1 + (batch - D) * (t0 + t1), p3 = p2 + D * t1;
   int *done0 = f.done0, *done1 = f.done1;
-  for (;;) {
-    if (threadIdx.x == 0) item_s = (int64_t)atomicAdd(f.work, 1ull);
-    __syncthreads();
-    const int64_t idx = item_s;
-    __syncthreads();
+  // the next item index is fetched while the current tile runs
+  if (threadIdx.x == 0) item_s[0] = (int64_t)atomicAdd(f.work, 1ull);
+  __syncthreads();
+  for (int it = 0;; ++it) {
+    const int64_t idx = item_s[it & 1];
     if (idx >= p3) break;
+    if (threadIdx.x == 0) item_s[(it + 1) & 1] = (int64_t)atomicAdd(f.work, 1ull);
     bool first;
     int64_t b, tile;
     if (idx < p1) {
@@ -221,9 +222,13 @@ fft_flow_kernel(const FlowArgs f) {
       group_tile<NS0, LIN, LAYOUT_RING, DIR, false>(f.g0, b * f.g0.idist, slot * f.n, tile, smem);
     else
       group_tile<NS1, LAYOUT_RING, LOUT, DIR, true>(f.g1, slot * f.n, b * f.g1.odist, tile, smem);
-    __threadfence();
+    // the barrier orders every thread's ring stores before thread 0's
+    // gpu-scope fence + release, which publishes them (cumulativity)
     __syncthreads();
-    if (threadIdx.x == 0) red_release_gpu((first ? done0 : done1) + slot, 1);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      red_release_gpu((first ? done0 : done1) + slot, 1);
+    }
   }
 }
 

@@ -177,11 +177,11 @@ def test_dataflow_kernel_matches_two_launch_path(fg, orc, l2, batch, layout, mon
         return y, plan
 
     for direction in (-1, 1):
+        monkeypatch.setenv("FFTGEN_ENABLE_FLOW", "1")
         flow, plan = run_once(direction)
+        monkeypatch.delenv("FFTGEN_ENABLE_FLOW")
         assert "dataflow" in plan.describe()
-        monkeypatch.setenv("FFTGEN_DISABLE_FLOW", "1")
         plain, plan2 = run_once(direction)
-        monkeypatch.delenv("FFTGEN_DISABLE_FLOW")
         assert "dataflow" not in plan2.describe()
         assert torch.equal(flow, plain), direction
     for b in (0, batch // 2, batch - 1):
