@@ -77,8 +77,10 @@ struct Pad {
 };
 FFTGEN_HD constexpr int padded(int i, Pad pd) { return pd.K ? i + pd.K * (i / pd.PP) : i; }
 
-template <int N> struct PadSearch {
+// ELEM = element bytes: 8 (float2 exchange) or 4 (one re/im plane).
+template <int N, int ELEM = 8> struct PadSearch {
   using G = BlockGeom<N>;
+  static constexpr int WAVE = 128 / ELEM;  // lanes served per shared-memory wavefront
   // Representative registers x and butterflies j suffice: the access
   // patterns are affine in both.
   static constexpr int cost(int p, Pad pd) {
@@ -93,14 +95,14 @@ template <int N> struct PadSearch {
         for (int xx = 0; xx < 4; ++xx) {
           const int j = js[jj], x = xs[xx];
           int wavefronts = 0;
-          for (int half = 0; half < 2; ++half) {
-            int cnt[16] = {};
+          for (int half = 0; half < 32 / WAVE; ++half) {
+            int cnt[32] = {};
             int deg = 0;
-            for (int l = 16 * half; l < 16 * half + 16; ++l) {
+            for (int l = WAVE * half; l < WAVE * half + WAVE; ++l) {
               const int t = l % T, f = l / T;  // T < 32: other transforms
               const int u = t + j * T, m = u / k, c = u % k;
               const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
-              const int b = (padded(idx, pd) + f * (padded(N - 1, pd) + 1)) & 15;
+              const int b = (padded(idx, pd) + f * (padded(N - 1, pd) + 1)) % WAVE;
               cnt[b]++;
               deg = cnt[b] > deg ? cnt[b] : deg;
             }
@@ -129,10 +131,10 @@ template <int N> struct PadSearch {
   }
 };
 
-template <int N, int p> struct BoundaryPad {
-  static constexpr Pad value = BlockGeom<N>::P > 1 ? PadSearch<N>::best(p) : Pad{16, 0};
+template <int N, int p, int ELEM = 8> struct BoundaryPad {
+  static constexpr Pad value = BlockGeom<N>::P > 1 ? PadSearch<N, ELEM>::best(p) : Pad{16, 0};
   static constexpr int region = padded(N - 1, value) + 1;
-  static constexpr int wavefronts = BlockGeom<N>::P > 1 ? PadSearch<N>::cost(p, value) : 0;
+  static constexpr int wavefronts = BlockGeom<N>::P > 1 ? PadSearch<N, ELEM>::cost(p, value) : 0;
 };
 
 template <int N> struct SmemGeom {
@@ -162,6 +164,22 @@ template <int N> struct TmaGeom {
   static constexpr int SLOT = ((RAW > XCH ? RAW : XCH) + 127) / 128 * 128;
   static constexpr int STAGE_BYTES = TP * SLOT;
   static constexpr int BYTES = STAGES * STAGE_BYTES + 128;            // + mbarriers
+};
+
+// -------------------------------------------------------------------------
+// Single-stage TMA variant for the largest smem-resident size (N = 2^14): the
+// raw input stage (8N bytes) is refilled by cp.async.bulk as soon as pass 0
+// has consumed it, while passes 1-2 exchange through ONE padded fp32 plane
+// (re, then im), so stage + plane fit one SM (192 KB).
+template <int N> struct Tma1Geom {
+  static constexpr bool ENABLED = N == 16384;
+  using G = BlockGeom<N>;
+  static constexpr int THREADS = G::THREADS;
+  static constexpr int RAW = 8 * N;
+  static constexpr int r0 = BoundaryPad<N, 0, 4>::region;
+  static constexpr int r1 = BoundaryPad<N, 1, 4>::region;
+  static constexpr int PLANE = ((r0 > r1 ? r0 : r1) * 4 + 127) / 128 * 128;
+  static constexpr int BYTES = RAW + PLANE + 128;
 };
 
 // -------------------------------------------------------------------------

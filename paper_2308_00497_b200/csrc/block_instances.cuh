@@ -27,7 +27,14 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
     e = cudaFuncSetAttribute(fft_block_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   *tma_blocks_per_sm = 0;
-  if constexpr (TmaGeom<N>::ENABLED) {
+  if constexpr (Tma1Geom<N>::ENABLED) {
+    constexpr int tsmem = Tma1Geom<N>::BYTES;
+    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tsmem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR>,
+                                                      Tma1Geom<N>::THREADS, tsmem);
+  } else if constexpr (TmaGeom<N>::ENABLED) {
     constexpr int tsmem = TmaGeom<N>::BYTES;
     e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR, false>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
@@ -48,7 +55,12 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
 
 template <int N, int LAYOUT, int DIR>
 cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, bool store_tma, cudaStream_t s) {
-  if constexpr (TmaGeom<N>::ENABLED) {
+  if constexpr (Tma1Geom<N>::ENABLED) {
+    if (grid <= 0 || a.batch <= 0) return cudaSuccess;
+    (void)store_tma;
+    fft_block_tma1_kernel<N, LAYOUT, DIR><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
+    return cudaGetLastError();
+  } else if constexpr (TmaGeom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
     if (store_tma)
       fft_block_tma_kernel<N, LAYOUT, DIR, true><<<grid, TmaGeom<N>::THREADS, TmaGeom<N>::BYTES, s>>>(a);

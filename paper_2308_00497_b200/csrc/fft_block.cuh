@@ -380,4 +380,114 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
   if (STORE_TMA && tid == 0) bulk_wait0();
 }
 
+// ---- variant 3: single-stage TMA + plane-wise exchange (N = 2^14) --------
+// One CTA (512 threads) per SM.  The raw stage is refilled with the next
+// transform right after pass 0 has read it; passes 1-2 exchange through a
+// single padded fp32 plane, re then im (BoundaryPad<N, p, 4> keeps the
+// 32-bit writer and reader patterns conflict-free).
+template <class G, int N, int p, int COMP>
+FFTGEN_FI void plane_write(float *X, int t, const float2 *v) {
+  constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R;
+  constexpr Pad pd = BoundaryPad<N, p, 4>::value;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+#pragma unroll
+    for (int B = 0; B < R; ++B) X[padded((B * cols + m) * k + c, pd)] = COMP ? v[j * R + B].y : v[j * R + B].x;
+  }
+}
+
+template <class G, int N, int p, int COMP>  // reader of pass p (pad of boundary p-1)
+FFTGEN_FI void plane_read(const float *X, int t, float2 *v) {
+  constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R;
+  constexpr Pad pd = BoundaryPad<N, p - 1, 4>::value;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+#pragma unroll
+    for (int A = 0; A < R; ++A) {
+      const float x = X[padded((m * R + A) * k + c, pd)];
+      if (COMP)
+        v[j * R + A].y = x;
+      else
+        v[j * R + A].x = x;
+    }
+  }
+}
+
+template <class G, int p, int DIR>
+FFTGEN_FI void pass_compute(int t, const float2 *__restrict__ tw, float2 *v) {
+  constexpr int R = G::R(p), k = G::K(p), cols = G::COLS(p), J = G::RMAX / R;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k;
+    const float2 *twp = tw + G::TW_OFF(p) + m;
+#pragma unroll
+    for (int A = 1; A < R; ++A) v[j * R + A] = mul_tw<DIR>(v[j * R + A], __ldg(twp + A * cols));
+    reg_fft<R, DIR>(v + j * R);
+  }
+}
+
+template <class G, int N, int p, int DIR>
+FFTGEN_FI void plane_exchange_pass(float *X, int t, const float2 *__restrict__ tw, float2 *v) {
+  plane_write<G, N, p - 1, 0>(X, t, v);
+  __syncthreads();
+  plane_read<G, N, p, 0>(X, t, v);  // overwrites .x only; old .y still in place
+  __syncthreads();
+  plane_write<G, N, p - 1, 1>(X, t, v);
+  __syncthreads();
+  plane_read<G, N, p, 1>(X, t, v);
+  pass_compute<G, p, DIR>(t, tw, v);
+}
+
+template <int N, int LAYOUT, int DIR>
+__global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel(const BlockArgs args) {
+  using TG = Tma1Geom<N>;
+  using G = typename TG::G;
+  static_assert(G::TPB == 1 && G::P == 3, "single-stage variant is for one 3-pass transform per CTA");
+  extern __shared__ float4 smem_f4[];
+  char *stage = reinterpret_cast<char *>(smem_f4);
+  float *X = reinterpret_cast<float *>(stage + TG::RAW);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(stage + TG::RAW + TG::PLANE);
+  const int t = threadIdx.x;
+  constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
+  auto issue = [&](int64_t b) {
+    mbar_expect_tx(bar, 8 * N);
+    if (LAYOUT == LAYOUT_SPLIT) {
+      bulk_g2s(stage, reinterpret_cast<const float *>(args.in0) + b * args.idist, plane, bar);
+      bulk_g2s(stage + plane, reinterpret_cast<const float *>(args.in1) + b * args.idist, plane, bar);
+    } else {
+      bulk_g2s(stage, reinterpret_cast<const float2 *>(args.in0) + b * args.idist, plane, bar);
+    }
+  };
+  if (t == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && blockIdx.x < args.batch) issue(blockIdx.x);
+  int it = 0;
+  for (int64_t b = blockIdx.x; b < args.batch; b += gridDim.x, ++it) {
+    mbar_wait(bar, it & 1);
+    float2 v[G::RMAX];
+    if constexpr (LAYOUT == LAYOUT_SPLIT) {
+      const float *re = reinterpret_cast<const float *>(stage), *im = re + N;
+      pass0<G, DIR>(t, v, [&](int e) { return make_float2(re[e], im[e]); });
+    } else {
+      const float2 *x = reinterpret_cast<const float2 *>(stage);
+      pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
+    }
+    __syncthreads();  // stage consumed: fetch the next transform behind passes 1-2
+    if (t == 0 && b + gridDim.x < args.batch) {
+      fence_proxy_async();
+      issue(b + gridDim.x);
+    }
+    plane_exchange_pass<G, N, 1, DIR>(X, t, args.tw, v);
+    __syncthreads();
+    plane_exchange_pass<G, N, 2, DIR>(X, t, args.tw, v);
+    store_last<G, LAYOUT>(args, b * args.odist, t, v);
+    __syncthreads();  // X is rewritten by the next iteration
+  }
+}
+
 }  // namespace fftgen_b200

@@ -275,7 +275,7 @@ def test_introspection_matches_reference_goldens(golden, golden_meta):
     assert "fft_block_tma_kernel<4096>" in p.describe()
 
 
-@pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096, 8192, 16384])
 def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
     """The persistent TMA variant and the direct variant run the same passes."""
     x = seeded_batch(orc, n, 37)
