@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "fft_block.cuh"
 #include "kernels.hpp"
@@ -55,7 +56,10 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
 
 bool block_tma_enabled(int log2n) {
   switch (log2n) {
-  case 14: return Tma1Geom<16384>::ENABLED;
+  case 14: {
+    const char *env = std::getenv("FFTGEN_TMA1");
+    return Tma1Geom<16384>::ENABLED && env && env[0] == '1';
+  }
   case 8: return TmaGeom<256>::ENABLED;
   case 9: return TmaGeom<512>::ENABLED;
   case 10: return TmaGeom<1024>::ENABLED;

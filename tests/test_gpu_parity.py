@@ -277,7 +277,9 @@ def test_introspection_matches_reference_goldens(golden, golden_meta):
 
 @pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096, 8192, 16384])
 def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
-    """The persistent TMA variant and the direct variant run the same passes."""
+    """The persistent TMA variant and the direct variant run the same passes
+    (2^14: the opt-in single-stage plane-exchange variant)."""
+    monkeypatch.setenv("FFTGEN_TMA1", "1")
     x = seeded_batch(orc, n, 37)
     for layout in ("interleaved", "split"):
         a = run(n, layout, -1, x)
