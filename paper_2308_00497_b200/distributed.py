@@ -115,6 +115,9 @@ class DistributedFFT:
         P, r, N1, N2 = self.world, self.rank, self.n1, self.n2
         if x_local.numel() != self.m or x_local.dtype != torch.complex64:
             raise ValueError(f"expected complex64 block of {self.m} elements")
+        if P == 1 and self.local_fft == self._gpu_fft:
+            # nothing to exchange: the single-GPU K3 plan is the whole transform
+            return self.local_fft(x_local.reshape(1, -1), self.n, direction).reshape(-1)
         X = x_local.reshape(N1 // P, N2)
         # 1. columns to their owners: chunk q = rows(r) x cols(q)
         R1 = self._a2a(X.reshape(N1 // P, P, N2 // P).transpose(0, 1).contiguous())
