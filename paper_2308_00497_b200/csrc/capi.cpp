@@ -201,8 +201,8 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       f.batch = batch;
       f.lag = std::min<int64_t>(p->flow_lag, batch);
       f.ring_slots = p->flow_ring;
-      f.tiles0 = f.g0.tiles_per_outer;
-      f.tiles1 = f.g1.tiles_per_outer;
+      f.tiles0 = n / gs[0].ns / flow_tile(gs[0].log2ns);
+      f.tiles1 = n / gs[1].ns / flow_tile(gs[1].log2ns);
       f.work = reinterpret_cast<unsigned long long *>(p->d_counters);
       f.done0 = reinterpret_cast<int *>(p->d_counters + 8);
       f.done1 = f.done0 + p->flow_ring;
@@ -427,7 +427,8 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           return bail(FFTGEN_ERR_CUDA, std::string("dataflow kernel attributes: ") + cudaGetErrorString(e));
         if (bps > 0) {
           const int64_t resident = (int64_t)bps * sms;
-          const int64_t t0 = cfg->n / gs[0].ns / gs[0].tc, t1 = cfg->n / gs[1].ns / gs[1].tc;
+          const int64_t t0 = cfg->n / gs[0].ns / flow_tile(gs[0].log2ns);
+          const int64_t t1 = cfg->n / gs[1].ns / flow_tile(gs[1].log2ns);
           // group 1 of b is dispatched LAG transforms after group 0 of b: far
           // enough that the resident CTAs have finished it; a slot is reused
           // R transforms later, after group 1 has drained it

@@ -69,11 +69,19 @@ template <> struct SIO<LAYOUT_SPLIT> {
   }
 };
 
+// Barrier among the THREADS compute threads: __syncthreads (BARID 0) or a
+// named barrier when a scheduler warp shares the CTA.
+template <int BARID, int THREADS> FFTGEN_FI void compute_sync() {
+  if constexpr (BARID == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;" ::"n"(BARID), "n"(THREADS) : "memory");
+}
+
 // One tile of one group: TC adjacent transforms (tile index tt) of the
 // transform whose input / output start at element offsets ib / ob.
-template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0>
 FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
-  using GG = GroupGeom<NS>;
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
   static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == G::R(1), "group sub-FFTs are 2-pass plans");
@@ -120,7 +128,7 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
     }
     smem_write<G, NS, 0>(smem + f * REG, t, v);
   }
-  __syncthreads();
+  compute_sync<BARID, GG::THREADS>();
 
   // ---- pass 1: smem -> registers (lanes over f), codelet, HBM store ------
   {
@@ -178,57 +186,110 @@ template <> struct SIO<LAYOUT_RING> {
   }
 };
 
+// Warp-specialised persistent CTA: CT = 256 compute threads plus one
+// scheduler warp.  The scheduler fetches item k+1 (atomic), waits for its
+// dependency (acquire spin) and publishes item k-1 (fence + release) while
+// the compute threads work on item k; hand-offs use named barriers
+//   READY_s (2 + s): scheduler arrives, compute syncs  -- descriptor slot s filled
+//   DONE_s  (4 + s): compute arrives, scheduler syncs  -- item in slot s stored
+// and the compute threads synchronise among themselves on barrier 1.
+template <int NS0, int NS1> struct FlowGeom {
+  using GG0 = GroupGeom<NS0, 256>;
+  using GG1 = GroupGeom<NS1, 256>;
+  static_assert(GG0::THREADS == GG1::THREADS, "both groups share the compute shape");
+  static constexpr int CT = GG0::THREADS;
+  static constexpr int THREADS = CT + 32;
+  static constexpr int SMEM = GG0::BYTES > GG1::BYTES ? GG0::BYTES : GG1::BYTES;
+  // 32-register codelets (NS >= 512) need the 2-CTA register budget
+  static constexpr int MIN_BLOCKS = (NS0 >= 512 || NS1 >= 512) ? 2 : 3;
+};
+
+FFTGEN_FI void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+FFTGEN_FI void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 template <int NS0, int NS1, int LIN, int LOUT, int DIR>
-__global__ void __launch_bounds__(GroupGeom<NS0>::THREADS, GroupGeom<NS0>::MIN_BLOCKS)
-fft_flow_kernel(const FlowArgs f) {
-  static_assert(GroupGeom<NS0>::THREADS == GroupGeom<NS1>::THREADS, "both groups share the CTA shape");
+__global__ void __launch_bounds__(FlowGeom<NS0, NS1>::THREADS, FlowGeom<NS0, NS1>::MIN_BLOCKS) fft_flow_kernel(const FlowArgs f) {
+  using FG = FlowGeom<NS0, NS1>;
+  constexpr int CT = FG::CT, ALL = FG::THREADS;
   extern __shared__ float4 smem_f4[];
   float2 *smem = reinterpret_cast<float2 *>(smem_f4);
-  __shared__ int64_t item_s[2];
+  __shared__ int64_t desc[2][3];  // {b, tile, first}; b < 0 marks the end
   const int64_t t0 = f.tiles0, t1 = f.tiles1, D = f.lag, batch = f.batch, R = f.ring_slots;
   const int64_t p1 = D * t0, p2 = p1 + (batch - D) * (t0 + t1), p3 = p2 + D * t1;
-  int *done0 = f.done0, *done1 = f.done1;
-  // the next item index is fetched while the current tile runs
-  if (threadIdx.x == 0) item_s[0] = (int64_t)atomicAdd(f.work, 1ull);
-  __syncthreads();
-  for (int it = 0;; ++it) {
-    const int64_t idx = item_s[it & 1];
-    if (idx >= p3) break;
-    if (threadIdx.x == 0) item_s[(it + 1) & 1] = (int64_t)atomicAdd(f.work, 1ull);
-    bool first;
-    int64_t b, tile;
-    if (idx < p1) {
-      first = true, b = idx / t0, tile = idx % t0;
-    } else if (idx < p2) {
-      const int64_t r = idx - p1, s = D + r / (t0 + t1), q = r % (t0 + t1);
-      first = q < t0;
-      b = first ? s : s - D;
-      tile = first ? q : q - t0;
-    } else {
-      const int64_t r = idx - p2;
-      first = false, b = batch - D + r / t1, tile = r % t1;
-    }
-    const int64_t slot = b % R, gen = b / R;
-    if (threadIdx.x == 0) {
-      if (first) {
-        if (gen > 0)
-          while (ld_acquire_gpu(done1 + slot) < gen * t1) __nanosleep(32);
-      } else {
-        while (ld_acquire_gpu(done0 + slot) < (gen + 1) * t0) __nanosleep(32);
+
+  if (threadIdx.x >= CT) {  // ---------------- scheduler warp ----------------
+    const int lane = threadIdx.x & 31;
+    int64_t prev_slot[2] = {0, 0};
+    int prev_first[2] = {0, 0};
+    int k = 0;
+    auto publish = [&](int s) {  // item in descriptor slot s has been stored by the compute threads
+      named_sync(4 + s, ALL);
+      if (lane == 0) {
+        __threadfence();
+        red_release_gpu((prev_first[s] ? f.done0 : f.done1) + prev_slot[s], 1);
       }
+    };
+    for (;; ++k) {
+      const int s = k & 1;
+      if (k >= 2) publish(s);
+      int64_t idx = 0;
+      if (lane == 0) idx = (int64_t)atomicAdd(f.work, 1ull);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      if (idx >= p3) {
+        if (lane == 0) desc[s][0] = -1;
+        named_arrive(2 + s, ALL);
+        break;
+      }
+      bool first;
+      int64_t b, tile;
+      if (idx < p1) {
+        first = true, b = idx / t0, tile = idx % t0;
+      } else if (idx < p2) {
+        const int64_t r = idx - p1, st = D + r / (t0 + t1), q = r % (t0 + t1);
+        first = q < t0;
+        b = first ? st : st - D;
+        tile = first ? q : q - t0;
+      } else {
+        const int64_t r = idx - p2;
+        first = false, b = batch - D + r / t1, tile = r % t1;
+      }
+      const int64_t slot = b % R, gen = b / R;
+      if (lane == 0) {
+        if (first) {
+          if (gen > 0)
+            while (ld_acquire_gpu(f.done1 + slot) < gen * t1) __nanosleep(32);
+        } else {
+          while (ld_acquire_gpu(f.done0 + slot) < (gen + 1) * t0) __nanosleep(32);
+        }
+        desc[s][0] = b;
+        desc[s][1] = tile;
+        desc[s][2] = first;
+      }
+      __syncwarp();
+      prev_slot[s] = slot;
+      prev_first[s] = first;
+      named_arrive(2 + s, ALL);
     }
-    __syncthreads();
+    if (k >= 1) publish((k - 1) & 1);  // the last item still in flight
+    return;
+  }
+
+  // ------------------------------ compute threads ----------------------------
+  for (int k = 0;; ++k) {
+    const int s = k & 1;
+    named_sync(2 + s, ALL);
+    const int64_t b = desc[s][0], tile = desc[s][1];
+    const bool first = desc[s][2] != 0;
+    if (b < 0) break;
+    const int64_t slot = b % R;
     if (first)
-      group_tile<NS0, LIN, LAYOUT_RING, DIR, false>(f.g0, b * f.g0.idist, slot * f.n, tile, smem);
+      group_tile<NS0, LIN, LAYOUT_RING, DIR, false, typename FG::GG0, 1>(f.g0, b * f.g0.idist, slot * f.n, tile,
+                                                                         smem);
     else
-      group_tile<NS1, LAYOUT_RING, LOUT, DIR, true>(f.g1, slot * f.n, b * f.g1.odist, tile, smem);
-    // the barrier orders every thread's ring stores before thread 0's
-    // gpu-scope fence + release, which publishes them (cumulativity)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      red_release_gpu((first ? done0 : done1) + slot, 1);
-    }
+      group_tile<NS1, LAYOUT_RING, LOUT, DIR, true, typename FG::GG1, 1>(f.g1, slot * f.n, b * f.g1.odist, tile,
+                                                                         smem);
+    named_sync(1, CT);       // tile's smem reads done before the next tile writes it
+    named_arrive(4 + s, ALL);  // stores issued: the scheduler fences and publishes
   }
 }
 

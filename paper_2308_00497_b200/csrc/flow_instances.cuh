@@ -7,11 +7,7 @@
 
 namespace fftgen_b200 {
 
-template <int NS0, int NS1> struct FlowShape {
-  static constexpr int SMEM = GroupGeom<NS0>::BYTES > GroupGeom<NS1>::BYTES ? GroupGeom<NS0>::BYTES
-                                                                          : GroupGeom<NS1>::BYTES;
-  static constexpr int THREADS = GroupGeom<NS0>::THREADS;
-};
+template <int NS0, int NS1> using FlowShape = FlowGeom<NS0, NS1>;
 
 template <int NS0, int NS1, int DIR>
 cudaError_t flow_launch_t(int layout, const FlowArgs &f, int grid, cudaStream_t s) {
@@ -43,6 +39,7 @@ cudaError_t flow_prepare_t(int *bps) {
   case 7 * 16 + 7: return FN<128, 128, DIR>(__VA_ARGS__);            \
   case 7 * 16 + 8: return FN<128, 256, DIR>(__VA_ARGS__);            \
   case 8 * 16 + 8: return FN<256, 256, DIR>(__VA_ARGS__);            \
+  case 8 * 16 + 9: return FN<256, 512, DIR>(__VA_ARGS__);            \
   case 9 * 16 + 9: return FN<512, 512, DIR>(__VA_ARGS__);            \
   case 9 * 16 + 10: return FN<512, 1024, DIR>(__VA_ARGS__);         \
   case 10 * 16 + 10: return FN<1024, 1024, DIR>(__VA_ARGS__);        \

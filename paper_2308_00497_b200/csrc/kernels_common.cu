@@ -249,7 +249,8 @@ cudaError_t flow_prepare_b(int, int, int *);
 
 bool flow_supported(int l0, int l1) {
   switch (l0 * 16 + l1) {
-  case 7 * 16 + 7: case 7 * 16 + 8: case 8 * 16 + 8: case 9 * 16 + 9: case 9 * 16 + 10: case 10 * 16 + 10:
+  case 7 * 16 + 7: case 7 * 16 + 8: case 8 * 16 + 8: case 8 * 16 + 9: case 9 * 16 + 9: case 9 * 16 + 10:
+  case 10 * 16 + 10:
     return true;
   default:
     return false;
@@ -263,7 +264,7 @@ cudaError_t flow_prepare(int l0, int l1, int *bps, int *smem) {
   *bps = std::min(a, b);
   switch (l0 * 16 + l1) {
 #define FFTGEN_FS(A, B, NA, NB) case A * 16 + B: *smem = FlowShape<NA, NB>::SMEM; break;
-    FFTGEN_FS(7, 7, 128, 128) FFTGEN_FS(7, 8, 128, 256) FFTGEN_FS(8, 8, 256, 256)
+    FFTGEN_FS(7, 7, 128, 128) FFTGEN_FS(7, 8, 128, 256) FFTGEN_FS(8, 8, 256, 256) FFTGEN_FS(8, 9, 256, 512)
     FFTGEN_FS(9, 9, 512, 512) FFTGEN_FS(9, 10, 512, 1024) FFTGEN_FS(10, 10, 1024, 1024)
 #undef FFTGEN_FS
   default: *smem = 0;

@@ -80,6 +80,7 @@ struct ExecPlan {
 // 2^6..2^10 points).
 std::vector<int> group_split(int log2n);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
+int64_t flow_tile(int log2ns);
 
 ExecPlan build_exec_plan(int64_t n);
 

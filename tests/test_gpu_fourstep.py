@@ -152,7 +152,7 @@ def test_2p26_random_sampled_bins_and_roundtrip(fg, orc):
     assert np.abs(got - want).max() / scale < 1e-4
 
 
-@pytest.mark.parametrize("l2,batch", [(14, 700), (15, 400), (16, 200), (18, 40), (19, 20), (20, 9)])
+@pytest.mark.parametrize("l2,batch", [(14, 700), (15, 400), (16, 200), (17, 90), (18, 40), (19, 20), (20, 9)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 def test_dataflow_kernel_matches_two_launch_path(fg, orc, l2, batch, layout, monkeypatch):
     """The persistent dataflow kernel (both groups, L2 ring of slots reused
