@@ -191,8 +191,7 @@ template <int N> struct Tma1Geom {
 // K3 group kernel tile: TC adjacent transforms of size NS per CTA (~64 KB of
 // float2 in shared memory, <= 512 threads); odd per-transform stride REG so
 // lanes walking over the tile index f hit distinct bank pairs.
-// MAXT caps the compute threads per CTA (the dataflow kernel uses 256 so that
-// three CTAs plus their scheduler warps stay resident).
+// MAXT caps the threads per CTA.
 template <int NS, int MAXT = 512> struct GroupGeom {
   static constexpr int T = BlockGeom<NS>::T;
   static constexpr int TC_BYTES = 65536 / (8 * NS);                   // ~64 KB tiles

@@ -76,12 +76,10 @@ struct fftgen_plan {
   float2 *d_twg = nullptr;
   float2 *d_scratch = nullptr;
   size_t scratch_bytes = 0;
-  // K3 dataflow (both groups in one persistent launch, L2 ring of slots)
-  bool use_flow = false;
-  int flow_grid = 0;
-  int64_t flow_lag = 0, flow_ring = 0;
-  char *d_counters = nullptr;
-  size_t counter_bytes = 0;
+  // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
+  bool use_cluster = false;
+  int max_clusters = 0, cluster_size = 0;
+  std::mutex scratch_mu;  // lazy two-launch scratch of cluster plans (unaligned data)
   // L2-resident chunked execution of 2-group plans (0 = off)
   int64_t chunk = 0;
   cudaStream_t xs[2] = {nullptr, nullptr};
@@ -190,25 +188,28 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
   case STRAT_FOURSTEP: {
     const auto &gs = p->ex.groups;
     const bool split = layout == FFTGEN_LAYOUT_SPLIT;
-    if (p->use_flow) {
-      // one persistent launch for both groups, intermediate in the L2 ring
-      cudaError_t e = cudaMemsetAsync(p->d_counters, 0, p->counter_bytes, s);
+    const int64_t esz = split ? 4 : 8;
+    const bool rows_aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
+                              (dist * esz) % 16 == 0;
+    if (p->use_cluster && rows_aligned) {
+      // persistent clusters, one transform per cluster at a time; group-0
+      // tiles arrive by cp.async.bulk, the intermediate moves through DSMEM
+      ClusterArgs c{};
+      c.in0 = in0;
+      c.in1 = in1;
+      c.out0 = out0;
+      c.out1 = out1;
+      c.idist = dist;
+      c.odist = dist;
+      c.batch = batch;
+      c.tw_local0 = p->d_tw + gs[0].local_off;
+      c.tw_local1 = p->d_tw + gs[1].local_off;
+      c.tw_q = p->d_twg + gs[1].q_off;
+      c.tw_p = p->d_twg + gs[1].p_off;
+      cudaError_t e = cluster_encode_maps(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, c);
       if (e != cudaSuccess) return e;
-      FlowArgs f{};
-      f.g0 = make_group_args(p, 0, in0, in1, p->d_scratch, nullptr, dist, n);
-      f.g1 = make_group_args(p, 1, p->d_scratch, nullptr, out0, out1, n, dist);
-      f.n = n;
-      f.batch = batch;
-      f.lag = std::min<int64_t>(p->flow_lag, batch);
-      f.ring_slots = p->flow_ring;
-      f.tiles0 = n / gs[0].ns / flow_tile(gs[0].log2ns);
-      f.tiles1 = n / gs[1].ns / flow_tile(gs[1].log2ns);
-      f.work = reinterpret_cast<unsigned long long *>(p->d_counters);
-      f.done0 = reinterpret_cast<int *>(p->d_counters + 8);
-      f.done1 = f.done0 + p->flow_ring;
-      const int64_t items = batch * (f.tiles0 + f.tiles1);
-      const int grid = (int)std::min<int64_t>(items, p->flow_grid);
-      return flow_launch(gs[0].log2ns, gs[1].log2ns, layout, direction, f, grid, s);
+      return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
+                            p->max_clusters, s);
     }
     if (gs.size() == 2 && p->chunk > 0 && batch >= 2 * p->chunk) {
       // L2-resident chunking: group 0 of chunk c on xs[0], group 1 on xs[1];
@@ -241,6 +242,17 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
         if ((e = cudaStreamWaitEvent(s, p->ev_join[i], 0)) != cudaSuccess) return e;
       }
       return cudaSuccess;
+    }
+    if (p->use_cluster) {
+      // cp.async.bulk needs 16-byte aligned rows: unaligned data takes the
+      // two-launch path, whose scratch is allocated on first use
+      auto *mp = const_cast<fftgen_plan *>(p);
+      std::lock_guard<std::mutex> lk(mp->scratch_mu);
+      const size_t need = (size_t)p->ex.scratch_buffers * (size_t)p->cfg.batch * (size_t)n * sizeof(float2);
+      if (!mp->d_scratch) {
+        cudaError_t e = cudaMalloc(&mp->d_scratch, need);
+        if (e != cudaSuccess) return e;
+      }
     }
     // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
     const size_t per = (size_t)p->cfg.batch * (size_t)n;  // float2 per scratch buffer
@@ -348,7 +360,8 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     // same validation order as compile_pipeline -> plan_* -> fuse
     auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);
     auto radices = stockham_radices(cfg->n, cfg->radix);
-    ExecPlan ex = build_exec_plan(cfg->n);
+    const char *c14 = std::getenv("FFTGEN_CLUSTER14");
+    ExecPlan ex = build_exec_plan(cfg->n, c14 && c14[0] != '0');
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -414,40 +427,24 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         }
       }
       const auto &gs = p->ex.groups;
-      // opt-in: measured on B200 the dataflow kernel keeps the intermediate
-      // in L2 (DRAM bytes == 16 N) but its per-tile fence/atomic/dependency
-      // serialization makes it ~8% slower than the two-launch path at 2^16
-      const char *flow_env = std::getenv("FFTGEN_ENABLE_FLOW");
-      const char *no_flow = std::getenv("FFTGEN_DISABLE_FLOW");
-      const bool want_flow = flow_env && flow_env[0] != '0' && !(no_flow && no_flow[0] != '0');
-      if (gs.size() == 2 && flow_supported(gs[0].log2ns, gs[1].log2ns) && want_flow && p->chunk == 0) {
-        int bps = 0, smem = 0, sms = 0;
-        if ((e = flow_prepare(gs[0].log2ns, gs[1].log2ns, &bps, &smem)) != cudaSuccess ||
-            (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, std::string("dataflow kernel attributes: ") + cudaGetErrorString(e));
-        if (bps > 0) {
-          const int64_t resident = (int64_t)bps * sms;
-          const int64_t t0 = cfg->n / gs[0].ns / flow_tile(gs[0].log2ns);
-          const int64_t t1 = cfg->n / gs[1].ns / flow_tile(gs[1].log2ns);
-          // group 1 of b is dispatched LAG transforms after group 0 of b: far
-          // enough that the resident CTAs have finished it; a slot is reused
-          // R transforms later, after group 1 has drained it
-          double lag_mult = 2.0;
-          if (const char *env = std::getenv("FFTGEN_FLOW_LAG_MULT")) lag_mult = std::atof(env);
-          p->flow_lag = std::min<int64_t>(
-              cfg->batch, (int64_t)(lag_mult * (double)((resident + t0 + t1 - 1) / (t0 + t1))) + 1);
-          p->flow_ring = std::min<int64_t>(cfg->batch, 2 * p->flow_lag + 1);
-          p->flow_grid = (int)resident;
-          p->use_flow = true;
-          p->counter_bytes = 8 + 2 * (size_t)p->flow_ring * sizeof(int);
-          if ((e = cudaMalloc(&p->d_counters, p->counter_bytes)) != cudaSuccess)
-            return bail(FFTGEN_ERR_NOMEM, "dataflow counters");
-        }
+      const char *no_cluster = std::getenv("FFTGEN_DISABLE_CLUSTER");
+      // K5 where measured faster than K3 (cluster_default_size); FFTGEN_CLUSTER_SIZE=C
+      // forces any compiled (NS0, NS1, C) shape
+      int csize = gs.size() == 2 ? cluster_default_size(gs[0].log2ns, gs[1].log2ns, cfg->layout) : 0;
+      if (const char *env = std::getenv("FFTGEN_CLUSTER_SIZE"); env && gs.size() == 2) {
+        int64_t t = 0, sm = 0;
+        cluster_geom(gs[0].log2ns, gs[1].log2ns, std::atoi(env), &t, &sm);
+        if (t > 0) csize = std::atoi(env);
       }
-      p->scratch_bytes = p->use_flow ? (size_t)p->flow_ring * (size_t)cfg->n * sizeof(float2)
-                                     : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
+      if (csize > 0 && !(no_cluster && no_cluster[0] != '0')) {
+        p->cluster_size = csize;
+        if ((e = cluster_prepare(gs[0].log2ns, gs[1].log2ns, csize, &p->max_clusters)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, std::string("cluster kernel attributes: ") + cudaGetErrorString(e));
+        p->use_cluster = p->max_clusters > 0;
+      }
+      p->scratch_bytes = p->use_cluster ? 0 : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
                                            sizeof(float2);
-      if ((e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
+      if (p->scratch_bytes > 0 && (e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
                                           " bytes): " + cudaGetErrorString(e));
     }
@@ -472,7 +469,6 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
     if (p->d_scratch) cudaFree(p->d_scratch);
-    if (p->d_counters) cudaFree(p->d_counters);
     for (auto &x : p->xs)
       if (x) cudaStreamDestroy(x);
     for (cudaEvent_t ev : {p->ev_fork, p->ev_a[0], p->ev_a[1], p->ev_b[0], p->ev_b[1], p->ev_join[0], p->ev_join[1]})
@@ -620,7 +616,7 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return p->use_flow ? 1 : (int)p->ex.groups.size();
+  default: return p->use_cluster ? 1 : (int)p->ex.groups.size();
   }
 }
 
@@ -654,11 +650,15 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_FOURSTEP) {
-    if (p->use_flow)
-      o << "four-step: 1 fft_flow_kernel<" << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
-        << "> launch (persistent dataflow, grid " << p->flow_grid << ", lag " << p->flow_lag << ", L2 ring "
-        << p->flow_ring << " slots = " << p->scratch_bytes << " B)\n";
-    else
+    if (p->use_cluster) {
+      int64_t threads, smem;
+      const int64_t csize = p->cluster_size;
+      cluster_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, p->cluster_size, &threads, &smem);
+      o << "cluster: 1 fft_cluster_kernel<" << p->ex.groups[0].ns << "," << p->ex.groups[1].ns << "," << csize
+        << "> launch grid[" << p->cfg.batch * csize << "] cluster[" << csize << "] block[" << threads
+        << "] smem=" << smem << "B co-resident clusters=" << p->max_clusters
+        << " (persistent; one transform per cluster, intermediate in DSMEM, no scratch)\n";
+    } else
       o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
         << " B\n";
     for (size_t i = 0; i < p->ex.groups.size(); ++i) {

@@ -1,0 +1,5 @@
+// K5 cluster-kernel instances, direction=-1.
+#include "cluster_instances.cuh"
+namespace fftgen_b200 {
+FFTGEN_CLUSTER_INSTANCES(f, -1)
+}  // namespace fftgen_b200

@@ -39,7 +39,6 @@ namespace fftgen_b200 {
 // buffers: measured on B200, keeping it L2-resident through chunked
 // execution (FFTGEN_L2_CHUNK_BYTES) lost to the extra launches and tails.
 constexpr int LAYOUT_SCRATCH = 2;
-constexpr int LAYOUT_RING = 3;
 
 template <int L> struct SIO;
 template <> struct SIO<LAYOUT_INTERLEAVED> {
@@ -152,145 +151,6 @@ fft_group_kernel(const GroupArgs a) {
   const int64_t b = blockIdx.x / a.tiles_per_outer;
   const int64_t tt = blockIdx.x - b * a.tiles_per_outer;
   group_tile<NS, LIN, LOUT, DIR, ROWS>(a, b * a.idist, b * a.odist, tt, reinterpret_cast<float2 *>(smem_f4));
-}
-
-// ---- K3 dataflow: both groups of a 2-group plan in ONE persistent launch ----
-//
-// Work items (one tile each) are handed out in a fixed global order by an
-// atomic counter: group 0 of transform s, interleaved with group 1 of
-// transform s - LAG.  The intermediate of transform b lives in slot b % R of
-// a ring small enough to stay in the 126 MB L2, so HBM only sees the input
-// read and the output write (16 N bytes per transform) instead of 32 N.
-// Dependencies are per-slot tile counters (release / acquire at gpu scope):
-//   group 1 of b waits for all group-0 tiles of b,
-//   group 0 of b waits until group 1 of b - R has drained the slot.
-// Every wait targets an item dispatched earlier, and the grid never exceeds
-// the co-resident CTA count, so the schedule cannot deadlock.
-FFTGEN_FI int ld_acquire_gpu(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-FFTGEN_FI void red_release_gpu(int *p, int v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// ring traffic: plain (write-back) stores, L2-only loads (the slot of an
-// earlier generation may still sit in this SM's L1)
-template <> struct SIO<LAYOUT_RING> {
-  static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
-    return __ldcg(reinterpret_cast<const float2 *>(p0) + off);
-  }
-  static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
-    reinterpret_cast<float2 *>(p0)[off] = v;
-  }
-};
-
-// Warp-specialised persistent CTA: CT = 256 compute threads plus one
-// scheduler warp.  The scheduler fetches item k+1 (atomic), waits for its
-// dependency (acquire spin) and publishes item k-1 (fence + release) while
-// the compute threads work on item k; hand-offs use named barriers
-//   READY_s (2 + s): scheduler arrives, compute syncs  -- descriptor slot s filled
-//   DONE_s  (4 + s): compute arrives, scheduler syncs  -- item in slot s stored
-// and the compute threads synchronise among themselves on barrier 1.
-template <int NS0, int NS1> struct FlowGeom {
-  using GG0 = GroupGeom<NS0, 256>;
-  using GG1 = GroupGeom<NS1, 256>;
-  static_assert(GG0::THREADS == GG1::THREADS, "both groups share the compute shape");
-  static constexpr int CT = GG0::THREADS;
-  static constexpr int THREADS = CT + 32;
-  static constexpr int SMEM = GG0::BYTES > GG1::BYTES ? GG0::BYTES : GG1::BYTES;
-  // 32-register codelets (NS >= 512) need the 2-CTA register budget
-  static constexpr int MIN_BLOCKS = (NS0 >= 512 || NS1 >= 512) ? 2 : 3;
-};
-
-FFTGEN_FI void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-FFTGEN_FI void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int NS0, int NS1, int LIN, int LOUT, int DIR>
-__global__ void __launch_bounds__(FlowGeom<NS0, NS1>::THREADS, FlowGeom<NS0, NS1>::MIN_BLOCKS) fft_flow_kernel(const FlowArgs f) {
-  using FG = FlowGeom<NS0, NS1>;
-  constexpr int CT = FG::CT, ALL = FG::THREADS;
-  extern __shared__ float4 smem_f4[];
-  float2 *smem = reinterpret_cast<float2 *>(smem_f4);
-  __shared__ int64_t desc[2][3];  // {b, tile, first}; b < 0 marks the end
-  const int64_t t0 = f.tiles0, t1 = f.tiles1, D = f.lag, batch = f.batch, R = f.ring_slots;
-  const int64_t p1 = D * t0, p2 = p1 + (batch - D) * (t0 + t1), p3 = p2 + D * t1;
-
-  if (threadIdx.x >= CT) {  // ---------------- scheduler warp ----------------
-    const int lane = threadIdx.x & 31;
-    int64_t prev_slot[2] = {0, 0};
-    int prev_first[2] = {0, 0};
-    int k = 0;
-    auto publish = [&](int s) {  // item in descriptor slot s has been stored by the compute threads
-      named_sync(4 + s, ALL);
-      if (lane == 0) {
-        __threadfence();
-        red_release_gpu((prev_first[s] ? f.done0 : f.done1) + prev_slot[s], 1);
-      }
-    };
-    for (;; ++k) {
-      const int s = k & 1;
-      if (k >= 2) publish(s);
-      int64_t idx = 0;
-      if (lane == 0) idx = (int64_t)atomicAdd(f.work, 1ull);
-      idx = __shfl_sync(0xffffffffu, idx, 0);
-      if (idx >= p3) {
-        if (lane == 0) desc[s][0] = -1;
-        named_arrive(2 + s, ALL);
-        break;
-      }
-      bool first;
-      int64_t b, tile;
-      if (idx < p1) {
-        first = true, b = idx / t0, tile = idx % t0;
-      } else if (idx < p2) {
-        const int64_t r = idx - p1, st = D + r / (t0 + t1), q = r % (t0 + t1);
-        first = q < t0;
-        b = first ? st : st - D;
-        tile = first ? q : q - t0;
-      } else {
-        const int64_t r = idx - p2;
-        first = false, b = batch - D + r / t1, tile = r % t1;
-      }
-      const int64_t slot = b % R, gen = b / R;
-      if (lane == 0) {
-        if (first) {
-          if (gen > 0)
-            while (ld_acquire_gpu(f.done1 + slot) < gen * t1) __nanosleep(32);
-        } else {
-          while (ld_acquire_gpu(f.done0 + slot) < (gen + 1) * t0) __nanosleep(32);
-        }
-        desc[s][0] = b;
-        desc[s][1] = tile;
-        desc[s][2] = first;
-      }
-      __syncwarp();
-      prev_slot[s] = slot;
-      prev_first[s] = first;
-      named_arrive(2 + s, ALL);
-    }
-    if (k >= 1) publish((k - 1) & 1);  // the last item still in flight
-    return;
-  }
-
-  // ------------------------------ compute threads ----------------------------
-  for (int k = 0;; ++k) {
-    const int s = k & 1;
-    named_sync(2 + s, ALL);
-    const int64_t b = desc[s][0], tile = desc[s][1];
-    const bool first = desc[s][2] != 0;
-    if (b < 0) break;
-    const int64_t slot = b % R;
-    if (first)
-      group_tile<NS0, LIN, LAYOUT_RING, DIR, false, typename FG::GG0, 1>(f.g0, b * f.g0.idist, slot * f.n, tile,
-                                                                         smem);
-    else
-      group_tile<NS1, LAYOUT_RING, LOUT, DIR, true, typename FG::GG1, 1>(f.g1, slot * f.n, b * f.g1.odist, tile,
-                                                                         smem);
-    named_sync(1, CT);       // tile's smem reads done before the next tile writes it
-    named_arrive(4 + s, ALL);  // stores issued: the scheduler fences and publishes
-  }
 }
 
 }  // namespace fftgen_b200

@@ -88,15 +88,4 @@ void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_
   }
 }
 
-// tile width of the dataflow kernel's groups (256 compute threads)
-int64_t flow_tile(int log2ns) {
-  switch (log2ns) {
-  case 7: return GroupGeom<128, 256>::TC;
-  case 8: return GroupGeom<256, 256>::TC;
-  case 9: return GroupGeom<512, 256>::TC;
-  case 10: return GroupGeom<1024, 256>::TC;
-  default: return 0;
-  }
-}
-
 }  // namespace fftgen_b200

@@ -47,23 +47,37 @@ struct GroupArgs {
   const float2 *tw_p;      // [c][m]  = w_s^{c m}
 };
 
-// Both groups of a 2-group plan in one persistent launch (fft_flow_kernel):
-// group-0 output goes to slot b % ring_slots of an L2-resident ring.
-struct FlowArgs {
-  GroupArgs g0, g1;        // g0: user in -> ring; g1: ring -> user out
-  int64_t n, batch, lag, ring_slots, tiles0, tiles1;
-  unsigned long long *work;  // work-item counter (zeroed per launch)
-  int *done0, *done1;        // per-slot completed tiles of group 0 / group 1
-};
-bool flow_supported(int log2ns0, int log2ns1);
-cudaError_t flow_prepare(int log2ns0, int log2ns1, int *blocks_per_sm, int *smem_bytes);
-cudaError_t flow_launch(int log2ns0, int log2ns1, int layout, int dir, const FlowArgs &f, int grid, cudaStream_t s);
-
 // shape: 0 interleaved->scratch columns, 1 split->scratch columns,
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
 cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);
 cudaError_t group_prepare(int log2ns);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
+
+// K5: one transform per thread-block cluster, N = NS0 * NS1 (2^14 .. 2^17),
+// intermediate exchanged through distributed shared memory (fft_cluster.cuh).
+struct ClusterArgs {
+  // TMA tensor maps (CUtensorMap, 128 B each) of the input planes viewed as
+  // [batch][NS0][NS1] (re / interleaved, im): group-0 tiles are 2-D boxes
+  alignas(64) unsigned char tmap[2][128];
+  const void *in0, *in1;
+  void *out0, *out1;
+  int64_t idist, odist;
+  int64_t batch;
+  const float2 *tw_local0;  // NS0-point block-plan pass table
+  const float2 *tw_local1;  // NS1-point block-plan pass table
+  const float2 *tw_q;       // group 1: [A0][m] = w_N^{A0 (NS1/R0) m}
+  const float2 *tw_p;       // group 1: [c][m]  = w_N^{c m}
+};
+// default cluster size C of the (NS0, NS1) split for a layout, 0 = none
+int cluster_default_size(int log2ns0, int log2ns1, int layout);
+// *max_clusters: co-resident clusters (the persistent grid)
+cudaError_t cluster_prepare(int log2ns0, int log2ns1, int csize, int *max_clusters);
+cudaError_t cluster_launch(int log2ns0, int log2ns1, int csize, int layout, int dir, const ClusterArgs &a,
+                           int64_t batch, int max_clusters, cudaStream_t s);
+// threads / dynamic smem of a compiled (NS0, NS1, C) shape; 0 if not compiled
+void cluster_geom(int log2ns0, int log2ns1, int csize, int64_t *threads, int64_t *smem);
+// encode a.tmap for a.in0 / a.in1 (16-byte aligned planes, idist * element a multiple of 16)
+cudaError_t cluster_encode_maps(int log2ns0, int log2ns1, int csize, int layout, ClusterArgs &a);
 
 // K4: out[x*cols + m] = w_s^{x*row_scale*m}, fp64-accurate, rounded to fp32
 cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_scale, int64_t s, cudaStream_t st);

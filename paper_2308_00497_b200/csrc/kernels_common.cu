@@ -237,43 +237,99 @@ cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, 
 
 }  // namespace fftgen_b200
 
-// ---- K3 dataflow dispatch ---------------------------------------------------
-#include "flow_instances.cuh"
+// ---- K5 cluster dispatch -----------------------------------------------------
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "cluster_instances.cuh"
 
 namespace fftgen_b200 {
 
-cudaError_t flow_launch_f(int, int, int, const FlowArgs &, int, cudaStream_t);
-cudaError_t flow_launch_b(int, int, int, const FlowArgs &, int, cudaStream_t);
-cudaError_t flow_prepare_f(int, int, int *);
-cudaError_t flow_prepare_b(int, int, int *);
+cudaError_t cluster_launch_f(int, int, int, int, const ClusterArgs &, int64_t, int, cudaStream_t);
+cudaError_t cluster_launch_b(int, int, int, int, const ClusterArgs &, int64_t, int, cudaStream_t);
+cudaError_t cluster_prepare_f(int, int, int, int *);
+cudaError_t cluster_prepare_b(int, int, int, int *);
 
-bool flow_supported(int l0, int l1) {
+// Default cluster size per (l0, l1, layout), 0 = the two-launch K3 path.
+// Measured on B200 (scripts/sweep.py, 1 GiB batches, TFLOP/s K5 vs K3):
+//   2^15 C=8: split 13.8 vs 12.5, interleaved 14.5 vs 12.3
+//   2^16 C=16: split 12.9 vs 12.6, interleaved 13.7 vs 14.4
+//   2^17 C=16: split 10.4 vs 12.0, interleaved 10.7 vs 13.2
+// 2^14 (FFTGEN_CLUSTER14 plans) C=4: 14.6 vs 17.0 for the K2 block kernel.
+int cluster_default_size(int l0, int l1, int layout) {
   switch (l0 * 16 + l1) {
-  case 7 * 16 + 7: case 7 * 16 + 8: case 8 * 16 + 8: case 8 * 16 + 9: case 9 * 16 + 9: case 9 * 16 + 10:
-  case 10 * 16 + 10:
-    return true;
-  default:
-    return false;
+  case 7 * 16 + 7: return 4;
+  case 7 * 16 + 8: return 8;
+  case 8 * 16 + 8: return layout == LAYOUT_SPLIT ? 16 : 0;
+  default: return 0;
   }
 }
 
-cudaError_t flow_prepare(int l0, int l1, int *bps, int *smem) {
-  int a = 0, b = 0;
-  cudaError_t e = flow_prepare_f(l0, l1, &a);
-  if (e == cudaSuccess) e = flow_prepare_b(l0, l1, &b);
-  *bps = std::min(a, b);
-  switch (l0 * 16 + l1) {
-#define FFTGEN_FS(A, B, NA, NB) case A * 16 + B: *smem = FlowShape<NA, NB>::SMEM; break;
-    FFTGEN_FS(7, 7, 128, 128) FFTGEN_FS(7, 8, 128, 256) FFTGEN_FS(8, 8, 256, 256) FFTGEN_FS(8, 9, 256, 512)
-    FFTGEN_FS(9, 9, 512, 512) FFTGEN_FS(9, 10, 512, 1024) FFTGEN_FS(10, 10, 1024, 1024)
-#undef FFTGEN_FS
-  default: *smem = 0;
+void cluster_geom(int l0, int l1, int c, int64_t *threads, int64_t *smem) {
+  *threads = *smem = 0;
+  switch (FFTGEN_CLUSTER_KEY(l0, l1, c)) {
+#define FFTGEN_CG(A, B, NA, NB, C)                       \
+  case FFTGEN_CLUSTER_KEY(A, B, C):                      \
+    *threads = ClusterGeom<NA, NB, C>::THREADS;           \
+    *smem = ClusterGeom<NA, NB, C>::BYTES;                \
+    break;
+    FFTGEN_CLUSTER_SHAPES(FFTGEN_CG)
+#undef FFTGEN_CG
+  default: break;
   }
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+cudaError_t cluster_encode_maps(int l0, int l1, int csize, int layout, ClusterArgs &a) {
+  int64_t threads, smem;
+  cluster_geom(l0, l1, csize, &threads, &smem);
+  if (threads == 0) return cudaErrorInvalidValue;
+  auto enc = tensor_map_encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t ns0 = int64_t(1) << l0, ns1 = int64_t(1) << l1, tc0 = ns1 / csize;
+  const bool split = layout == LAYOUT_SPLIT;
+  const int64_t w = split ? 1 : 2;  // floats per element of a plane
+  // dims (innermost first): floats of a row, rows, transforms
+  cuuint64_t dims[3] = {(cuuint64_t)(ns1 * w), (cuuint64_t)ns0, (cuuint64_t)a.batch};
+  cuuint64_t strides[2] = {(cuuint64_t)(ns1 * w * 4), (cuuint64_t)(a.idist * w * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)(tc0 * w), (cuuint32_t)ns0, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const void *planes[2] = {a.in0, split ? a.in1 : a.in0};
+  for (int i = 0; i < (split ? 2 : 1); ++i) {
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(a.tmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                     const_cast<void *>(planes[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t cluster_prepare(int l0, int l1, int c, int *max_clusters) {
+  int a = 0, b = 0;
+  cudaError_t e = cluster_prepare_f(l0, l1, c, &a);
+  if (e == cudaSuccess) e = cluster_prepare_b(l0, l1, c, &b);
+  *max_clusters = a < b ? a : b;
   return e;
 }
 
-cudaError_t flow_launch(int l0, int l1, int layout, int dir, const FlowArgs &f, int grid, cudaStream_t s) {
-  return dir < 0 ? flow_launch_f(l0, l1, layout, f, grid, s) : flow_launch_b(l0, l1, layout, f, grid, s);
+cudaError_t cluster_launch(int l0, int l1, int c, int layout, int dir, const ClusterArgs &a, int64_t batch,
+                           int max_clusters, cudaStream_t s) {
+  return dir < 0 ? cluster_launch_f(l0, l1, c, layout, a, batch, max_clusters, s)
+                 : cluster_launch_b(l0, l1, c, layout, a, batch, max_clusters, s);
 }
 
 }  // namespace fftgen_b200

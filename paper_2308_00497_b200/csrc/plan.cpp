@@ -156,7 +156,7 @@ void op_map(const RefOp &op, int64_t n, int64_t *map, int64_t *s_out) {
   }
 }
 
-ExecPlan build_exec_plan(int64_t n) {
+ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
   if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
   ExecPlan p;
   p.n = n;
@@ -165,7 +165,7 @@ ExecPlan build_exec_plan(int64_t n) {
     p.strategy = STRAT_IDENTITY;
     return p;
   }
-  if (p.log2n <= 14) {
+  if (p.log2n <= 14 && !(fourstep_14 && p.log2n == 14)) {
     p.strategy = STRAT_BLOCK;
     const int np = block_num_passes(p.log2n);
     for (int q = 0; q < np; ++q) {

@@ -80,9 +80,10 @@ struct ExecPlan {
 // 2^6..2^10 points).
 std::vector<int> group_split(int log2n);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
-int64_t flow_tile(int log2ns);
 
-ExecPlan build_exec_plan(int64_t n);
+// fourstep_14: plan N = 2^14 as two 2^7-point groups (run by the K5 cluster
+// kernel) instead of the K2 block kernel.
+ExecPlan build_exec_plan(int64_t n, bool fourstep_14 = false);
 
 // K2 pass structure of an N-point block kernel (defined in kernels_common.cu
 // from the compile-time BlockPlan), and its [A][m] twiddle table in floats.

@@ -84,8 +84,12 @@ def test_fourstep_plan_shape(fg):
     assert p.launches() == 3
     assert p.scratch_bytes() == 2 * (1 << 24) * 8
     assert "transposed store" in p.describe()
-    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, batch=4))
-    assert [d[0] for d in q.passes()] == [256, 256] and q.scratch_bytes() == 4 * (1 << 16) * 8
+    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, layout="split", batch=4))
+    # split 2^16 runs as one cluster per transform: one launch, no HBM scratch
+    assert [d[0] for d in q.passes()] == [256, 256] and q.scratch_bytes() == 0 and q.launches() == 1
+    assert "fft_cluster_kernel<256,256,16>" in q.describe()
+    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, layout="interleaved", batch=4))
+    assert q.launches() == 2 and q.scratch_bytes() == 4 * (1 << 16) * 8
 
 
 def test_fourstep_host_and_interpret_paths(fg, orc):
@@ -152,44 +156,6 @@ def test_2p26_random_sampled_bins_and_roundtrip(fg, orc):
     assert np.abs(got - want).max() / scale < 1e-4
 
 
-@pytest.mark.parametrize("l2,batch", [(14, 700), (15, 400), (16, 200), (17, 90), (18, 40), (19, 20), (20, 9)])
-@pytest.mark.parametrize("layout", ["interleaved", "split"])
-def test_dataflow_kernel_matches_two_launch_path(fg, orc, l2, batch, layout, monkeypatch):
-    """The persistent dataflow kernel (both groups, L2 ring of slots reused
-    several times over the batch) is bitwise the two-launch path."""
-    n = 1 << l2
-    if l2 == 14:  # 2^14 runs on the block kernel by default; force the group split
-        pytest.skip("2^14 is planned on the K2 block kernel")
-    g = torch.Generator(device="cuda").manual_seed(l2)
-    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
-
-    def run_once(direction):
-        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
-        if layout == "interleaved":
-            y = torch.full_like(x, float("nan"))
-            plan.execute(x, y, direction=direction)
-        else:
-            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
-            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
-            plan.execute(re, ore, im, oim, direction=direction)
-            y = torch.stack([ore, oim], dim=-1)
-        torch.cuda.synchronize()
-        return y, plan
-
-    for direction in (-1, 1):
-        monkeypatch.setenv("FFTGEN_ENABLE_FLOW", "1")
-        flow, plan = run_once(direction)
-        monkeypatch.delenv("FFTGEN_ENABLE_FLOW")
-        assert "dataflow" in plan.describe()
-        plain, plan2 = run_once(direction)
-        assert "dataflow" not in plan2.describe()
-        assert torch.equal(flow, plain), direction
-    for b in (0, batch // 2, batch - 1):
-        xi = x[b].reshape(-1).double().cpu().numpy()
-        got = plain[b].reshape(-1).double().cpu().numpy()
-        assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4, inverse=True)) < 3e-6, b
-
-
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
     """Batched 2-group plans run in L2-sized chunks on two internal streams;
@@ -211,6 +177,8 @@ def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
         torch.cuda.synchronize()
         return y
 
+    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+    monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", str(32 << 20))
     chunked = run_once()
     monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", "0")
     plain = run_once()
@@ -220,3 +188,66 @@ def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
         xi = x[b].reshape(-1).double().cpu().numpy()
         got = chunked[b].reshape(-1).double().cpu().numpy()
         assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4)) < 3e-6, b
+
+
+@pytest.mark.parametrize("l2,batch,csize", [(14, 301, 2), (14, 301, 4), (15, 301, 4), (15, 301, 8),
+                                            (16, 150, 8), (16, 150, 16), (17, 77, 16)])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layout, direction, monkeypatch):
+    """K5 (persistent clusters, one transform per cluster, TMA tensor tiles in,
+    the intermediate exchanged through distributed shared memory) performs
+    exactly the arithmetic of the two-launch K3 path, so the results are
+    bitwise equal for every compiled cluster size; both match the oracle."""
+    n = 1 << l2
+    g = torch.Generator(device="cuda").manual_seed(100 + l2)
+    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
+    if l2 == 14:
+        monkeypatch.setenv("FFTGEN_CLUSTER14", "1")  # plan 2^14 as 2^7 x 2^7 groups
+
+    def run_once():
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+        if layout == "interleaved":
+            y = torch.full_like(x, float("nan"))
+            plan.execute(x, y, direction=direction)
+        else:
+            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+            plan.execute(re, ore, im, oim, direction=direction)
+            y = torch.stack([ore, oim], dim=-1)
+        torch.cuda.synchronize()
+        return y, plan.describe()
+
+    monkeypatch.setenv("FFTGEN_CLUSTER_SIZE", str(csize))
+    cl, d1 = run_once()
+    assert f"fft_cluster_kernel<{1 << (l2 // 2)},{1 << (l2 - l2 // 2)},{csize}>" in d1
+    monkeypatch.delenv("FFTGEN_CLUSTER_SIZE")
+    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+    two, d2 = run_once()
+    assert "fft_cluster_kernel" not in d2
+    assert torch.equal(cl, two)
+    for b in (0, batch // 2, batch - 1):
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        got = cl[b].reshape(-1).double().cpu().numpy()
+        want = orc.forward(xi, "stockham", 4, inverse=direction > 0)
+        assert oracle.rel_l2(got, want) < 3e-6, b
+
+
+def test_cluster_kernel_unaligned_rows_fall_back(fg, orc):
+    """TMA tensor tiles need 16-byte aligned rows: an odd element offset runs
+    the two-launch path on lazily allocated scratch, with the same result."""
+    n, batch = 1 << 15, 9
+    g = torch.Generator(device="cuda").manual_seed(5)
+    buf = torch.rand(batch * n * 2 + 2, device="cuda", generator=g) * 2 - 1
+    x = buf[2:].view(batch, n, 2)                    # 8-byte offset: not 16-byte aligned
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="interleaved", batch=batch))
+    assert "fft_cluster_kernel" in plan.describe()
+    y = torch.full((batch, n, 2), float("nan"), device="cuda")
+    plan.execute(x, y)
+    aligned = x.clone()
+    y2 = torch.full_like(y, float("nan"))
+    plan.execute(aligned, y2)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+    want = orc.forward(x[3].reshape(-1).double().cpu().numpy(), "stockham", 4)
+    assert oracle.rel_l2(y[3].reshape(-1).double().cpu().numpy(), want) < 3e-6
