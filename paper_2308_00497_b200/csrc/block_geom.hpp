@@ -202,7 +202,8 @@ template <int NS, int MAXT = 512> struct GroupGeom {
   static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
   static constexpr int BYTES = TC * REG * 8;
   // resident CTAs the register budget must allow (smem allows 3 at ~66 KB)
-  static constexpr int MIN_BLOCKS = THREADS >= 512 ? 2 : 3;
+  // 32-point codelets (NS >= 512: 64 registers of data) need the 2-CTA budget
+  static constexpr int MIN_BLOCKS = (THREADS >= 512 || BlockGeom<NS>::RMAX > 16) ? 2 : 3;
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };

@@ -89,7 +89,10 @@ struct fftgen_plan {
   std::mutex mu;
   void *d_stage = nullptr;
   size_t stage_bytes = 0;
-  cudaStream_t streams[2] = {nullptr, nullptr};
+  // host pipeline: chunk i uses slot / stream i % kHostSlots, so the H2D copy
+  // of one chunk overlaps the kernels and the D2H copy of the previous one
+  static constexpr int kHostSlots = 2;
+  cudaStream_t streams[kHostSlots] = {};
   // persistent TMA variant: resident CTAs on the device (0 = unavailable)
   int tma_grid = 0;
   bool use_tma = true;
@@ -278,18 +281,22 @@ size_t elem_bytes(const fftgen_plan *p) { return 8; }  // fp32 complex, either l
 template <class F>
 fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &&stage) {
   const int64_t batch = p->cfg.batch;
-  const int64_t target = int64_t(64) << 20;  // ~64 MiB per chunk and slot
+  constexpr int K = fftgen_plan::kHostSlots;
+  // ~64 MiB per chunk and slot.  Measured on B200 at N=4096 split (4 GiB of
+  // PCIe traffic per execute): 2 slots x 64 MiB 47.8 ms, 4 slots x 32 MiB
+  // 50.2 ms, against a 94.6 GB/s concurrent H2D+D2H ceiling (45.4 ms).
+  const int64_t target = int64_t(64) << 20;
   int64_t chunk = std::max<int64_t>(1, target / (int64_t)slot_bytes_per_transform);
   chunk = std::min(chunk, batch);
   const size_t slot = (size_t)chunk * slot_bytes_per_transform;
   cudaError_t e;
-  if (p->stage_bytes < 2 * slot) {
+  if (p->stage_bytes < K * slot) {
     if (p->d_stage) cudaFree(p->d_stage);
     p->d_stage = nullptr;
     p->stage_bytes = 0;
-    if ((e = cudaMalloc(&p->d_stage, 2 * slot)) != cudaSuccess)
+    if ((e = cudaMalloc(&p->d_stage, K * slot)) != cudaSuccess)
       return fail(FFTGEN_ERR_NOMEM, std::string("staging buffers: ") + cudaGetErrorString(e));
-    p->stage_bytes = 2 * slot;
+    p->stage_bytes = K * slot;
   }
   for (auto &s : p->streams)
     if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
@@ -297,9 +304,10 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
   int i = 0;
   for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++i) {
     const int64_t cnt = std::min(chunk, batch - b0);
-    char *slot_ptr = (char *)p->d_stage + (i & 1) * slot;
-    // four-step plans share one scratch buffer: keep their chunks stream-ordered
-    const int sid = p->ex.strategy == STRAT_FOURSTEP ? 0 : (i & 1);
+    char *slot_ptr = (char *)p->d_stage + (i % K) * slot;
+    // two-launch four-step plans share one scratch buffer: keep their chunks
+    // stream-ordered (the K5 cluster path has no scratch)
+    const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster) ? 0 : (i % K);
     if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) return cuda_fail(e, "host pipeline");
   }
   for (auto &s : p->streams)

@@ -1,6 +1,8 @@
 // plan.cpp -- host plan builder (see plan.hpp).
 #include "plan.hpp"
 
+#include <cstdlib>
+
 #include <cmath>
 #include <sstream>
 
@@ -222,9 +224,14 @@ ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
 }
 
 std::vector<int> group_split(int log2n) {
-  // 2 groups up to 2^20 (NS <= 2^10), 3 groups up to 2^27 (NS <= 2^9),
-  // 4 groups up to 2^30; sizes as even as possible, larger ones last
-  int g = log2n <= 20 ? 2 : (log2n <= 27 ? 3 : 4);
+  // 2 groups up to 2^20 (NS <= 2^10), 3 groups up to 2^28, 4 groups up to
+  // 2^30; sizes as even as possible, larger ones last.  Measured on B200:
+  // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
+  // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
+  // 64-byte segments).  FFTGEN_GROUP_MAX_LOG2=L allows 3 groups up to 2^(3L).
+  int max3 = 28;
+  if (const char *env = std::getenv("FFTGEN_GROUP_MAX_LOG2")) max3 = 3 * std::atoi(env);
+  int g = log2n <= 20 ? 2 : (log2n <= max3 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   for (int i = 0; i < log2n % g; ++i) out[g - 1 - i] += 1;
   return out;
