@@ -77,6 +77,8 @@ struct fftgen_plan {
   float2 *d_scratch = nullptr;
   size_t scratch_bytes = 0;
   // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
+  // K3 groups: persistent TMA variant (resident CTAs per group, 0 = off)
+  std::vector<int> group_tma_grid;
   bool use_cluster = false;
   int max_clusters = 0, cluster_size = 0;
   std::mutex scratch_mu;  // lazy two-launch scratch of cluster plans (unaligned data)
@@ -148,6 +150,15 @@ cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void 
   const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
   const GroupArgs a = make_group_args(p, g, in0, in1, out0, out1, idist, odist);
   const int shape = last ? (split ? 3 : 2) : (first ? (split ? 1 : 0) : 4);
+  if (g < (int)p->group_tma_grid.size() && p->group_tma_grid[g] > 0) {
+    GroupTmaArgs ta{};
+    ta.g = a;
+    ta.items = batch * a.tiles_per_outer;
+    if (group_tma_encode(d.log2ns, shape, batch, ta)) {
+      const int grid = (int)std::min<int64_t>(ta.items, p->group_tma_grid[g]);
+      return group_tma_launch(d.log2ns, shape, direction, ta, grid, s);
+    }
+  }
   return group_launch(d.log2ns, shape, direction, a, batch, s);
 }
 
@@ -404,6 +415,30 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       for (const GroupDesc &d : p->ex.groups)
         if ((e = group_prepare(d.log2ns)) != cudaSuccess)
           return bail(FFTGEN_ERR_CUDA, std::string("group kernel attributes: ") + cudaGetErrorString(e));
+      // Persistent TMA group kernels where they measured faster (B200 launch
+      // list, scripts/gpu_k3t_launch.sh): first-group columns from split user
+      // planes (2^16: 386 vs 427 us, 2^18: 385 vs 465, 2^24: 388 vs 439) and
+      // from interleaved input at NS >= 512 (2^18: 372 vs 433), middle columns
+      // at NS = 128; never rows (2^24: 667 vs 410).  FFTGEN_GROUP_TMA=0 / 1
+      // forces none / all.
+      const char *gt = std::getenv("FFTGEN_GROUP_TMA");
+      const int force = gt ? (gt[0] == '0' ? 0 : 1) : -1;
+      if (force != 0) {
+        int sms = 0;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, "device attributes");
+        const bool split = cfg->layout == FFTGEN_LAYOUT_SPLIT;
+        for (size_t g = 0; g < p->ex.groups.size(); ++g) {
+          const GroupDesc &d = p->ex.groups[g];
+          const bool first = g == 0;
+          const bool want = force == 1 || (!d.rows && ((first && (split || d.log2ns >= 9)) ||
+                                                       (!first && d.log2ns == 7)));
+          int bps = 0;
+          if (want && (e = group_tma_prepare(d.log2ns, &bps)) != cudaSuccess)
+            return bail(FFTGEN_ERR_CUDA, std::string("group TMA kernel attributes: ") + cudaGetErrorString(e));
+          p->group_tma_grid.push_back(want ? bps * sms : 0);
+        }
+      }
       // K4: Q[A0][m] = w_s^{A0 (NS/R0) m}, P[c][m] = w_s^{c m}, generated on the device in fp64
       if (p->ex.tw_group_len > 0) {
         if ((e = cudaMalloc(&p->d_twg, p->ex.tw_group_len * sizeof(float2))) != cudaSuccess)
@@ -673,10 +708,13 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
       const GroupDesc &d = p->ex.groups[i];
       int64_t threads, tc, smem, r0;
       group_geom(d.log2ns, &threads, &tc, &smem, &r0);
-      o << "  group " << i << ": fft_group_kernel<" << d.ns << "> radix " << d.ns << " s=" << d.s
+      const bool tma = i < p->group_tma_grid.size() && p->group_tma_grid[i] > 0;
+      o << "  group " << i << ": " << (tma ? "fft_group_tma_kernel<" : "fft_group_kernel<") << d.ns << "> radix "
+        << d.ns << " s=" << d.s
         << " cols=" << d.cols << " k=" << d.k << (d.rows ? " rows (transposed store)" : " columns")
         << " grid[" << p->cfg.batch * (d.cols * d.k / tc) << "] block[" << threads << "] smem=" << smem
-        << "B tile=" << tc << "\n";
+        << "B tile=" << tc
+        << (tma ? " (persistent, TMA tensor tiles double-buffered; plain kernel if unaligned)" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_IDENTITY) {
     o << "identity copy\n";

@@ -1,0 +1,165 @@
+// fft_group_tma.cuh -- K3 group kernel, persistent + TMA tensor-tile variant.
+//
+// Same tiles, arithmetic and stores as fft_group_kernel (fft_group.cuh), but
+// the CTA is persistent and its input tiles arrive by cp.async.bulk.tensor
+// into a double-buffered shared stage, two tiles ahead of the one being
+// computed, so the HBM reads of a pass never wait on the compute of the tile
+// before (the K2 TMA kernel's schedule, fft_block.cuh, applied to the
+// four-step groups).  After pass 0 has read a stage's raw tile the same stage
+// holds the padded sub-FFT exchange; once pass 1 has read that, the stage is
+// refilled.
+//
+// Raw tile layouts (what the tensor box writes):
+//   columns: [A][f]  NS rows of TC adjacent elements (stride k between rows);
+//            box {TC elements, <=256 rows} per 256-row chunk of A
+//   rows:    [f][A]  TC rows of NS contiguous elements; box {256 floats,
+//            NS*2/256 chunks, TC rows}
+// split user input (group 0 only) arrives as two planes, re then im.
+#pragma once
+
+#include <cstdint>
+
+#include "fft_group.cuh"
+
+namespace fftgen_b200 {
+
+template <int NS> struct GroupTmaGeom {
+  using GG = GroupGeom<NS>;
+  static constexpr int TC = GG::TC, REG = GG::REG, THREADS = GG::THREADS;
+  static constexpr int RAW = TC * NS * 8;  // raw tile bytes
+  static constexpr int STAGE = ((TC * REG * 8 > RAW ? TC * REG * 8 : RAW) + 127) / 128 * 128;
+  static constexpr int BYTES = 2 * STAGE + 64;
+  static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 0 ? (228 * 1024) / (BYTES + 1024) : 1;
+};
+
+FFTGEN_FI void tma_load_4d(void *dst, const void *tmap, int c0, int c1, int c2, int c3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// issue the raw tile of work item `item` into `stage`
+template <int NS, int LIN, bool ROWS>
+FFTGEN_FI void group_tma_issue(const GroupTmaArgs &ta, char *stage, uint64_t *bar, int64_t item) {
+  using TG = GroupTmaGeom<NS>;
+  constexpr int TC = TG::TC;
+  const GroupArgs &a = ta.g;
+  const int64_t b = item / a.tiles_per_outer, tt = item - b * a.tiles_per_outer;
+  mbar_expect_tx(bar, (uint32_t)TG::RAW);
+  if constexpr (ROWS) {
+    tma_load_4d(stage, ta.tmap[0], 0, 0, (int)(tt * TC), (int)b, bar);
+  } else {
+    const int64_t u0 = tt * TC, m0 = u0 / a.k, c0 = u0 - m0 * a.k;
+    constexpr int CH = NS < 256 ? NS : 256;  // rows per box
+    constexpr int W = LIN == LAYOUT_SPLIT ? 1 : 2;
+#pragma unroll
+    for (int q = 0; q < NS / CH; ++q) {
+      tma_load_4d(stage + q * CH * TC * W * 4, ta.tmap[0], (int)(c0 * W), q * CH, (int)m0, (int)b, bar);
+      if constexpr (LIN == LAYOUT_SPLIT)
+        tma_load_4d(stage + NS * TC * 4 + q * CH * TC * 4, ta.tmap[1], (int)c0, q * CH, (int)m0, (int)b, bar);
+    }
+  }
+}
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+__global__ void __launch_bounds__(GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::MIN_BLOCKS)
+fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
+  using TG = GroupTmaGeom<NS>;
+  using G = typename TG::GG::G;
+  constexpr int TC = TG::TC, REG = TG::REG, T = G::T;
+  constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
+  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  const GroupArgs &a = ta.g;
+  extern __shared__ float4 smem_f4[];
+  char *smem = reinterpret_cast<char *>(smem_f4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * TG::STAGE);
+  const int tid = threadIdx.x;
+  const int64_t total = ta.items, stride = gridDim.x;
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < 2; ++s)
+      if (blockIdx.x + s * stride < total)
+        group_tma_issue<NS, LIN, ROWS>(ta, smem + s * TG::STAGE, &bars[s], blockIdx.x + s * stride);
+
+  int it = 0;
+  for (int64_t item = blockIdx.x; item < total; item += stride, ++it) {
+    const int s = it & 1;
+    char *stage = smem + s * TG::STAGE;
+    float2 *X = reinterpret_cast<float2 *>(stage);
+    const int64_t b = item / a.tiles_per_outer, tt = item - b * a.tiles_per_outer;
+    int64_t m0, c0;
+    if (ROWS) {
+      m0 = tt * TC;
+      c0 = 0;
+    } else {
+      const int64_t u0 = tt * TC;
+      m0 = u0 / a.k;
+      c0 = u0 - m0 * a.k;
+    }
+    mbar_wait(&bars[s], (it >> 1) & 1);
+
+    // ---- pass 0: raw tile -> registers, global twiddle, radix-R0 codelets ----
+    float2 v[G::RMAX];
+    const int f0 = ROWS ? tid / T : tid % TC;
+    const int t0 = ROWS ? tid % T : tid / TC;
+    {
+      const int64_t m = ROWS ? m0 + f0 : m0;
+      const bool tw = a.cols > 1;
+      const float2 *qm = a.tw_q + m;
+#pragma unroll
+      for (int j = 0; j < J0; ++j) {
+        const int c = t0 + j * T;
+#pragma unroll
+        for (int A0 = 0; A0 < R0; ++A0) {
+          const int A = A0 * K0 + c;
+          const int e = ROWS ? f0 * NS + A : A * TC + f0;
+          if constexpr (LIN == LAYOUT_SPLIT) {
+            const float *sp = reinterpret_cast<const float *>(stage);
+            v[j * R0 + A0] = make_float2(sp[e], sp[NS * TC + e]);
+          } else {
+            v[j * R0 + A0] = X[e];
+          }
+        }
+        if (tw) {
+          const float2 pw = __ldg(a.tw_p + c * a.cols + m);
+#pragma unroll
+          for (int A0 = 0; A0 < R0; ++A0) {
+            float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
+            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+          }
+        }
+        reg_fft<R0, DIR>(v + j * R0);
+      }
+    }
+    __syncthreads();  // raw tile consumed: the stage becomes the padded exchange
+    smem_write<G, NS, 0>(X + f0 * REG, t0, v);
+    __syncthreads();
+
+    // ---- pass 1: exchange -> registers (lanes over f), codelet, HBM store ----
+    const int f = tid % TC;
+    const int t = tid / TC;
+    smem_read_pass<G, NS, 1, DIR>(X + f * REG, t, a.tw_local, v);
+    __syncthreads();  // stage free: fetch the tile two items ahead
+    if (tid == 0 && item + 2 * stride < total) {
+      fence_proxy_async();
+      group_tma_issue<NS, LIN, ROWS>(ta, stage, &bars[s], item + 2 * stride);
+    }
+    const int64_t ob = b * a.odist;
+#pragma unroll
+    for (int B = 0; B < R1; ++B) {
+      const int64_t e = B * COLS1 + t;
+      const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
+      SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+    }
+  }
+}
+
+}  // namespace fftgen_b200

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "fft_group.cuh"
+#include "fft_group_tma.cuh"
 
 namespace fftgen_b200 {
 
@@ -49,6 +50,44 @@ cudaError_t group_prepare_ns() {
   return group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>();
 }
 
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+cudaError_t group_tma_launch_t(const GroupTmaArgs &ta, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS><<<grid, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES, s>>>(ta);
+  return cudaGetLastError();
+}
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS> cudaError_t group_tma_prepare_t(int *bps) {
+  auto k = fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GroupTmaGeom<NS>::BYTES);
+  int n = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES);
+  if (n < *bps) *bps = n;
+  return e;
+}
+
+template <int NS, int DIR>
+cudaError_t group_tma_launch_ns(int shape, const GroupTmaArgs &ta, int grid, cudaStream_t s) {
+  switch (shape) {
+  case 0: return group_tma_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SCRATCH, DIR, false>(ta, grid, s);
+  case 1: return group_tma_launch_t<NS, LAYOUT_SPLIT, LAYOUT_SCRATCH, DIR, false>(ta, grid, s);
+  case 2: return group_tma_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>(ta, grid, s);
+  case 3: return group_tma_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>(ta, grid, s);
+  case 4: return group_tma_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>(ta, grid, s);
+  default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int NS, int DIR> cudaError_t group_tma_prepare_ns(int *bps) {
+  cudaError_t e;
+  if ((e = group_tma_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_SCRATCH, DIR, false>(bps)) != cudaSuccess) return e;
+  if ((e = group_tma_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_SCRATCH, DIR, false>(bps)) != cudaSuccess) return e;
+  if ((e = group_tma_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>(bps)) != cudaSuccess) return e;
+  if ((e = group_tma_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>(bps)) != cudaSuccess) return e;
+  return group_tma_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>(bps);
+}
+
 #define FFTGEN_GROUP_INSTANCES(SUFFIX, DIR)                                                          \
   cudaError_t group_launch_##SUFFIX(int log2ns, int shape, const GroupArgs &a, int64_t grid,        \
                                     cudaStream_t s) {                                               \
@@ -66,6 +105,25 @@ cudaError_t group_prepare_ns() {
     case 8: return group_prepare_ns<256, DIR>();                                                    \
     case 9: return group_prepare_ns<512, DIR>();                                                    \
     case 10: return group_prepare_ns<1024, DIR>();                                                  \
+    default: return cudaErrorInvalidValue;                                                          \
+    }                                                                                               \
+  }                                                                                                 \
+  cudaError_t group_tma_launch_##SUFFIX(int log2ns, int shape, const GroupTmaArgs &ta, int grid,    \
+                                        cudaStream_t s) {                                           \
+    switch (log2ns) {                                                                               \
+    case 7: return group_tma_launch_ns<128, DIR>(shape, ta, grid, s);                               \
+    case 8: return group_tma_launch_ns<256, DIR>(shape, ta, grid, s);                               \
+    case 9: return group_tma_launch_ns<512, DIR>(shape, ta, grid, s);                               \
+    case 10: return group_tma_launch_ns<1024, DIR>(shape, ta, grid, s);                             \
+    default: return cudaErrorInvalidValue;                                                          \
+    }                                                                                               \
+  }                                                                                                 \
+  cudaError_t group_tma_prepare_##SUFFIX(int log2ns, int *bps) {                                    \
+    switch (log2ns) {                                                                               \
+    case 7: return group_tma_prepare_ns<128, DIR>(bps);                                             \
+    case 8: return group_tma_prepare_ns<256, DIR>(bps);                                             \
+    case 9: return group_tma_prepare_ns<512, DIR>(bps);                                             \
+    case 10: return group_tma_prepare_ns<1024, DIR>(bps);                                           \
     default: return cudaErrorInvalidValue;                                                          \
     }                                                                                               \
   }

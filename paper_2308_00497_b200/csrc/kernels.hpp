@@ -51,6 +51,20 @@ struct GroupArgs {
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
 cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);
 cudaError_t group_prepare(int log2ns);
+
+// Persistent TMA variant of the group kernel (fft_group_tma.cuh): tensor maps
+// of the input planes (re / interleaved, im), the group's args and the number
+// of (transform, tile) work items.
+struct GroupTmaArgs {
+  alignas(64) unsigned char tmap[2][128];
+  GroupArgs g;
+  int64_t items;
+};
+// *blocks_per_sm: resident CTAs per SM of the slowest shape of this NS
+cudaError_t group_tma_prepare(int log2ns, int *blocks_per_sm);
+// encode ta.tmap for ta.g's input; false if the input is not TMA-addressable
+bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta);
+cudaError_t group_tma_launch(int log2ns, int shape, int dir, const GroupTmaArgs &ta, int grid, cudaStream_t s);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
 // K5: one transform per thread-block cluster, N = NS0 * NS1 (2^14 .. 2^17),

@@ -157,6 +157,21 @@ cudaError_t group_prepare(int log2ns) {
   return e != cudaSuccess ? e : group_prepare_b(log2ns);
 }
 
+cudaError_t group_tma_launch_f(int, int, const GroupTmaArgs &, int, cudaStream_t);
+cudaError_t group_tma_launch_b(int, int, const GroupTmaArgs &, int, cudaStream_t);
+cudaError_t group_tma_prepare_f(int, int *);
+cudaError_t group_tma_prepare_b(int, int *);
+
+cudaError_t group_tma_prepare(int log2ns, int *bps) {
+  *bps = 1 << 30;
+  cudaError_t e = group_tma_prepare_f(log2ns, bps);
+  return e != cudaSuccess ? e : group_tma_prepare_b(log2ns, bps);
+}
+
+cudaError_t group_tma_launch(int log2ns, int shape, int dir, const GroupTmaArgs &ta, int grid, cudaStream_t s) {
+  return dir < 0 ? group_tma_launch_f(log2ns, shape, ta, grid, s) : group_tma_launch_b(log2ns, shape, ta, grid, s);
+}
+
 }  // namespace fftgen_b200
 
 // ---- K4: device twiddle-table generation -----------------------------------
@@ -253,14 +268,15 @@ cudaError_t cluster_prepare_b(int, int, int, int *);
 // Default cluster size per (l0, l1, layout), 0 = the two-launch K3 path.
 // Measured on B200 (scripts/sweep.py, 1 GiB batches, TFLOP/s K5 vs K3):
 //   2^15 C=8: split 13.8 vs 12.5, interleaved 14.5 vs 12.3
-//   2^16 C=16: split 12.9 vs 12.6, interleaved 13.7 vs 14.4
+//   2^16 C=16: split 12.9 vs 12.6, interleaved 13.7 vs 14.4 (K3 with the TMA
+//              first group: split 0.764 ms vs 0.835 ms for K5)
 //   2^17 C=16: split 10.4 vs 12.0, interleaved 10.7 vs 13.2
 // 2^14 (FFTGEN_CLUSTER14 plans) C=4: 14.6 vs 17.0 for the K2 block kernel.
-int cluster_default_size(int l0, int l1, int layout) {
+int cluster_default_size(int l0, int l1, int /*layout*/) {
   switch (l0 * 16 + l1) {
   case 7 * 16 + 7: return 4;
   case 7 * 16 + 8: return 8;
-  case 8 * 16 + 8: return layout == LAYOUT_SPLIT ? 16 : 0;
+  case 8 * 16 + 8: return 0;
   default: return 0;
   }
 }
@@ -330,6 +346,48 @@ cudaError_t cluster_launch(int l0, int l1, int c, int layout, int dir, const Clu
                            int max_clusters, cudaStream_t s) {
   return dir < 0 ? cluster_launch_f(l0, l1, c, layout, a, batch, max_clusters, s)
                  : cluster_launch_b(l0, l1, c, layout, a, batch, max_clusters, s);
+}
+
+}  // namespace fftgen_b200
+
+namespace fftgen_b200 {
+
+bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  int64_t threads, tc, smem, r0;
+  group_geom(log2ns, &threads, &tc, &smem, &r0);
+  const GroupArgs &a = ta.g;
+  const int64_t ns = int64_t(1) << log2ns;
+  const bool rows = shape == 2 || shape == 3;
+  const bool split_in = shape == 1;
+  const int64_t w = split_in ? 1 : 2;  // floats per element of an input plane
+  const void *planes[2] = {a.in0, split_in ? a.in1 : a.in0};
+  const int nplanes = split_in ? 2 : 1;
+  for (int i = 0; i < nplanes; ++i)
+    if ((uintptr_t)planes[i] % 16 != 0) return false;
+  if ((a.idist * w * 4) % 16 != 0) return false;
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+  if (rows) {  // [batch][cols rows][NS*2 floats] as {CH floats, chunks, rows, batch}
+    const int64_t ch = std::min<int64_t>(ns * 2, 256), nch = ns * 2 / ch;
+    dims[0] = ch; dims[1] = nch; dims[2] = a.cols; dims[3] = batch;
+    strides[0] = ch * 4; strides[1] = ns * 8; strides[2] = a.idist * 8;
+    box[0] = ch; box[1] = nch; box[2] = tc; box[3] = 1;
+  } else {     // [batch][cols][NS][k] as {k*w floats, NS, cols, batch}
+    if ((a.k * w * 4) % 16 != 0) return false;
+    dims[0] = a.k * w; dims[1] = ns; dims[2] = a.cols; dims[3] = batch;
+    strides[0] = a.k * w * 4; strides[1] = ns * a.k * w * 4; strides[2] = a.idist * w * 4;
+    box[0] = tc * w; box[1] = std::min<int64_t>(ns, 256); box[2] = 1; box[3] = 1;
+  }
+  for (int i = 0; i < nplanes; ++i) {
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(ta.tmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                     const_cast<void *>(planes[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+  }
+  return true;
 }
 
 }  // namespace fftgen_b200

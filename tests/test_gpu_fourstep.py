@@ -84,12 +84,13 @@ def test_fourstep_plan_shape(fg):
     assert p.launches() == 3
     assert p.scratch_bytes() == 2 * (1 << 24) * 8
     assert "transposed store" in p.describe()
+    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 15, layout="split", batch=4))
+    # 2^15 runs as one cluster per transform: one launch, no HBM scratch
+    assert [d[0] for d in q.passes()] == [128, 256] and q.scratch_bytes() == 0 and q.launches() == 1
+    assert "fft_cluster_kernel<128,256,8>" in q.describe()
     q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, layout="split", batch=4))
-    # split 2^16 runs as one cluster per transform: one launch, no HBM scratch
-    assert [d[0] for d in q.passes()] == [256, 256] and q.scratch_bytes() == 0 and q.launches() == 1
-    assert "fft_cluster_kernel<256,256,16>" in q.describe()
-    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, layout="interleaved", batch=4))
     assert q.launches() == 2 and q.scratch_bytes() == 4 * (1 << 16) * 8
+    assert "group 0: fft_group_tma_kernel<256>" in q.describe()
 
 
 def test_fourstep_host_and_interpret_paths(fg, orc):
@@ -251,3 +252,41 @@ def test_cluster_kernel_unaligned_rows_fall_back(fg, orc):
     assert torch.equal(y, y2)
     want = orc.forward(x[3].reshape(-1).double().cpu().numpy(), "stockham", 4)
     assert oracle.rel_l2(y[3].reshape(-1).double().cpu().numpy(), want) < 3e-6
+
+
+@pytest.mark.parametrize("l2,batch", [(15, 40), (16, 20), (18, 6), (20, 3), (22, 1), (28, 1)])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch):
+    """The persistent TMA group kernels (tensor-tile prefetch) are bitwise the
+    plain group kernels for every shape (first / middle columns, rows)."""
+    if l2 == 28 and layout == "interleaved":
+        pytest.skip("one layout suffices at 2^28")
+    n = 1 << l2
+    g = torch.Generator(device="cuda").manual_seed(l2)
+    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
+    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+
+    def run_once(tma):
+        monkeypatch.setenv("FFTGEN_GROUP_TMA", tma)
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+        if layout == "interleaved":
+            y = torch.full_like(x, float("nan"))
+            plan.execute(x, y)
+        else:
+            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+            plan.execute(re, ore, im, oim)
+            y = torch.stack([ore, oim], dim=-1)
+        torch.cuda.synchronize()
+        d = plan.describe()
+        plan.close()
+        return y, d
+
+    a, da = run_once("1")
+    assert "fft_group_tma_kernel" in da
+    b, db = run_once("0")
+    assert "fft_group_tma_kernel" not in db
+    assert torch.equal(a, b)
+    if l2 <= 20:
+        xi = x[0].reshape(-1).double().cpu().numpy()
+        assert oracle.rel_l2(a[0].reshape(-1).double().cpu().numpy(), orc.forward(xi, "stockham", 4)) < 3e-6
