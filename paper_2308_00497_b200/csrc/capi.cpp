@@ -75,11 +75,17 @@ struct fftgen_plan {
   // K3 four-step: device-generated group twiddles and intermediate buffers
   float2 *d_twg = nullptr;
   float2 *d_scratch = nullptr;
+  float2 *d_fallback = nullptr;  // full-batch scratch of cluster / phased plans, on first unaligned execute
   size_t scratch_bytes = 0;
   // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
   // K3 groups: persistent TMA variant (resident CTAs per group, 0 = off)
   std::vector<int> group_tma_grid;
   bool use_cluster = false;
+  // K6: 2-group plans in one cooperative launch, intermediate in two L2 slots
+  bool use_phased = false;
+  int phased_grid = 0;
+  int64_t phased_chunk = 0;
+  int *d_done = nullptr;  // per-chunk completed tiles of group 0 and group 1
   int max_clusters = 0, cluster_size = 0;
   std::mutex scratch_mu;  // lazy two-launch scratch of cluster plans (unaligned data)
   // L2-resident chunked execution of 2-group plans (0 = off)
@@ -225,6 +231,26 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
                             p->max_clusters, s);
     }
+    if (p->use_phased) {
+      // one cooperative launch; chunks stream through two L2-resident slots
+      PhasedArgs pa{};
+      pa.g0 = make_group_args(p, 0, in0, in1, p->d_scratch, nullptr, dist, n);
+      pa.g1 = make_group_args(p, 1, p->d_scratch, nullptr, out0, out1, n, dist);
+      pa.batch = batch;
+      pa.chunk = std::min<int64_t>(p->phased_chunk, batch);
+      pa.done = p->d_done;
+      int64_t threads, smem, t0, t1;
+      phased_geom(gs[0].log2ns, gs[1].log2ns, &threads, &smem, &t0, &t1);
+      const int64_t nchunks = (batch + pa.chunk - 1) / pa.chunk;
+      if (encode_tile_maps(pa.g0, gs[0].log2ns, split ? 1 : 0, batch, gs[1].ns / t0, pa.tmap0) &&
+          encode_tile_maps(pa.g1, gs[1].log2ns, 2, kPhasedSlots * pa.chunk, gs[0].ns / t1,
+                           reinterpret_cast<unsigned char(*)[128]>(pa.tmap1))) {
+        cudaError_t e = cudaMemsetAsync(p->d_done, 0, 2 * nchunks * sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        const int grid = (int)std::min<int64_t>(p->phased_grid, batch * (t0 + t1));
+        return phased_launch(gs[0].log2ns, gs[1].log2ns, layout, direction, pa, grid, s);
+      }
+    }
     if (gs.size() == 2 && p->chunk > 0 && batch >= 2 * p->chunk) {
       // L2-resident chunking: group 0 of chunk c on xs[0], group 1 on xs[1];
       // the intermediate of a chunk (<= 2 slots live) is read back from L2.
@@ -257,23 +283,25 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       }
       return cudaSuccess;
     }
-    if (p->use_cluster) {
-      // cp.async.bulk needs 16-byte aligned rows: unaligned data takes the
-      // two-launch path, whose scratch is allocated on first use
+    float2 *scratch = p->d_scratch;
+    if (p->use_cluster || p->use_phased) {
+      // TMA tiles need 16-byte aligned rows: unaligned data takes the
+      // two-launch path, whose full-batch scratch is allocated on first use
       auto *mp = const_cast<fftgen_plan *>(p);
       std::lock_guard<std::mutex> lk(mp->scratch_mu);
       const size_t need = (size_t)p->ex.scratch_buffers * (size_t)p->cfg.batch * (size_t)n * sizeof(float2);
-      if (!mp->d_scratch) {
-        cudaError_t e = cudaMalloc(&mp->d_scratch, need);
+      if (!mp->d_fallback) {
+        cudaError_t e = cudaMalloc(&mp->d_fallback, need);
         if (e != cudaSuccess) return e;
       }
+      scratch = mp->d_fallback;
     }
     // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
     const size_t per = (size_t)p->cfg.batch * (size_t)n;  // float2 per scratch buffer
     for (size_t g = 0; g < gs.size(); ++g) {
       const bool first = g == 0, last = g + 1 == gs.size();
-      float2 *src = first ? nullptr : p->d_scratch + ((g - 1) % p->ex.scratch_buffers) * per;
-      float2 *dst = last ? nullptr : p->d_scratch + (g % p->ex.scratch_buffers) * per;
+      float2 *src = first ? nullptr : scratch + ((g - 1) % p->ex.scratch_buffers) * per;
+      float2 *dst = last ? nullptr : scratch + (g % p->ex.scratch_buffers) * per;
       cudaError_t e = launch_group(p, (int)g, direction, first ? in0 : src, first ? in1 : nullptr,
                                    last ? out0 : dst, last ? out1 : nullptr, first ? dist : n, last ? dist : n,
                                    batch, s);
@@ -485,7 +513,35 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           return bail(FFTGEN_ERR_CUDA, std::string("cluster kernel attributes: ") + cudaGetErrorString(e));
         p->use_cluster = p->max_clusters > 0;
       }
-      p->scratch_bytes = p->use_cluster ? 0 : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
+      // K6 phased kernel (opt-in, FFTGEN_PHASED=1).  Measured on B200 it keeps
+      // DRAM bytes at exactly 16 N per transform (the intermediate never leaves
+      // L2), but runs below the two-launch K3 path: 2^16 0.29 vs 0.43, 2^18
+      // 0.28 vs 0.41, 2^20 0.25 vs 0.35 of the single-pass roofline.  K3's
+      // passes are bound by the per-tile processing rate of one 16-warp CTA per
+      // SM (3.5 us per 64 KB tile at 2^16), not by HBM, so halving the HBM
+      // bytes of a tile does not shorten it.
+      const char *ph = std::getenv("FFTGEN_PHASED");
+      if (gs.size() == 2 && !p->use_cluster && phased_supported(gs[0].log2ns, gs[1].log2ns) && ph &&
+          ph[0] == '1') {
+        int bps = 0, sms = 0;
+        if ((e = phased_prepare(gs[0].log2ns, gs[1].log2ns, &bps)) != cudaSuccess ||
+            (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, std::string("phased kernel attributes: ") + cudaGetErrorString(e));
+        if (bps > 0) {
+          int64_t slot_mb = 16;
+          if (const char *env = std::getenv("FFTGEN_PHASE_SLOT_MB")) slot_mb = std::max<int64_t>(1, std::atoll(env));
+          p->phased_chunk = std::min<int64_t>(cfg->batch, std::max<int64_t>(1, (slot_mb << 20) / (cfg->n * 8)));
+          p->phased_grid = bps * sms;
+          p->use_phased = true;
+          p->chunk = 0;
+          const int64_t nchunks = (cfg->batch + p->phased_chunk - 1) / p->phased_chunk;
+          if ((e = cudaMalloc(&p->d_done, 2 * nchunks * sizeof(int))) != cudaSuccess)
+            return bail(FFTGEN_ERR_NOMEM, "chunk counters");
+        }
+      }
+      p->scratch_bytes = p->use_cluster ? 0
+                         : p->use_phased ? kPhasedSlots * (size_t)p->phased_chunk * (size_t)cfg->n * sizeof(float2)
+                                         : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
                                            sizeof(float2);
       if (p->scratch_bytes > 0 && (e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
@@ -512,6 +568,8 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
     if (p->d_scratch) cudaFree(p->d_scratch);
+    if (p->d_done) cudaFree(p->d_done);
+    if (p->d_fallback) cudaFree(p->d_fallback);
     for (auto &x : p->xs)
       if (x) cudaStreamDestroy(x);
     for (cudaEvent_t ev : {p->ev_fork, p->ev_a[0], p->ev_a[1], p->ev_b[0], p->ev_b[1], p->ev_join[0], p->ev_join[1]})
@@ -659,7 +717,7 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return p->use_cluster ? 1 : (int)p->ex.groups.size();
+  default: return (p->use_cluster || p->use_phased) ? 1 : (int)p->ex.groups.size();
   }
 }
 
@@ -701,6 +759,14 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << "> launch grid[" << p->cfg.batch * csize << "] cluster[" << csize << "] block[" << threads
         << "] smem=" << smem << "B co-resident clusters=" << p->max_clusters
         << " (persistent; one transform per cluster, intermediate in DSMEM, no scratch)\n";
+    } else if (p->use_phased) {
+      int64_t threads, smem, t0, t1;
+      phased_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, &threads, &smem, &t0, &t1);
+      o << "phased: 1 fft_phased_kernel<" << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
+        << "> cooperative launch grid[" << p->phased_grid << "] block[" << threads << "] smem=" << smem
+        << "B chunk=" << p->phased_chunk << " transforms, " << kPhasedSlots << " L2 slots = " << p->scratch_bytes
+        << " B (both groups streamed through L2 with per-chunk dependencies, TMA tiles, intermediate "
+           "discarded after use)\n";
     } else
       o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
         << " B\n";

@@ -57,6 +57,17 @@ template <> struct SIO<LAYOUT_SCRATCH> {
     __stcs(reinterpret_cast<float2 *>(p0) + off, v);
   }
 };
+// L2-resident intermediate of the phased kernel: L2-only loads (no stale L1
+// lines across phases) and write-back stores that stay in L2.
+constexpr int LAYOUT_L2 = 3;
+template <> struct SIO<LAYOUT_L2> {
+  static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
+    return __ldcg(reinterpret_cast<const float2 *>(p0) + off);
+  }
+  static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
+    __stcg(reinterpret_cast<float2 *>(p0) + off, v);
+  }
+};
 template <> struct SIO<LAYOUT_SPLIT> {
   static FFTGEN_FI float2 load(const void *p0, const void *p1, int64_t off) {
     return make_float2(__ldcs(reinterpret_cast<const float *>(p0) + off),
@@ -79,7 +90,11 @@ template <int BARID, int THREADS> FFTGEN_FI void compute_sync() {
 
 // One tile of one group: TC adjacent transforms (tile index tt) of the
 // transform whose input / output start at element offsets ib / ob.
-template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0>
+// DISCARD (rows tiles): once pass 0 has read the tile, its 128-byte L2 lines
+// are dropped without write-back (discard.global.L2) -- the tile is an
+// L2-resident intermediate no one reads again.
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0,
+          bool DISCARD = false>
 FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
@@ -128,6 +143,11 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
     smem_write<G, NS, 0>(smem + f * REG, t, v);
   }
   compute_sync<BARID, GG::THREADS>();
+  if constexpr (DISCARD && ROWS) {
+    const char *base = reinterpret_cast<const char *>(reinterpret_cast<const float2 *>(a.in0) + ib + m0 * NS);
+    for (int l = tid; l < TC * NS * 8 / 128; l += GG::THREADS)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + l * 128) : "memory");
+  }
 
   // ---- pass 1: smem -> registers (lanes over f), codelet, HBM store ------
   {

@@ -23,12 +23,20 @@
 
 namespace fftgen_b200 {
 
-template <int NS> struct GroupTmaGeom {
+#ifndef FFTGEN_GROUP_TMA_STAGES
+#define FFTGEN_GROUP_TMA_STAGES 2
+#endif
+constexpr int kGroupTmaStages = FFTGEN_GROUP_TMA_STAGES;
+
+// STAGES = 2: one CTA per SM, the tile two items ahead is in flight;
+// STAGES = 1: two CTAs per SM, each refilling its stage after pass 1.
+template <int NS, int STAGES_ = kGroupTmaStages> struct GroupTmaGeom {
   using GG = GroupGeom<NS>;
+  static constexpr int STAGES = STAGES_;
   static constexpr int TC = GG::TC, REG = GG::REG, THREADS = GG::THREADS;
   static constexpr int RAW = TC * NS * 8;  // raw tile bytes
   static constexpr int STAGE = ((TC * REG * 8 > RAW ? TC * REG * 8 : RAW) + 127) / 128 * 128;
-  static constexpr int BYTES = 2 * STAGE + 64;
+  static constexpr int BYTES = STAGES * STAGE + 64;
   static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 0 ? (228 * 1024) / (BYTES + 1024) : 1;
 };
 
@@ -63,6 +71,64 @@ FFTGEN_FI void group_tma_issue(const GroupTmaArgs &ta, char *stage, uint64_t *ba
   }
 }
 
+// One tile whose raw input already sits in `stage` (columns [A][f], rows
+// [f][A]; split planes re then im): pass 0 with the group twiddle, padded
+// exchange in the same stage, pass 1, stores to a.out* at element offset ob.
+// The caller synchronises before the stage is refilled.
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG>
+FFTGEN_FI void tile_from_stage(const GroupArgs &a, char *stage, int64_t ob, int64_t m0, int64_t c0) {
+  using G = typename GG::G;
+  constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
+  constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
+  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  const int tid = threadIdx.x;
+  float2 *X = reinterpret_cast<float2 *>(stage);
+  float2 v[G::RMAX];
+  const int f0 = ROWS ? tid / T : tid % TC;
+  const int t0 = ROWS ? tid % T : tid / TC;
+  {
+    const int64_t m = ROWS ? m0 + f0 : m0;
+    const bool tw = a.cols > 1;
+    const float2 *qm = a.tw_q + m;
+#pragma unroll
+    for (int j = 0; j < J0; ++j) {
+      const int c = t0 + j * T;
+#pragma unroll
+      for (int A0 = 0; A0 < R0; ++A0) {
+        const int A = A0 * K0 + c;
+        const int e = ROWS ? f0 * NS + A : A * TC + f0;
+        if constexpr (LIN == LAYOUT_SPLIT) {
+          const float *sp = reinterpret_cast<const float *>(stage);
+          v[j * R0 + A0] = make_float2(sp[e], sp[NS * TC + e]);
+        } else {
+          v[j * R0 + A0] = X[e];
+        }
+      }
+      if (tw) {
+        const float2 pw = __ldg(a.tw_p + c * a.cols + m);
+#pragma unroll
+        for (int A0 = 0; A0 < R0; ++A0) {
+          float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
+          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+        }
+      }
+      reg_fft<R0, DIR>(v + j * R0);
+    }
+  }
+  __syncthreads();  // raw tile consumed: the stage becomes the padded exchange
+  smem_write<G, NS, 0>(X + f0 * REG, t0, v);
+  __syncthreads();
+  const int f = tid % TC;
+  const int t = tid / TC;
+  smem_read_pass<G, NS, 1, DIR>(X + f * REG, t, a.tw_local, v);
+#pragma unroll
+  for (int B = 0; B < R1; ++B) {
+    const int64_t e = B * COLS1 + t;
+    const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
+    SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+  }
+}
+
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
 __global__ void __launch_bounds__(GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::MIN_BLOCKS)
 fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
@@ -74,7 +140,8 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
   const GroupArgs &a = ta.g;
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * TG::STAGE);
+  constexpr int NST = TG::STAGES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NST * TG::STAGE);
   const int tid = threadIdx.x;
   const int64_t total = ta.items, stride = gridDim.x;
 
@@ -85,13 +152,13 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
   }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < 2; ++s)
+    for (int s = 0; s < NST; ++s)
       if (blockIdx.x + s * stride < total)
         group_tma_issue<NS, LIN, ROWS>(ta, smem + s * TG::STAGE, &bars[s], blockIdx.x + s * stride);
 
   int it = 0;
   for (int64_t item = blockIdx.x; item < total; item += stride, ++it) {
-    const int s = it & 1;
+    const int s = NST == 2 ? (it & 1) : 0;
     char *stage = smem + s * TG::STAGE;
     float2 *X = reinterpret_cast<float2 *>(stage);
     const int64_t b = item / a.tiles_per_outer, tt = item - b * a.tiles_per_outer;
@@ -104,7 +171,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
       m0 = u0 / a.k;
       c0 = u0 - m0 * a.k;
     }
-    mbar_wait(&bars[s], (it >> 1) & 1);
+    mbar_wait(&bars[s], (NST == 2 ? (it >> 1) : it) & 1);
 
     // ---- pass 0: raw tile -> registers, global twiddle, radix-R0 codelets ----
     float2 v[G::RMAX];
@@ -148,9 +215,9 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     const int t = tid / TC;
     smem_read_pass<G, NS, 1, DIR>(X + f * REG, t, a.tw_local, v);
     __syncthreads();  // stage free: fetch the tile two items ahead
-    if (tid == 0 && item + 2 * stride < total) {
+    if (tid == 0 && item + NST * stride < total) {
       fence_proxy_async();
-      group_tma_issue<NS, LIN, ROWS>(ta, stage, &bars[s], item + 2 * stride);
+      group_tma_issue<NS, LIN, ROWS>(ta, stage, &bars[s], item + NST * stride);
     }
     const int64_t ob = b * a.odist;
 #pragma unroll

@@ -47,6 +47,24 @@ struct GroupArgs {
   const float2 *tw_p;      // [c][m]  = w_s^{c m}
 };
 
+// K6: both groups of a 2-group plan in one persistent cooperative launch;
+// chunks of `chunk` transforms alternate between two L2-resident slots
+// (fft_phased.cuh).  g0: user in -> slots, g1: slots -> user out.
+constexpr int kPhasedSlots = 3;  // L2-resident intermediate slots of the K6 kernel
+struct PhasedArgs {
+  alignas(64) unsigned char tmap0[2][128];  // group-0 input planes (columns view)
+  alignas(64) unsigned char tmap1[128];     // the slots (rows view, kPhasedSlots*chunk transforms)
+  GroupArgs g0, g1;
+  int64_t batch, chunk;
+  int *done;  // [2][nchunks] tiles completed per chunk (group 0, group 1), zeroed per launch
+};
+bool phased_supported(int log2ns0, int log2ns1);
+// *blocks_per_sm: co-resident CTAs per SM (the cooperative grid)
+cudaError_t phased_prepare(int log2ns0, int log2ns1, int *blocks_per_sm);
+cudaError_t phased_launch(int log2ns0, int log2ns1, int layout, int dir, const PhasedArgs &pa, int grid,
+                          cudaStream_t s);
+void phased_geom(int log2ns0, int log2ns1, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1);
+
 // shape: 0 interleaved->scratch columns, 1 split->scratch columns,
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
 cudaError_t group_launch(int log2ns, int shape, int dir, const GroupArgs &a, int64_t batch, cudaStream_t s);
@@ -64,6 +82,9 @@ struct GroupTmaArgs {
 cudaError_t group_tma_prepare(int log2ns, int *blocks_per_sm);
 // encode ta.tmap for ta.g's input; false if the input is not TMA-addressable
 bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta);
+// tensor maps of a's input planes for tiles of tc transforms (shape as group_launch)
+bool encode_tile_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, int64_t tc,
+                      unsigned char (*tmap)[128]);
 cudaError_t group_tma_launch(int log2ns, int shape, int dir, const GroupTmaArgs &ta, int grid, cudaStream_t s);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 

@@ -352,12 +352,10 @@ cudaError_t cluster_launch(int l0, int l1, int c, int layout, int dir, const Clu
 
 namespace fftgen_b200 {
 
-bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
+bool encode_tile_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, int64_t tc,
+                      unsigned char (*tmap)[128]) {
   auto enc = tensor_map_encoder();
   if (!enc) return false;
-  int64_t threads, tc, smem, r0;
-  group_geom(log2ns, &threads, &tc, &smem, &r0);
-  const GroupArgs &a = ta.g;
   const int64_t ns = int64_t(1) << log2ns;
   const bool rows = shape == 2 || shape == 3;
   const bool split_in = shape == 1;
@@ -381,13 +379,63 @@ bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
     box[0] = tc * w; box[1] = std::min<int64_t>(ns, 256); box[2] = 1; box[3] = 1;
   }
   for (int i = 0; i < nplanes; ++i) {
-    CUresult r = enc(reinterpret_cast<CUtensorMap *>(ta.tmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(tmap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                      const_cast<void *>(planes[i]), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
   }
   return true;
+}
+
+bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
+  int64_t threads, tc, smem, r0;
+  group_geom(log2ns, &threads, &tc, &smem, &r0);
+  return encode_tile_maps(ta.g, log2ns, shape, batch, tc, ta.tmap);
+}
+
+}  // namespace fftgen_b200
+
+// ---- K6 phased dispatch ------------------------------------------------------
+#include "phased_instances.cuh"
+
+namespace fftgen_b200 {
+
+cudaError_t phased_launch_f(int, int, int, const PhasedArgs &, int, cudaStream_t);
+cudaError_t phased_launch_b(int, int, int, const PhasedArgs &, int, cudaStream_t);
+cudaError_t phased_prepare_f(int, int, int *);
+cudaError_t phased_prepare_b(int, int, int *);
+
+void phased_geom(int l0, int l1, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1) {
+  *threads = *smem = *tiles0 = *tiles1 = 0;
+  switch (l0 * 16 + l1) {
+#define FFTGEN_PG(A, B, NA, NB)                  \
+  case A * 16 + B:                               \
+    *threads = PhasedGeom<NA, NB>::THREADS;      \
+    *smem = PhasedGeom<NA, NB>::SMEM;            \
+    *tiles0 = PhasedGeom<NA, NB>::TILES0;        \
+    *tiles1 = PhasedGeom<NA, NB>::TILES1;        \
+    break;
+    FFTGEN_PHASED_SHAPES(FFTGEN_PG)
+#undef FFTGEN_PG
+  default: break;
+  }
+}
+
+bool phased_supported(int l0, int l1) {
+  int64_t t, m, a, b;
+  phased_geom(l0, l1, &t, &m, &a, &b);
+  return t > 0;
+}
+
+cudaError_t phased_prepare(int l0, int l1, int *bps) {
+  *bps = 1 << 30;
+  cudaError_t e = phased_prepare_f(l0, l1, bps);
+  return e != cudaSuccess ? e : phased_prepare_b(l0, l1, bps);
+}
+
+cudaError_t phased_launch(int l0, int l1, int layout, int dir, const PhasedArgs &pa, int grid, cudaStream_t s) {
+  return dir < 0 ? phased_launch_f(l0, l1, layout, pa, grid, s) : phased_launch_b(l0, l1, layout, pa, grid, s);
 }
 
 }  // namespace fftgen_b200

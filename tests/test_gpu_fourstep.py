@@ -179,6 +179,7 @@ def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
         return y
 
     monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+    monkeypatch.setenv("FFTGEN_PHASED", "0")
     monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", str(32 << 20))
     chunked = run_once()
     monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", "0")
@@ -265,6 +266,7 @@ def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch
     g = torch.Generator(device="cuda").manual_seed(l2)
     x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
     monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+    monkeypatch.setenv("FFTGEN_PHASED", "0")
 
     def run_once(tma):
         monkeypatch.setenv("FFTGEN_GROUP_TMA", tma)
@@ -290,3 +292,46 @@ def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch
     if l2 <= 20:
         xi = x[0].reshape(-1).double().cpu().numpy()
         assert oracle.rel_l2(a[0].reshape(-1).double().cpu().numpy(), orc.forward(xi, "stockham", 4)) < 3e-6
+
+
+@pytest.mark.parametrize("l2,batch,slot_mb", [(15, 301, 24), (15, 37, 1), (16, 150, 24), (16, 9, 1),
+                                              (17, 77, 3), (18, 20, 24), (19, 7, 8), (20, 5, 8), (20, 2, 24)])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layout, direction, monkeypatch):
+    """K6 (both groups in one cooperative launch, chunks alternating between two
+    L2-resident slots, grid barrier per chunk, intermediate discarded after use)
+    (opt-in) is bitwise the two-launch K3 path, for ragged last chunks, one-transform
+    chunks and batches smaller than a chunk; both match the oracle."""
+    n = 1 << l2
+    g = torch.Generator(device="cuda").manual_seed(200 + l2)
+    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
+    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
+    monkeypatch.setenv("FFTGEN_PHASED", "1")
+    monkeypatch.setenv("FFTGEN_PHASE_SLOT_MB", str(slot_mb))
+
+    def run_once():
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+        if layout == "interleaved":
+            y = torch.full_like(x, float("nan"))
+            plan.execute(x, y, direction=direction)
+        else:
+            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
+            plan.execute(re, ore, im, oim, direction=direction)
+            y = torch.stack([ore, oim], dim=-1)
+        torch.cuda.synchronize()
+        d = plan.describe()
+        plan.close()
+        return y, d
+
+    ph, d1 = run_once()
+    assert "fft_phased_kernel" in d1
+    monkeypatch.setenv("FFTGEN_PHASED", "0")
+    two, d2 = run_once()
+    assert "fft_phased_kernel" not in d2
+    assert torch.equal(ph, two)
+    for b in (0, batch - 1):
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        want = orc.forward(xi, "stockham", 4, inverse=direction > 0)
+        assert oracle.rel_l2(ph[b].reshape(-1).double().cpu().numpy(), want) < 3e-6, b
