@@ -29,7 +29,7 @@ def check_rows(orc, x, y, n, inverse=False, rows=(0, -1)):
         assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4, inverse=inverse)) < 3e-6, b
 
 
-@pytest.mark.parametrize("n", [1024, 4096, 16384, 1 << 16, 1 << 21])
+@pytest.mark.parametrize("n", [1024, 4096, 16384, 1 << 15, 1 << 16, 1 << 18, 1 << 21])
 def test_in_place_execution(fg, orc, n):
     batch = 4 if n <= 1 << 16 else 1
     x = rand((batch, n, 2), 1)
@@ -45,7 +45,7 @@ def test_in_place_execution(fg, orc, n):
     check_rows(orc, ref, torch.stack([re, im], -1), n, inverse=True)
 
 
-@pytest.mark.parametrize("n", [4096, 1 << 16])
+@pytest.mark.parametrize("n", [4096, 1 << 15, 1 << 16, 1 << 18])
 def test_cuda_graph_capture_and_replay(fg, orc, n):
     batch = 64
     x = rand((batch, n, 2), 2)
