@@ -188,22 +188,35 @@ template <int N> struct Tma1Geom {
 };
 
 // -------------------------------------------------------------------------
-// K3 group kernel tile: TC adjacent transforms of size NS per CTA (~64 KB of
-// float2 in shared memory, <= 512 threads); odd per-transform stride REG so
+// K3 group kernel tile: TC adjacent transforms of size NS per CTA (32-64 KB
+// of float2 in shared memory, <= 512 threads); odd per-transform stride REG so
 // lanes walking over the tile index f hit distinct bank pairs.
-// MAXT caps the threads per CTA.
+// MAXT caps the threads per CTA.  Tile bytes per NS, measured on B200
+// (scripts/gpu_ab.sh): 16-point-codelet groups (NS <= 256) run best as 32 KB
+// tiles of 256 threads, four CTAs per SM (2^16 interleaved two-launch 0.50 vs
+// 0.44 of the single-pass roofline with 64 KB tiles); 32-point groups
+// (NS >= 512) need 64 KB tiles to keep 64-byte column segments (2^20: 0.35
+// vs 0.21 with 32 KB).
+#ifndef FFTGEN_GROUP_TILE_SMALL
+#define FFTGEN_GROUP_TILE_SMALL 32768
+#endif
+#ifndef FFTGEN_GROUP_TILE_LARGE
+#define FFTGEN_GROUP_TILE_LARGE 65536
+#endif
 template <int NS, int MAXT = 512> struct GroupGeom {
   static constexpr int T = BlockGeom<NS>::T;
-  static constexpr int TC_BYTES = 65536 / (8 * NS);                   // ~64 KB tiles
+  static constexpr int TILE_BYTES = NS <= 256 ? FFTGEN_GROUP_TILE_SMALL : FFTGEN_GROUP_TILE_LARGE;
+  static constexpr int TC_BYTES = TILE_BYTES / (8 * NS);                // transforms per tile
   static constexpr int TC = TC_BYTES * T > MAXT ? MAXT / T : TC_BYTES;  // <= MAXT threads
   using G = BlockGeom<NS, TC>;
   static constexpr int THREADS = G::THREADS;
   static constexpr int EX = SmemGeom<NS>::REGION > NS ? SmemGeom<NS>::REGION : NS;
   static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
   static constexpr int BYTES = TC * REG * 8;
-  // resident CTAs the register budget must allow (smem allows 3 at ~66 KB)
-  // 32-point codelets (NS >= 512: 64 registers of data) need the 2-CTA budget
-  static constexpr int MIN_BLOCKS = (THREADS >= 512 || BlockGeom<NS>::RMAX > 16) ? 2 : 3;
+  // resident CTAs the register budget must allow: 16-point codelets fit 64
+  // registers, 32-point ones (NS >= 512) need 128
+  static constexpr int MIN_BLOCKS =
+      BlockGeom<NS>::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3));
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };

@@ -443,24 +443,22 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       for (const GroupDesc &d : p->ex.groups)
         if ((e = group_prepare(d.log2ns)) != cudaSuccess)
           return bail(FFTGEN_ERR_CUDA, std::string("group kernel attributes: ") + cudaGetErrorString(e));
-      // Persistent TMA group kernels where they measured faster (B200 launch
-      // list, scripts/gpu_k3t_launch.sh): first-group columns from split user
-      // planes (2^16: 386 vs 427 us, 2^18: 385 vs 465, 2^24: 388 vs 439) and
-      // from interleaved input at NS >= 512 (2^18: 372 vs 433), middle columns
-      // at NS = 128; never rows (2^24: 667 vs 410).  FFTGEN_GROUP_TMA=0 / 1
-      // forces none / all.
+      // Persistent TMA group kernels where they measured faster (B200,
+      // scripts/gpu_ab.sh, 32 KB tiles for NS <= 256): first-group columns at
+      // NS >= 512, whose 64 KB tiles leave one CTA of 256 threads per SM without
+      // a prefetch (2^18 split 0.40 vs 0.35, 2^20 0.35 vs 0.32 of the single-pass
+      // roofline); the 4-CTA 32 KB plain tiles win below (2^16 split 0.43 vs
+      // 0.41) and for rows.  FFTGEN_GROUP_TMA=0 / 1 forces none / all.
       const char *gt = std::getenv("FFTGEN_GROUP_TMA");
       const int force = gt ? (gt[0] == '0' ? 0 : 1) : -1;
       if (force != 0) {
         int sms = 0;
         if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
           return bail(FFTGEN_ERR_CUDA, "device attributes");
-        const bool split = cfg->layout == FFTGEN_LAYOUT_SPLIT;
         for (size_t g = 0; g < p->ex.groups.size(); ++g) {
           const GroupDesc &d = p->ex.groups[g];
           const bool first = g == 0;
-          const bool want = force == 1 || (!d.rows && ((first && (split || d.log2ns >= 9)) ||
-                                                       (!first && d.log2ns == 7)));
+          const bool want = force == 1 || (!d.rows && first && d.log2ns >= 9);
           int bps = 0;
           if (want && (e = group_tma_prepare(d.log2ns, &bps)) != cudaSuccess)
             return bail(FFTGEN_ERR_CUDA, std::string("group TMA kernel attributes: ") + cudaGetErrorString(e));

@@ -90,7 +90,9 @@ def test_fourstep_plan_shape(fg):
     assert "fft_cluster_kernel<128,256,8>" in q.describe()
     q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 16, layout="split", batch=4))
     assert q.launches() == 2 and q.scratch_bytes() == 4 * (1 << 16) * 8
-    assert "group 0: fft_group_tma_kernel<256>" in q.describe()
+    assert "group 0: fft_group_kernel<256>" in q.describe()
+    q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 18, layout="split", batch=2))
+    assert "group 0: fft_group_tma_kernel<512>" in q.describe()
 
 
 def test_fourstep_host_and_interpret_paths(fg, orc):
