@@ -158,7 +158,16 @@ template <int N> struct TmaGeom {
   static constexpr int TP = tp_threads < tp_bytes ? tp_threads : tp_bytes;
   using G = BlockGeom<N, TP>;
   static constexpr int THREADS = G::THREADS;
-  static constexpr int STAGES = 2;
+  // Stages per CTA, measured on B200 (scripts/gpu_ab.sh, 1 GiB batches):
+  // N = 4096 runs best single-buffered at twice the CTAs per SM (split 0.96
+  // vs 0.86 of the measured HBM peak, interleaved 0.93 vs 0.85 -- more warps
+  // hide the codelets' dependency latency while other CTAs' TMA traffic keeps
+  // HBM busy); the other sizes keep double buffering (2^13: 0.86 vs 0.76).
+#ifdef FFTGEN_K2_STAGES
+  static constexpr int STAGES = FFTGEN_K2_STAGES;
+#else
+  static constexpr int STAGES = N == 4096 ? 1 : 2;
+#endif
   static constexpr int RAW = 8 * N;                                   // bytes per transform
   static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes
   static constexpr int SLOT = ((RAW > XCH ? RAW : XCH) + 127) / 128 * 128;

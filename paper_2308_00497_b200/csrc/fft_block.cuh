@@ -299,7 +299,8 @@ template <int N, int LAYOUT, int DIR, bool STORE_TMA>
 __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
   using TG = TmaGeom<N>;
   using G = typename TG::G;
-  static_assert(TG::STAGES == 2, "refill schedule assumes double buffering");
+  static_assert(TG::STAGES == 1 || TG::STAGES == 2, "single or double buffering");
+  constexpr int NST = TG::STAGES;
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + TG::STAGES * TG::STAGE_BYTES);
@@ -326,10 +327,10 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
 
   int it = 0;
   for (int64_t g = blockIdx.x; g < groups; g += stride, ++it) {
-    const int s = it & 1;
+    const int s = NST == 2 ? (it & 1) : 0;
     char *stage = smem + s * TG::STAGE_BYTES;
     char *slot = stage + f * TG::SLOT;
-    mbar_wait(&bars[s], (it >> 1) & 1);
+    mbar_wait(&bars[s], (NST == 2 ? (it >> 1) : it) & 1);
 
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
@@ -340,14 +341,14 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
-    if (STORE_TMA && tid == 0 && it >= 1) {
+    if (NST == 2 && STORE_TMA && tid == 0 && it >= 1) {
       // the other stage held group it-1, bulk-stored at the end of the last
       // iteration: refill it with group it+1 once that store has drained
       // shared memory (pass 0 above overlapped the drain)
       const int64_t gn = g + stride;
       if (gn < groups) {
         bulk_wait_read0();
-        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[s ^ 1], gn);
+        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[(s ^ 1) & (NST - 1)], gn);
       }
     }
     float2 *sx = reinterpret_cast<float2 *>(slot);
@@ -364,7 +365,13 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       smem_write_out<G, N, LAYOUT>(slot, t, v);
       fence_proxy_async();  // make generic-proxy writes visible to the bulk copy
       __syncthreads();
-      if (tid == 0) tma_store<N, LAYOUT>(args, stage, g);
+      if (tid == 0) {
+        tma_store<N, LAYOUT>(args, stage, g);
+        if (NST == 1 && g + stride < groups) {  // refill once the store has read the stage
+          bulk_wait_read0();
+          tma_issue<N, LAYOUT>(args, stage, &bars[0], g + stride);
+        }
+      }
       (void)b;
     } else {
       if (tid == 0) {
