@@ -1,9 +1,6 @@
-# round-1 evidence: ncu --set full of the default kernels + launch list of the bench command
-D=gpurun_out/r1b; mkdir -p $D
+D=gpurun_out/r1c; mkdir -p $D
 NCU="ncu --set full --clock-control none --import-source on"
 timeout 600 $NCU -k regex:fft_block_tma -s 3 -c 1 -o $D/block_tma_4096_split -f python bench.py --profile --steps 1 --warmup 4 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
-timeout 600 $NCU -k regex:fft_cluster -s 2 -c 1 -o $D/cluster_32768_il -f python scripts/sweep.py --sizes 15 --layouts interleaved --steps 1 --warmup 2 > /dev/null 2>&1
-timeout 600 $NCU -k regex:fft_group -s 2 -c 2 -o $D/group_tma_262144_split -f python scripts/sweep.py --sizes 18 --layouts split --steps 1 --warmup 1 > /dev/null 2>&1
-timeout 600 $NCU -k regex:fft_block_kernel -s 2 -c 1 -o $D/block_16384_il -f python scripts/sweep.py --sizes 14 --layouts interleaved --steps 1 --warmup 2 > /dev/null 2>&1
+timeout 600 $NCU -k regex:fft_group -s 2 -c 2 -o $D/group_65536_il -f python scripts/sweep.py --sizes 16 --layouts interleaved --steps 1 --warmup 1 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $D/launches_bench.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
 ls -la $D
