@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_fourstep.py -x -q -k "phased or plan_shape" 2>&1 | tail -5
-timeout 400 python scripts/sweep.py --sizes 16,18,20 --layouts split,interleaved --variants default,FFTGEN_PHASE_SLOT_MB=8,FFTGEN_PHASE_SLOT_MB=32,FFTGEN_PHASED=0 --steps 20 2>&1 | tail -40
+timeout 400 python scripts/sweep.py --sizes 15,16,17,18,20 --layouts split,interleaved --variants default,FFTGEN_PHASED=1+FFTGEN_DISABLE_CLUSTER=1,FFTGEN_PHASED=1+FFTGEN_DISABLE_CLUSTER=1+FFTGEN_PHASE_SLOT_MB=32 --steps 20 2>&1 | grep '"n"' | python -c "
+import sys,json
+for l in sys.stdin:
+    d=json.loads(l); print(d['n'], d['layout'], d['variant'], d['frac'], d['ms'], d['kernel'])"
