@@ -83,7 +83,8 @@ struct fftgen_plan {
   bool use_cluster = false;
   // K6: 2-group plans in one cooperative launch, intermediate in two L2 slots
   bool use_phased = false;
-  int phased_grid = 0;
+  int phased_grid = 0, phased_variant = 0;
+  int64_t phased_lag = 1, phased_slots = 3;
   int64_t phased_chunk = 0;
   int *d_done = nullptr;  // per-chunk completed tiles of group 0 and group 1
   int max_clusters = 0, cluster_size = 0;
@@ -239,12 +240,16 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       pa.batch = batch;
       pa.chunk = std::min<int64_t>(p->phased_chunk, batch);
       pa.done = p->d_done;
+      pa.variant = p->phased_variant;
+      pa.lag = p->phased_lag;
+      pa.slots = p->phased_slots;
       int64_t threads, smem, t0, t1;
-      phased_geom(gs[0].log2ns, gs[1].log2ns, &threads, &smem, &t0, &t1);
+      phased_geom(gs[0].log2ns, gs[1].log2ns, p->phased_variant, &threads, &smem, &t0, &t1);
       const int64_t nchunks = (batch + pa.chunk - 1) / pa.chunk;
-      if (encode_tile_maps(pa.g0, gs[0].log2ns, split ? 1 : 0, batch, gs[1].ns / t0, pa.tmap0) &&
-          encode_tile_maps(pa.g1, gs[1].log2ns, 2, kPhasedSlots * pa.chunk, gs[0].ns / t1,
-                           reinterpret_cast<unsigned char(*)[128]>(pa.tmap1))) {
+      if (p->phased_variant == 2 ||
+          (encode_tile_maps(pa.g0, gs[0].log2ns, split ? 1 : 0, batch, gs[1].ns / t0, pa.tmap0) &&
+           encode_tile_maps(pa.g1, gs[1].log2ns, 2, p->phased_slots * pa.chunk, gs[0].ns / t1,
+                            reinterpret_cast<unsigned char(*)[128]>(pa.tmap1)))) {
         cudaError_t e = cudaMemsetAsync(p->d_done, 0, 2 * nchunks * sizeof(int), s);
         if (e != cudaSuccess) return e;
         const int grid = (int)std::min<int64_t>(p->phased_grid, batch * (t0 + t1));
@@ -520,15 +525,18 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       // bytes of a tile does not shorten it.
       const char *ph = std::getenv("FFTGEN_PHASED");
       if (gs.size() == 2 && !p->use_cluster && phased_supported(gs[0].log2ns, gs[1].log2ns) && ph &&
-          ph[0] == '1') {
+          (ph[0] == '1' || ph[0] == '2')) {
         int bps = 0, sms = 0;
-        if ((e = phased_prepare(gs[0].log2ns, gs[1].log2ns, &bps)) != cudaSuccess ||
+        p->phased_variant = ph[0] - '0';
+        if ((e = phased_prepare(gs[0].log2ns, gs[1].log2ns, p->phased_variant, &bps)) != cudaSuccess ||
             (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
           return bail(FFTGEN_ERR_CUDA, std::string("phased kernel attributes: ") + cudaGetErrorString(e));
         if (bps > 0) {
           int64_t slot_mb = 16;
           if (const char *env = std::getenv("FFTGEN_PHASE_SLOT_MB")) slot_mb = std::max<int64_t>(1, std::atoll(env));
           p->phased_chunk = std::min<int64_t>(cfg->batch, std::max<int64_t>(1, (slot_mb << 20) / (cfg->n * 8)));
+          if (const char *env = std::getenv("FFTGEN_PHASE_LAG")) p->phased_lag = std::max<int64_t>(1, std::atoll(env));
+          p->phased_slots = p->phased_lag + 2;
           p->phased_grid = bps * sms;
           p->use_phased = true;
           p->chunk = 0;
@@ -538,7 +546,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         }
       }
       p->scratch_bytes = p->use_cluster ? 0
-                         : p->use_phased ? kPhasedSlots * (size_t)p->phased_chunk * (size_t)cfg->n * sizeof(float2)
+                         : p->use_phased ? (size_t)p->phased_slots * (size_t)p->phased_chunk * (size_t)cfg->n * sizeof(float2)
                                          : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
                                            sizeof(float2);
       if (p->scratch_bytes > 0 && (e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
@@ -759,10 +767,11 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << " (persistent; one transform per cluster, intermediate in DSMEM, no scratch)\n";
     } else if (p->use_phased) {
       int64_t threads, smem, t0, t1;
-      phased_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, &threads, &smem, &t0, &t1);
-      o << "phased: 1 fft_phased_kernel<" << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
+      phased_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, p->phased_variant, &threads, &smem, &t0, &t1);
+      o << "phased: 1 " << (p->phased_variant == 2 ? "fft_stream_kernel<" : "fft_phased_kernel<") << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
         << "> cooperative launch grid[" << p->phased_grid << "] block[" << threads << "] smem=" << smem
-        << "B chunk=" << p->phased_chunk << " transforms, " << kPhasedSlots << " L2 slots = " << p->scratch_bytes
+        << "B chunk=" << p->phased_chunk << " transforms, lag " << p->phased_lag << ", " << p->phased_slots
+        << " L2 slots = " << p->scratch_bytes
         << " B (both groups streamed through L2 with per-chunk dependencies, TMA tiles, intermediate "
            "discarded after use)\n";
     } else

@@ -2,7 +2,7 @@
 // persistent cooperative launch, with the intermediate held in L2.
 //
 // The batch is cut into chunks of `chunk` transforms whose intermediate (one
-// "slot", chunk * N * 8 bytes) stays in L2; kPhasedSlots = 3 slots rotate.
+// "slot", chunk * N * 8 bytes) stays in L2; pa.slots = 3 slots rotate.
 // All tiles of the launch form one global sequence
 //     G0(0) | G0(1) G1(0) | G0(2) G1(1) | ... | G1(last)
 // (G0(c): the column tiles of group 0 for chunk c, user input -> slot c%3;
@@ -61,51 +61,52 @@ struct StreamItem {
   int64_t tt;     // tile within the transform
 };
 
+// Segment c of the sequence holds G0(c) (c < nchunks) then G1(c - lag)
+// (0 <= c - lag < nchunks).  P(c) = tiles before segment c, monotone, so the
+// segment of item t is found by bisection.
 template <class PG>
-FFTGEN_FI StreamItem stream_decode(int64_t t, int64_t chunk, int64_t nchunks, int64_t batch) {
-  constexpr int64_t T0 = PG::TILES0, T1 = PG::TILES1;
-  auto cnt = [&](int64_t c) { return c + 1 < nchunks ? chunk : batch - c * chunk; };
+FFTGEN_FI int64_t stream_prefix(int64_t c, const PhasedArgs &pa, int64_t nchunks) {
+  auto done_tf = [&](int64_t m) {  // transforms in the first m chunks
+    m = m < 0 ? 0 : (m > nchunks ? nchunks : m);
+    const int64_t v = m * pa.chunk;
+    return v < pa.batch ? v : pa.batch;
+  };
+  return PG::TILES0 * done_tf(c) + PG::TILES1 * done_tf(c - pa.lag);
+}
+
+template <class PG>
+FFTGEN_FI StreamItem stream_decode(int64_t t, const PhasedArgs &pa, int64_t nchunks) {
+  int64_t lo = 0, hi = nchunks + pa.lag;  // P(lo) <= t < P(hi)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (stream_prefix<PG>(mid, pa, nchunks) <= t)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  const int64_t c = lo, r = t - stream_prefix<PG>(c, pa, nchunks);
+  auto cnt = [&](int64_t k) { return k + 1 < nchunks ? pa.chunk : pa.batch - k * pa.chunk; };
+  const int64_t n0 = c < nchunks ? cnt(c) * PG::TILES0 : 0;
   StreamItem it{};
   int64_t j;
-  const int64_t seg0 = cnt(0) * T0;
-  if (t < seg0) {
-    it.grp = 0, it.c = 0, j = t;
-  } else {
-    t -= seg0;
-    const int64_t lf = chunk * (T0 + T1), nfull = nchunks > 2 ? nchunks - 2 : 0;
-    if (t < nfull * lf) {
-      const int64_t c = 1 + t / lf, r = t - (c - 1) * lf;
-      if (r < chunk * T0)
-        it.grp = 0, it.c = c, j = r;
-      else
-        it.grp = 1, it.c = c - 1, j = r - chunk * T0;
-    } else {
-      t -= nfull * lf;
-      const int64_t cl = nchunks - 1;
-      if (nchunks >= 2 && t < cnt(cl) * T0 + chunk * T1) {
-        if (t < cnt(cl) * T0)
-          it.grp = 0, it.c = cl, j = t;
-        else
-          it.grp = 1, it.c = cl - 1, j = t - cnt(cl) * T0;
-      } else {
-        if (nchunks >= 2) t -= cnt(cl) * T0 + chunk * T1;
-        it.grp = 1, it.c = cl, j = t;
-      }
-    }
-  }
-  const int64_t T = it.grp ? T1 : T0;
+  if (r < n0)
+    it.grp = 0, it.c = c, j = r;
+  else
+    it.grp = 1, it.c = c - pa.lag, j = r - n0;
+  const int64_t T = it.grp ? PG::TILES1 : PG::TILES0;
   it.bl = j / T;
   it.tt = j - it.bl * T;
   return it;
 }
 
-// dependency of an item: counter and the value it must reach (none: cnt < 0)
+// G1(c) needs every G0(c) tile stored; G0(c) needs every G1(c - slots) tile
+// read (the slot it overwrites)
 template <class PG>
 FFTGEN_FI bool stream_ready(const PhasedArgs &pa, const StreamItem &it, int64_t nchunks) {
   auto cnt = [&](int64_t c) { return c + 1 < nchunks ? pa.chunk : pa.batch - c * pa.chunk; };
   if (it.grp == 1) return ld_acquire_gpu_s32(pa.done + it.c) >= (int)(cnt(it.c) * PG::TILES0);
-  if (it.c >= kPhasedSlots)
-    return ld_acquire_gpu_s32(pa.done + nchunks + it.c - kPhasedSlots) >= (int)(cnt(it.c - kPhasedSlots) * PG::TILES1);
+  if (it.c >= pa.slots)
+    return ld_acquire_gpu_s32(pa.done + nchunks + it.c - pa.slots) >= (int)(cnt(it.c - pa.slots) * PG::TILES1);
   return true;
 }
 
@@ -125,7 +126,7 @@ FFTGEN_FI void stream_issue(const PhasedArgs &pa, const StreamItem &it, char *st
   } else {
     constexpr int TC = PG::GG1::TC;
     mbar_expect_tx(bar, (uint32_t)PG::RAW1);
-    tma_load_4d(stage, pa.tmap1, 0, 0, (int)(it.tt * TC), (int)((it.c % kPhasedSlots) * pa.chunk + it.bl), bar);
+    tma_load_4d(stage, pa.tmap1, 0, 0, (int)(it.tt * TC), (int)((it.c % pa.slots) * pa.chunk + it.bl), bar);
   }
 }
 
@@ -152,7 +153,7 @@ fft_phased_kernel(const __grid_constant__ PhasedArgs pa) {
       const int64_t t = blockIdx.x + s * stride;
       issued[s] = 0;
       if (t < total) {
-        const StreamItem it = stream_decode<PG>(t, pa.chunk, nchunks, pa.batch);
+        const StreamItem it = stream_decode<PG>(t, pa, nchunks);
         if (stream_ready<PG>(pa, it, nchunks)) {
           stream_issue<PG, NS0, NS1, LIN>(pa, it, smem + s * PG::STAGE, &bars[s]);
           issued[s] = 1;
@@ -166,7 +167,7 @@ fft_phased_kernel(const __grid_constant__ PhasedArgs pa) {
   for (int64_t t = blockIdx.x; t < total; t += stride, ++k) {
     const int s = k & 1;
     char *stage = smem + s * PG::STAGE;
-    const StreamItem it = stream_decode<PG>(t, pa.chunk, nchunks, pa.batch);
+    const StreamItem it = stream_decode<PG>(t, pa, nchunks);
     if (tid == 0 && !issued[s]) {  // front of the queue: everything before it is published
       while (!stream_ready<PG>(pa, it, nchunks)) __nanosleep(64);
       stream_issue<PG, NS0, NS1, LIN>(pa, it, stage, &bars[s]);
@@ -176,13 +177,13 @@ fft_phased_kernel(const __grid_constant__ PhasedArgs pa) {
     if (it.grp == 0) {
       const int64_t c0 = it.tt * PG::GG0::TC;
       GroupArgs a = pa.g0;
-      tile_from_stage<NS0, LIN, LAYOUT_L2, DIR, false, typename PG::GG0>(a, stage, (it.c % kPhasedSlots) * pa.chunk * N + it.bl * N,
+      tile_from_stage<NS0, LIN, LAYOUT_L2, DIR, false, typename PG::GG0>(a, stage, (it.c % pa.slots) * pa.chunk * N + it.bl * N,
                                                                           0, c0);
     } else {
       // the TMA has read the slot's lines: drop them without write-back
       const int64_t m0 = it.tt * PG::GG1::TC;
       const char *lines = reinterpret_cast<const char *>(
-          reinterpret_cast<const float2 *>(pa.g1.in0) + ((it.c % kPhasedSlots) * pa.chunk + it.bl) * N + m0 * NS1);
+          reinterpret_cast<const float2 *>(pa.g1.in0) + ((it.c % pa.slots) * pa.chunk + it.bl) * N + m0 * NS1);
       for (int l = tid; l < PG::RAW1 / 128; l += PG::THREADS)
         asm volatile("discard.global.L2 [%0], 128;" ::"l"(lines + l * 128) : "memory");
       tile_from_stage<NS1, LAYOUT_L2, LOUT, DIR, true, typename PG::GG1>(
@@ -196,7 +197,7 @@ fft_phased_kernel(const __grid_constant__ PhasedArgs pa) {
       issued[s] = 0;
       const int64_t tn = t + 2 * stride;
       if (tn < total) {
-        const StreamItem nx = stream_decode<PG>(tn, pa.chunk, nchunks, pa.batch);
+        const StreamItem nx = stream_decode<PG>(tn, pa, nchunks);
         if (stream_ready<PG>(pa, nx, nchunks)) {
           stream_issue<PG, NS0, NS1, LIN>(pa, nx, stage, &bars[s]);
           issued[s] = 1;
@@ -207,4 +208,69 @@ fft_phased_kernel(const __grid_constant__ PhasedArgs pa) {
   }
 }
 
+
+// ---- K6b: the same stream of tiles with the plain group tiles --------------
+//
+// Geometry of fft_group_kernel (32 KB tiles of 256 threads for NS <= 256, up to
+// four CTAs per SM, loads straight to registers), and dependencies published
+// once per CTA and group-chunk instead of once per tile: a CTA adds its tile
+// count for (group, chunk) when its walk moves on to the next group-chunk,
+// after one fence, and waits for the next group-chunk's dependency only after
+// that -- so it never waits with an unpublished tile of its own, and the walk
+// stays deadlock-free under the co-residency of the cooperative launch.
+template <int NS0, int NS1> struct StreamGeom {
+  using PG = PhasedGeom<NS0, NS1>;
+  using GG0 = typename PG::GG0;
+  using GG1 = typename PG::GG1;
+  static constexpr int THREADS = PG::THREADS;
+  static constexpr int SMEM = GG0::BYTES > GG1::BYTES ? GG0::BYTES : GG1::BYTES;
+  static constexpr int MIN_BLOCKS = GG0::MIN_BLOCKS < GG1::MIN_BLOCKS ? GG0::MIN_BLOCKS : GG1::MIN_BLOCKS;
+  static constexpr int TILES0 = PG::TILES0, TILES1 = PG::TILES1;
+};
+
+template <int NS0, int NS1, int LIN, int LOUT, int DIR>
+__global__ void __launch_bounds__(StreamGeom<NS0, NS1>::THREADS, StreamGeom<NS0, NS1>::MIN_BLOCKS)
+fft_stream_kernel(const __grid_constant__ PhasedArgs pa) {
+  using SG = StreamGeom<NS0, NS1>;
+  using PG = typename SG::PG;
+  constexpr int64_t N = (int64_t)NS0 * NS1;
+  extern __shared__ float4 smem_f4[];
+  float2 *smem = reinterpret_cast<float2 *>(smem_f4);
+  const int tid = threadIdx.x;
+  const int64_t nchunks = (pa.batch + pa.chunk - 1) / pa.chunk;
+  const int64_t total = pa.batch * (PG::TILES0 + PG::TILES1), stride = gridDim.x;
+  int64_t cur = -1;  // current group-chunk key: grp * nchunks + c
+  int mine = 0;      // tiles of `cur` done by this CTA
+  auto publish = [&]() {
+    __syncthreads();  // every thread's stores of `cur` precede the release
+    if (tid == 0 && cur >= 0 && mine > 0) {
+      __threadfence();
+      atomicAdd(pa.done + cur, mine);
+    }
+    mine = 0;
+  };
+  for (int64_t t = blockIdx.x; t < total; t += stride) {
+    const StreamItem it = stream_decode<PG>(t, pa, nchunks);
+    const int64_t key = it.grp * nchunks + it.c;
+    if (key != cur) {
+      publish();
+      cur = key;
+      if (tid == 0)
+        while (!stream_ready<PG>(pa, it, nchunks)) __nanosleep(64);
+      __syncthreads();
+    }
+    if (it.grp == 0) {
+      const int64_t ob = (it.c % pa.slots) * pa.chunk * N + it.bl * N;
+      group_tile<NS0, LIN, LAYOUT_L2, DIR, false, typename SG::GG0>(pa.g0, (it.c * pa.chunk + it.bl) * pa.g0.idist,
+                                                                    ob, it.tt, smem);
+    } else {
+      const int64_t ib = (it.c % pa.slots) * pa.chunk * N + it.bl * N;
+      group_tile<NS1, LAYOUT_L2, LOUT, DIR, true, typename SG::GG1, 0, true>(
+          pa.g1, ib, (it.c * pa.chunk + it.bl) * pa.g1.odist, it.tt, smem);
+    }
+    ++mine;
+    __syncthreads();  // the next tile rewrites the exchange buffer
+  }
+  publish();
+}
 }  // namespace fftgen_b200

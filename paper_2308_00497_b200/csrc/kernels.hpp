@@ -50,20 +50,23 @@ struct GroupArgs {
 // K6: both groups of a 2-group plan in one persistent cooperative launch;
 // chunks of `chunk` transforms alternate between two L2-resident slots
 // (fft_phased.cuh).  g0: user in -> slots, g1: slots -> user out.
-constexpr int kPhasedSlots = 3;  // L2-resident intermediate slots of the K6 kernel
 struct PhasedArgs {
   alignas(64) unsigned char tmap0[2][128];  // group-0 input planes (columns view)
-  alignas(64) unsigned char tmap1[128];     // the slots (rows view, kPhasedSlots*chunk transforms)
+  alignas(64) unsigned char tmap1[128];     // the slots (rows view, slots*chunk transforms)
   GroupArgs g0, g1;
   int64_t batch, chunk;
   int *done;  // [2][nchunks] tiles completed per chunk (group 0, group 1), zeroed per launch
+  int variant;  // 1: TMA tiles (fft_phased_kernel), 2: plain tiles (fft_stream_kernel)
+  int64_t lag;    // group 1 of chunk c runs in segment c + lag of the tile sequence
+  int64_t slots;  // L2-resident intermediate slots (>= lag + 2)
 };
 bool phased_supported(int log2ns0, int log2ns1);
 // *blocks_per_sm: co-resident CTAs per SM (the cooperative grid)
-cudaError_t phased_prepare(int log2ns0, int log2ns1, int *blocks_per_sm);
+cudaError_t phased_prepare(int log2ns0, int log2ns1, int variant, int *blocks_per_sm);
 cudaError_t phased_launch(int log2ns0, int log2ns1, int layout, int dir, const PhasedArgs &pa, int grid,
                           cudaStream_t s);
-void phased_geom(int log2ns0, int log2ns1, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1);
+void phased_geom(int log2ns0, int log2ns1, int variant, int64_t *threads, int64_t *smem, int64_t *tiles0,
+                 int64_t *tiles1);
 
 // shape: 0 interleaved->scratch columns, 1 split->scratch columns,
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns

@@ -403,18 +403,18 @@ namespace fftgen_b200 {
 
 cudaError_t phased_launch_f(int, int, int, const PhasedArgs &, int, cudaStream_t);
 cudaError_t phased_launch_b(int, int, int, const PhasedArgs &, int, cudaStream_t);
-cudaError_t phased_prepare_f(int, int, int *);
-cudaError_t phased_prepare_b(int, int, int *);
+cudaError_t phased_prepare_f(int, int, int *, int);
+cudaError_t phased_prepare_b(int, int, int *, int);
 
-void phased_geom(int l0, int l1, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1) {
+void phased_geom(int l0, int l1, int variant, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1) {
   *threads = *smem = *tiles0 = *tiles1 = 0;
   switch (l0 * 16 + l1) {
-#define FFTGEN_PG(A, B, NA, NB)                  \
-  case A * 16 + B:                               \
-    *threads = PhasedGeom<NA, NB>::THREADS;      \
-    *smem = PhasedGeom<NA, NB>::SMEM;            \
-    *tiles0 = PhasedGeom<NA, NB>::TILES0;        \
-    *tiles1 = PhasedGeom<NA, NB>::TILES1;        \
+#define FFTGEN_PG(A, B, NA, NB)                                                                    \
+  case A * 16 + B:                                                                                 \
+    *threads = PhasedGeom<NA, NB>::THREADS;                                                        \
+    *smem = variant == 2 ? StreamGeom<NA, NB>::SMEM : PhasedGeom<NA, NB>::SMEM;                    \
+    *tiles0 = PhasedGeom<NA, NB>::TILES0;                                                          \
+    *tiles1 = PhasedGeom<NA, NB>::TILES1;                                                          \
     break;
     FFTGEN_PHASED_SHAPES(FFTGEN_PG)
 #undef FFTGEN_PG
@@ -424,14 +424,14 @@ void phased_geom(int l0, int l1, int64_t *threads, int64_t *smem, int64_t *tiles
 
 bool phased_supported(int l0, int l1) {
   int64_t t, m, a, b;
-  phased_geom(l0, l1, &t, &m, &a, &b);
+  phased_geom(l0, l1, 1, &t, &m, &a, &b);
   return t > 0;
 }
 
-cudaError_t phased_prepare(int l0, int l1, int *bps) {
+cudaError_t phased_prepare(int l0, int l1, int variant, int *bps) {
   *bps = 1 << 30;
-  cudaError_t e = phased_prepare_f(l0, l1, bps);
-  return e != cudaSuccess ? e : phased_prepare_b(l0, l1, bps);
+  cudaError_t e = phased_prepare_f(l0, l1, bps, variant);
+  return e != cudaSuccess ? e : phased_prepare_b(l0, l1, bps, variant);
 }
 
 cudaError_t phased_launch(int l0, int l1, int layout, int dir, const PhasedArgs &pa, int grid, cudaStream_t s) {

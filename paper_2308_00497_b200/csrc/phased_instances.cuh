@@ -7,20 +7,31 @@
 
 namespace fftgen_b200 {
 
+// variant 1: TMA tiles (fft_phased_kernel); 2: plain tiles (fft_stream_kernel)
 template <int NS0, int NS1, int L, int DIR>
 cudaError_t phased_launch_t(const PhasedArgs &pa, int grid, cudaStream_t s) {
-  using PG = PhasedGeom<NS0, NS1>;
   void *args[] = {const_cast<PhasedArgs *>(&pa)};
+  if (pa.variant == 2)
+    return cudaLaunchCooperativeKernel((const void *)fft_stream_kernel<NS0, NS1, L, L, DIR>, dim3(grid),
+                                       dim3(StreamGeom<NS0, NS1>::THREADS), args, StreamGeom<NS0, NS1>::SMEM, s);
   return cudaLaunchCooperativeKernel((const void *)fft_phased_kernel<NS0, NS1, L, L, DIR>, dim3(grid),
-                                     dim3(PG::THREADS), args, PG::SMEM, s);
+                                     dim3(PhasedGeom<NS0, NS1>::THREADS), args, PhasedGeom<NS0, NS1>::SMEM, s);
 }
 
-template <int NS0, int NS1, int L, int DIR> cudaError_t phased_prepare_t(int *bps) {
-  using PG = PhasedGeom<NS0, NS1>;
-  auto k = fft_phased_kernel<NS0, NS1, L, L, DIR>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PG::SMEM);
+template <int NS0, int NS1, int L, int DIR> cudaError_t phased_prepare_t(int *bps, int variant) {
+  cudaError_t e;
   int n = 0;
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, PG::THREADS, PG::SMEM);
+  if (variant == 2) {
+    auto k = fft_stream_kernel<NS0, NS1, L, L, DIR>;
+    using SG = StreamGeom<NS0, NS1>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SG::SMEM);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, SG::THREADS, SG::SMEM);
+  } else {
+    auto k = fft_phased_kernel<NS0, NS1, L, L, DIR>;
+    using PG = PhasedGeom<NS0, NS1>;
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, PG::SMEM);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, PG::THREADS, PG::SMEM);
+  }
   if (n < *bps) *bps = n;
   return e;
 }
@@ -30,9 +41,9 @@ cudaError_t phased_launch_l(int layout, const PhasedArgs &pa, int grid, cudaStre
   return layout == LAYOUT_SPLIT ? phased_launch_t<NS0, NS1, LAYOUT_SPLIT, DIR>(pa, grid, s)
                                 : phased_launch_t<NS0, NS1, LAYOUT_INTERLEAVED, DIR>(pa, grid, s);
 }
-template <int NS0, int NS1, int DIR> cudaError_t phased_prepare_l(int *bps) {
-  cudaError_t e = phased_prepare_t<NS0, NS1, LAYOUT_SPLIT, DIR>(bps);
-  return e != cudaSuccess ? e : phased_prepare_t<NS0, NS1, LAYOUT_INTERLEAVED, DIR>(bps);
+template <int NS0, int NS1, int DIR> cudaError_t phased_prepare_l(int *bps, int variant) {
+  cudaError_t e = phased_prepare_t<NS0, NS1, LAYOUT_SPLIT, DIR>(bps, variant);
+  return e != cudaSuccess ? e : phased_prepare_t<NS0, NS1, LAYOUT_INTERLEAVED, DIR>(bps, variant);
 }
 
 #define FFTGEN_PHASED_SHAPES(X)                                                                        \
@@ -49,10 +60,10 @@ cudaError_t phased_launch_dir(int l0, int l1, int layout, const PhasedArgs &pa, 
   default: return cudaErrorInvalidValue;
   }
 }
-template <int DIR> cudaError_t phased_prepare_dir(int l0, int l1, int *bps) {
+template <int DIR> cudaError_t phased_prepare_dir(int l0, int l1, int *bps, int variant) {
   switch (l0 * 16 + l1) {
 #define FFTGEN_PH_PREPARE(A, B, NA, NB) \
-  case A * 16 + B: return phased_prepare_l<NA, NB, DIR>(bps);
+  case A * 16 + B: return phased_prepare_l<NA, NB, DIR>(bps, variant);
     FFTGEN_PHASED_SHAPES(FFTGEN_PH_PREPARE)
 #undef FFTGEN_PH_PREPARE
   default: return cudaErrorInvalidValue;
@@ -64,6 +75,8 @@ template <int DIR> cudaError_t phased_prepare_dir(int l0, int l1, int *bps) {
                                      cudaStream_t s) {                                                \
     return phased_launch_dir<DIR>(l0, l1, layout, pa, grid, s);                                       \
   }                                                                                                   \
-  cudaError_t phased_prepare_##SUFFIX(int l0, int l1, int *bps) { return phased_prepare_dir<DIR>(l0, l1, bps); }
+  cudaError_t phased_prepare_##SUFFIX(int l0, int l1, int *bps, int variant) {                         \
+    return phased_prepare_dir<DIR>(l0, l1, bps, variant);                                             \
+  }
 
 }  // namespace fftgen_b200

@@ -300,7 +300,9 @@ def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch
                                               (17, 77, 3), (18, 20, 24), (19, 7, 8), (20, 5, 8), (20, 2, 24)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 @pytest.mark.parametrize("direction", [-1, 1])
-def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layout, direction, monkeypatch):
+@pytest.mark.parametrize("variant,lag", [("1", "1"), ("2", "1"), ("2", "3")])
+def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layout, direction, variant, lag,
+                                               monkeypatch):
     """K6 (both groups in one cooperative launch, chunks alternating between two
     L2-resident slots, grid barrier per chunk, intermediate discarded after use)
     (opt-in) is bitwise the two-launch K3 path, for ragged last chunks, one-transform
@@ -309,7 +311,8 @@ def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layo
     g = torch.Generator(device="cuda").manual_seed(200 + l2)
     x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
     monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
-    monkeypatch.setenv("FFTGEN_PHASED", "1")
+    monkeypatch.setenv("FFTGEN_PHASED", variant)
+    monkeypatch.setenv("FFTGEN_PHASE_LAG", lag)
     monkeypatch.setenv("FFTGEN_PHASE_SLOT_MB", str(slot_mb))
 
     def run_once():
@@ -328,10 +331,10 @@ def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layo
         return y, d
 
     ph, d1 = run_once()
-    assert "fft_phased_kernel" in d1
+    assert ("fft_phased_kernel" if variant == "1" else "fft_stream_kernel") in d1
     monkeypatch.setenv("FFTGEN_PHASED", "0")
     two, d2 = run_once()
-    assert "fft_phased_kernel" not in d2
+    assert "fft_phased_kernel" not in d2 and "fft_stream_kernel" not in d2
     assert torch.equal(ph, two)
     for b in (0, batch - 1):
         xi = x[b].reshape(-1).double().cpu().numpy()
