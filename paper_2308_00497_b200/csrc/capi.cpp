@@ -214,7 +214,7 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
                               (dist * esz) % 16 == 0;
     if (p->use_cluster && rows_aligned) {
       // persistent clusters, one transform per cluster at a time; group-0
-      // tiles arrive by cp.async.bulk, the intermediate moves through DSMEM
+      // tiles arrive as TMA tensor boxes, the intermediate moves through DSMEM
       ClusterArgs c{};
       c.in0 = in0;
       c.in1 = in1;
@@ -227,10 +227,10 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       c.tw_local1 = p->d_tw + gs[1].local_off;
       c.tw_q = p->d_twg + gs[1].q_off;
       c.tw_p = p->d_twg + gs[1].p_off;
-      cudaError_t e = cluster_encode_maps(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, c);
-      if (e != cudaSuccess) return e;
-      return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
-                            p->max_clusters, s);
+      // a tensor map the driver rejects takes the two-launch path below
+      if (cluster_encode_maps(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, c) == cudaSuccess)
+        return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
+                              p->max_clusters, s);
     }
     if (p->use_phased) {
       // one cooperative launch; chunks stream through two L2-resident slots
