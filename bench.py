@@ -188,10 +188,10 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local)  # before NCCL init: each rank's communicator binds its own GPU
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     n, batch = a.n, a.batch
     direction = fg.FORWARD if a.direction == "forward" else fg.INVERSE
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=a.layout, batch=batch, device=local,
