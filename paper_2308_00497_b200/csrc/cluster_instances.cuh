@@ -64,7 +64,7 @@ template <int NS0, int NS1, int C, int DIR> cudaError_t cluster_prepare_l(int *m
 // is a non-portable cluster size.
 #define FFTGEN_CLUSTER_SHAPES(X)                                                                          \
   X(7, 7, 128, 128, 2) X(7, 7, 128, 128, 4) X(7, 8, 128, 256, 4) X(7, 8, 128, 256, 8) X(8, 8, 256, 256, 8) \
-  X(8, 8, 256, 256, 16) X(8, 9, 256, 512, 16)
+  X(8, 8, 256, 256, 16)
 #define FFTGEN_CLUSTER_KEY(A, B, C) ((A) * 4096 + (B) * 64 + (C))
 
 template <int DIR> cudaError_t cluster_launch_dir(int l0, int l1, int c, int layout, const ClusterArgs &a,

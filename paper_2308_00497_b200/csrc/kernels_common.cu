@@ -270,7 +270,7 @@ cudaError_t cluster_prepare_b(int, int, int, int *);
 //   2^15 C=8: split 13.8 vs 12.5, interleaved 14.5 vs 12.3
 //   2^16 C=16: split 12.9 vs 12.6, interleaved 13.7 vs 14.4 (K3 with the TMA
 //              first group: split 0.764 ms vs 0.835 ms for K5)
-//   2^17 C=16: split 10.4 vs 12.0, interleaved 10.7 vs 13.2
+//   2^17 C=16: split 10.4 vs 12.0, interleaved 10.7 vs 13.2 (shape dropped: 2^17 now splits 2^9 x 2^8)
 // 2^14 (FFTGEN_CLUSTER14 plans) C=4: 14.6 vs 17.0 for the K2 block kernel.
 int cluster_default_size(int l0, int l1, int /*layout*/) {
   switch (l0 * 16 + l1) {

@@ -47,7 +47,7 @@ template <int NS0, int NS1, int DIR> cudaError_t phased_prepare_l(int *bps, int 
 }
 
 #define FFTGEN_PHASED_SHAPES(X)                                                                        \
-  X(7, 8, 128, 256) X(8, 8, 256, 256) X(8, 9, 256, 512) X(9, 9, 512, 512) X(9, 10, 512, 1024)        \
+  X(7, 8, 128, 256) X(8, 8, 256, 256) X(8, 9, 256, 512) X(9, 8, 512, 256) X(9, 9, 512, 512) X(9, 10, 512, 1024) \
   X(10, 10, 1024, 1024)
 
 template <int DIR>

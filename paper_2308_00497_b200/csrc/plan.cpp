@@ -225,7 +225,7 @@ ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
 
 std::vector<int> group_split(int log2n) {
   // 2 groups up to 2^20 (NS <= 2^10), 3 groups up to 2^28, 4 groups up to
-  // 2^30; sizes as even as possible, larger ones last.  Measured on B200:
+  // 2^30; sizes as even as possible.  Measured on B200:
   // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
   // 64-byte segments).  FFTGEN_GROUP_MAX_LOG2=L allows 3 groups up to 2^(3L).
@@ -233,7 +233,13 @@ std::vector<int> group_split(int log2n) {
   if (const char *env = std::getenv("FFTGEN_GROUP_MAX_LOG2")) max3 = 3 * std::atoi(env);
   int g = log2n <= 20 ? 2 : (log2n <= max3 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
-  for (int i = 0; i < log2n % g; ++i) out[g - 1 - i] += 1;
+  // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs
+  // it (measured on B200: 2^17 0.45 / 0.47 vs 0.42 / 0.45, 2^25 0.29 / 0.30 vs
+  // 0.27 / 0.28 split / interleaved); otherwise the larger groups go last
+  // (2^19 as 10+9: 0.36 vs 0.38).  FFTGEN_LARGE_FIRST=0 / 1 forces either.
+  bool large_first = log2n / g == 8 && log2n % g == 1;
+  if (const char *lf = std::getenv("FFTGEN_LARGE_FIRST")) large_first = lf[0] == '1';
+  for (int i = 0; i < log2n % g; ++i) out[large_first ? i : g - 1 - i] += 1;
   return out;
 }
 

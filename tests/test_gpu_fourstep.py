@@ -195,7 +195,7 @@ def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
 
 
 @pytest.mark.parametrize("l2,batch,csize", [(14, 301, 2), (14, 301, 4), (15, 301, 4), (15, 301, 8),
-                                            (16, 150, 8), (16, 150, 16), (17, 77, 16)])
+                                            (16, 150, 8), (16, 150, 16)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 @pytest.mark.parametrize("direction", [-1, 1])
 def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layout, direction, monkeypatch):
