@@ -155,7 +155,8 @@ template <int N> struct TmaGeom {
   static constexpr int T = BlockGeom<N>::T;
   static constexpr int tp_threads = T >= 128 ? 1 : 128 / T;
   static constexpr int tp_bytes = (32768 / (8 * N)) > 0 ? 32768 / (8 * N) : 1;
-  static constexpr int TP = tp_threads < tp_bytes ? tp_threads : tp_bytes;
+  // N = 2048 runs one transform (one warp) per CTA (measured below)
+  static constexpr int TP = N == 2048 ? 1 : (tp_threads < tp_bytes ? tp_threads : tp_bytes);
   using G = BlockGeom<N, TP>;
   static constexpr int THREADS = G::THREADS;
   // Stages per CTA, measured on B200 (scripts/gpu_ab.sh, 1 GiB batches):
@@ -166,7 +167,9 @@ template <int N> struct TmaGeom {
 #ifdef FFTGEN_K2_STAGES
   static constexpr int STAGES = FFTGEN_K2_STAGES;
 #else
-  static constexpr int STAGES = N == 4096 ? 1 : 2;
+  // N = 2048 likewise with one-warp, one-transform CTAs (0.87 vs 0.85; the
+  // same change at 1024 loses: 0.87 vs 0.89).
+  static constexpr int STAGES = (N == 4096 || N == 2048) ? 1 : 2;
 #endif
   static constexpr int RAW = 8 * N;                                   // bytes per transform
   static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes

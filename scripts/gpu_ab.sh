@@ -1,11 +1,9 @@
-run() { timeout 300 python scripts/sweep.py --sizes 12,11,13,10 --layouts split,interleaved --steps 30 2>&1 | grep '"n"' | python -c "
+run() { timeout 300 python scripts/sweep.py --sizes $2 --layouts split,interleaved --steps 30 2>&1 | grep '"n"' | python -c "
 import sys,json
 for l in sys.stdin:
-    d=json.loads(l); print('$1', d['n'], d['layout'], d['variant'], d['frac'], d['ms'], d['kernel'])"
-  python -c "
-import paper_2308_00497_b200 as fg
-print('$1', fg.compile_pipeline(fg.PipelineConfig(n=4096, layout='split', batch=65536)).describe().splitlines()[2])"
+    d=json.loads(l); print('$1', d['n'], d['layout'], d['frac'], d['ms'], d['kernel'])"
 }
-run CARVE
-cp paper_2308_00497_b200/lib_m7/libfftgen_b200.so paper_2308_00497_b200/lib/
-run CARVE_M7
+cp paper_2308_00497_b200/lib/libfftgen_b200.so /tmp/base.so
+run BASE 10,11
+for v in vA vB vC; do cp paper_2308_00497_b200/lib_$v/libfftgen_b200.so paper_2308_00497_b200/lib/; run $v 10,11; done
+cp /tmp/base.so paper_2308_00497_b200/lib/libfftgen_b200.so
