@@ -122,7 +122,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU legs
-def cpu_reference_rate(a, budget_s: float, threads: int) -> dict:
+def cpu_reference_rate(a, budget_s: float, threads: int, with_aot: bool = True) -> dict:
     """The reference's own CPU path (compile_pipeline + interpret, fp64,
     oracle/_ref) batch-parallel over `threads` host cores on a bounded sample
     of the workload; GFLOP/s of 5N log2N."""
@@ -146,9 +146,38 @@ def cpu_reference_rate(a, budget_s: float, threads: int) -> dict:
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
+    out = {"value": gflop(a.n, done) / el, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+           "sample": f"{done} transforms of N={a.n} {lay} (fp32-rounded seeded_input), "
+                     f"compile_pipeline(stockham, radix 4)+interpret fp64, {el:.1f} s wall, "
+                     f"{threads} threads"}
+    aot = cpu_aot_rate(a, x if lay == "split" else None, min(4.0, budget_s), threads) if with_aot else None
+    if aot is not None:
+        out["aot_emit_c"] = aot
+    return out
+
+
+def cpu_aot_rate(a, x_split, budget_s: float, threads: int):
+    """The reference's ahead-of-time path (its emit_c output for this plan,
+    compiled -O3, oracle/_ref/libref_aot.so) on the same sample: reported
+    beside the interpreter, which is the reference's execute API."""
+    import oracle
+    if a.n != oracle.AotRef.N or a.layout != oracle.AotRef.LAYOUT or x_split is None:
+        return None
+    if not os.path.exists(oracle.AOT_SO):
+        return {"value": None, "sample": "oracle/_ref/libref_aot.so not built"}
+    aot = oracle.AotRef()
+    xb = np.tile(x_split, (max(1, 4096 // x_split.shape[0]), 1))
+    aot.forward(xb[:threads], threads)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        aot.forward(xb, threads)
+        done += xb.shape[0]
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
     return {"value": gflop(a.n, done) / el, "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-            "sample": f"{done} transforms of N={a.n} {lay} (fp32-rounded seeded_input), "
-                      f"compile_pipeline(stockham, radix 4)+interpret fp64, {el:.1f} s wall, "
+            "sample": f"{done} transforms, the reference's emit_c output for (N={a.n}, stockham radix 4, "
+                      f"split) compiled -O3 -march=x86-64-v3, _Thread_local scratch, {el:.1f} s wall, "
                       f"{threads} threads"}
 
 
@@ -340,13 +369,24 @@ def run_reference(a):
     # batch would take ~1 min per step on the interpreter)
     per_step = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
     for _ in range(a.warmup):
-        cpu_reference_rate(a, per_step / 2, threads)
+        cpu_reference_rate(a, per_step / 2, threads, with_aot=False)
     vals, samples = [], []
     for _ in range(a.steps):
-        r = cpu_reference_rate(a, per_step, threads)
+        r = cpu_reference_rate(a, per_step, threads, with_aot=False)
         vals.append(r["value"])
         samples.append(r["sample"])
     v = float(np.mean(vals))
+    # the reference's ahead-of-time C path on the same workload, reported beside it once
+    aot = None
+    if a.layout == "split":
+        ref_x = None
+        try:
+            ref = oracle.Ref()
+            ref_x = oracle.relayout_to_split(np.stack([ref.seeded_input(a.n, 1 + b) for b in range(64)]))
+            ref_x = ref_x.astype(np.float32).astype(np.float64)
+        except Exception:
+            pass
+        aot = cpu_aot_rate(a, ref_x, 4.0, threads)
     line = {
         "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(gflop(a.n, a.batch) / v * 1e3, 1),
@@ -354,7 +394,7 @@ def run_reference(a):
         "data": "synthetic: fp32-rounded seeded_input (verify.cpp:69-78)", "config": workload(a),
         "impl": "reference",
         "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": samples[-1]},
+                         "sample": samples[-1], "aot_emit_c": aot},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference = unmodified fftgen compile_pipeline+interpret (oracle/_ref), batch-parallel "
                 "one transform per thread; ms_per_step extrapolated to the full batch",

@@ -24,6 +24,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "libfftgen_oracle.so")
+AOT_SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "libref_aot.so")
 REF_SO = os.path.join(HERE, "_ref", "libfftgen_ref.so")
 
 ALG = {"cooley-tukey": 0, "ct": 0, "stockham": 1}
@@ -280,6 +281,29 @@ class Ref:
 
     def mflops(self, n: int, seconds: float) -> float:
         return self.lib.ref_mflops(n, seconds)
+
+
+class AotRef:
+    """The reference's ahead-of-time C path (emit_c output for N=4096,
+    Stockham radix 4, split layout) with a batch-parallel driver
+    (oracle/_ref/libref_aot.so, built by oracle/build_aot.py).  Baseline
+    infrastructure only: bench.py's cpu_baseline leg and tests."""
+
+    N, ALG, RADIX, LAYOUT = 4096, "stockham", 4, "split"
+
+    def __init__(self, path: str = AOT_SO):
+        self.lib = C.CDLL(path)
+        self.lib.ref_aot_batch.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_int]
+        self.lib.ref_aot_batch.restype = C.c_int
+
+    def forward(self, x: np.ndarray, threads: int = 1) -> np.ndarray:
+        """x: (batch, 2N) float64 in the split ComplexBuffer layout [re N | im N]."""
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, 2 * self.N)
+        y = np.empty_like(x)
+        rc = self.lib.ref_aot_batch(_ptr(x), _ptr(y), x.shape[0], self.N, threads)
+        if rc != 0:
+            raise RuntimeError("ref_aot_batch failed")
+        return y
 
 
 def relayout_to_split(inter: np.ndarray) -> np.ndarray:

@@ -5,6 +5,8 @@ reference (tests/golden/make_golden.py) or, where oracle/_ref exists, against
 the reference library itself.  Bit-exact unless stated: the restatement
 follows the lowered arithmetic of lower_complex.cpp operation for operation.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -169,3 +171,15 @@ def test_plan_errors_mirror_reference(orc):
         orc.fuse(16, "stockham", 3)   # PlanError: radix not a power of two
     with pytest.raises(RuntimeError):
         orc.fuse(256, "stockham", 128)  # FuseError: kernel cap 64
+
+
+def test_reference_aot_path_matches_interpreter(ref):
+    """The reference's emit_c output (oracle/_ref/libref_aot.so, the CPU
+    baseline's ahead-of-time leg) is bitwise the reference interpreter."""
+    if not os.path.exists(oracle.AOT_SO):
+        pytest.skip("oracle/_ref/libref_aot.so not built (reference tree absent)")
+    a = oracle.AotRef()
+    x = oracle.relayout_to_split(np.stack([ref.seeded_input(a.N, 1 + b) for b in range(6)]))
+    got = a.forward(x, threads=3)
+    want = ref.forward(x, a.ALG, a.RADIX, a.LAYOUT, threads=3)
+    assert np.array_equal(got, want)
