@@ -38,9 +38,17 @@ template <> struct BlockPlan<4096> : PlanT<2, 64, 64, 1> {};
 template <> struct BlockPlan<8192> : PlanT<3, 32, 16, 16> {};
 template <> struct BlockPlan<16384> : PlanT<3, 32, 32, 16> {};
 
+// Plans of the K3 group sub-FFTs (default: the block plan of the same size).
+template <int N> struct GroupPlan : BlockPlan<N> {};
+#ifdef FFTGEN_GROUP3
+// three 8/16-point register passes: 64-register codelets, four CTAs per SM
+template <> struct GroupPlan<512> : PlanT<3, 8, 8, 8> {};
+template <> struct GroupPlan<1024> : PlanT<3, 8, 8, 16> {};
+#endif
+
 // TP = transforms per CTA.  0 -> the direct kernel's default (128 threads).
-template <int N, int TP_ = 0> struct BlockGeom {
-  using PL = BlockPlan<N>;
+template <int N, int TP_ = 0, class PL_ = BlockPlan<N>> struct BlockGeom {
+  using PL = PL_;
   static constexpr int P = PL::P;
   static constexpr int RMAX = PL::r(0) > PL::r(1) ? (PL::r(0) > PL::r(2) ? PL::r(0) : PL::r(2))
                                                   : (PL::r(1) > PL::r(2) ? PL::r(1) : PL::r(2));
@@ -78,8 +86,8 @@ struct Pad {
 FFTGEN_HD constexpr int padded(int i, Pad pd) { return pd.K ? i + pd.K * (i / pd.PP) : i; }
 
 // ELEM = element bytes: 8 (float2 exchange) or 4 (one re/im plane).
-template <int N, int ELEM = 8> struct PadSearch {
-  using G = BlockGeom<N>;
+template <int N, int ELEM = 8, class PL = BlockPlan<N>> struct PadSearch {
+  using G = BlockGeom<N, 0, PL>;
   static constexpr int WAVE = 128 / ELEM;  // lanes served per shared-memory wavefront
   // Representative registers x and butterflies j suffice: the access
   // patterns are affine in both.
@@ -131,16 +139,16 @@ template <int N, int ELEM = 8> struct PadSearch {
   }
 };
 
-template <int N, int p, int ELEM = 8> struct BoundaryPad {
-  static constexpr Pad value = BlockGeom<N>::P > 1 ? PadSearch<N, ELEM>::best(p) : Pad{16, 0};
+template <int N, int p, int ELEM = 8, class PL = BlockPlan<N>> struct BoundaryPad {
+  static constexpr Pad value = BlockGeom<N, 0, PL>::P > 1 ? PadSearch<N, ELEM, PL>::best(p) : Pad{16, 0};
   static constexpr int region = padded(N - 1, value) + 1;
-  static constexpr int wavefronts = BlockGeom<N>::P > 1 ? PadSearch<N, ELEM>::cost(p, value) : 0;
+  static constexpr int wavefronts = BlockGeom<N, 0, PL>::P > 1 ? PadSearch<N, ELEM, PL>::cost(p, value) : 0;
 };
 
-template <int N> struct SmemGeom {
-  using G = BlockGeom<N>;
-  static constexpr int r0 = BoundaryPad<N, 0>::region;
-  static constexpr int r1 = G::P > 2 ? BoundaryPad<N, 1>::region : 0;
+template <int N, class PL = BlockPlan<N>> struct SmemGeom {
+  using G = BlockGeom<N, 0, PL>;
+  static constexpr int r0 = BoundaryPad<N, 0, 8, PL>::region;
+  static constexpr int r1 = G::P > 2 ? BoundaryPad<N, 1, 8, PL>::region : 0;
   static constexpr int REGION = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;  // float2 per transform
   static constexpr int BYTES = G::TPB * REGION * 8;
 };
@@ -216,19 +224,20 @@ template <int N> struct Tma1Geom {
 #define FFTGEN_GROUP_TILE_LARGE 65536
 #endif
 template <int NS, int MAXT = 512> struct GroupGeom {
-  static constexpr int T = BlockGeom<NS>::T;
+  using PL = GroupPlan<NS>;
+  static constexpr int T = BlockGeom<NS, 0, PL>::T;
   static constexpr int TILE_BYTES = NS <= 256 ? FFTGEN_GROUP_TILE_SMALL : FFTGEN_GROUP_TILE_LARGE;
   static constexpr int TC_BYTES = TILE_BYTES / (8 * NS);                // transforms per tile
   static constexpr int TC = TC_BYTES * T > MAXT ? MAXT / T : TC_BYTES;  // <= MAXT threads
-  using G = BlockGeom<NS, TC>;
+  using G = BlockGeom<NS, TC, PL>;
   static constexpr int THREADS = G::THREADS;
-  static constexpr int EX = SmemGeom<NS>::REGION > NS ? SmemGeom<NS>::REGION : NS;
+  static constexpr int EX = SmemGeom<NS, PL>::REGION > NS ? SmemGeom<NS, PL>::REGION : NS;
   static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
   static constexpr int BYTES = TC * REG * 8;
   // resident CTAs the register budget must allow: 16-point codelets fit 64
   // registers, 32-point ones (NS >= 512) need 128
   static constexpr int MIN_BLOCKS =
-      BlockGeom<NS>::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3));
+      G::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3));
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };

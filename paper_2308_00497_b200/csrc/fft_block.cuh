@@ -77,7 +77,7 @@ FFTGEN_FI void pass0(int t, float2 *v, Load &&load) {
 template <class G, int N, int p>
 FFTGEN_FI void smem_write(float2 *sx, int t, const float2 *v) {
   constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R;
-  constexpr Pad pd = BoundaryPad<N, p>::value;
+  constexpr Pad pd = BoundaryPad<N, p, 8, typename G::PL>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
@@ -89,7 +89,7 @@ FFTGEN_FI void smem_write(float2 *sx, int t, const float2 *v) {
 template <class G, int N, int p, int DIR>
 FFTGEN_FI void smem_read_pass(const float2 *sx, int t, const float2 *__restrict__ tw, float2 *v) {
   constexpr int R = G::R(p), k = G::K(p), cols = G::COLS(p), J = G::RMAX / R;
-  constexpr Pad pd = BoundaryPad<N, p - 1>::value;
+  constexpr Pad pd = BoundaryPad<N, p - 1, 8, typename G::PL>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
@@ -129,7 +129,7 @@ template <class G> struct TwPQ {
 template <class G, int N, int DIR>
 FFTGEN_FI void smem_read_pass1_pq(const float2 *sx, int t, const TwPQ<G> &w, float2 *v) {
   constexpr int R = G::R(1);
-  constexpr Pad pd = BoundaryPad<N, 0>::value;
+  constexpr Pad pd = BoundaryPad<N, 0, 8, typename G::PL>::value;
   static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == R, "factored twiddles need a 2-pass plan");
 #pragma unroll
   for (int A = 0; A < R; ++A) v[A] = w.template apply<DIR>(sx[padded(t * R + A, pd)], A);

@@ -90,6 +90,20 @@ template <int BARID, int THREADS> FFTGEN_FI void compute_sync() {
 
 // One tile of one group: TC adjacent transforms (tile index tt) of the
 // transform whose input / output start at element offsets ib / ob.
+// Passes 1 .. P-1 of a group sub-FFT whose pass-0 results sit in the padded
+// exchange (this column at Xf); lanes run over the tile's columns, thread t
+// owns the pass-p butterflies t + j T.
+template <class G, int NS, int DIR, int BARID, int THREADS>
+FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ tw, float2 *v) {
+  smem_read_pass<G, NS, 1, DIR>(Xf, t, tw, v);
+  if constexpr (G::P == 3) {
+    compute_sync<BARID, THREADS>();  // pass-1 reads done before the rewrite
+    smem_write<G, NS, 1>(Xf, t, v);
+    compute_sync<BARID, THREADS>();
+    smem_read_pass<G, NS, 2, DIR>(Xf, t, tw, v);
+  }
+}
+
 // DISCARD (rows tiles): once pass 0 has read the tile, its 128-byte L2 lines
 // are dropped without write-back (discard.global.L2) -- the tile is an
 // L2-resident intermediate no one reads again.
@@ -98,9 +112,10 @@ template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS
 FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
-  static_assert(G::P == 2 && G::K(1) == 1 && G::RMAX == G::R(1), "group sub-FFTs are 2-pass plans");
+  static_assert((G::P == 2 || G::P == 3) && G::K(G::P - 1) == 1 && G::RMAX == G::R(G::P - 1),
+                "group sub-FFTs: 2 or 3 register passes, the last one a full-width stage");
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
-  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  constexpr int R1 = G::R(G::P - 1), COLS1 = G::COLS(G::P - 1);  // the last pass
   const int tid = threadIdx.x;
   int64_t m0, c0;
   if (ROWS) {
@@ -153,8 +168,8 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
   {
     const int f = tid % TC;
     const int t = tid / TC;  // pass-1 butterfly m1 = t (k == 1, J == 1)
-    // local pass-1 twiddles w^{A t}: lanes share t -> L1 broadcast loads
-    smem_read_pass<G, NS, 1, DIR>(smem + f * REG, t, a.tw_local, v);
+    // local pass twiddles w^{A t}: lanes share t -> L1 broadcast loads
+    group_passes_rest<G, NS, DIR, BARID, GG::THREADS>(smem + f * REG, t, a.tw_local, v);
 #pragma unroll
     for (int B = 0; B < R1; ++B) {
       const int64_t e = B * COLS1 + t;  // local output index

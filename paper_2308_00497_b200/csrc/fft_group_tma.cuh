@@ -80,7 +80,7 @@ FFTGEN_FI void tile_from_stage(const GroupArgs &a, char *stage, int64_t ob, int6
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
-  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  constexpr int R1 = G::R(G::P - 1), COLS1 = G::COLS(G::P - 1);  // the last pass
   const int tid = threadIdx.x;
   float2 *X = reinterpret_cast<float2 *>(stage);
   float2 v[G::RMAX];
@@ -120,7 +120,7 @@ FFTGEN_FI void tile_from_stage(const GroupArgs &a, char *stage, int64_t ob, int6
   __syncthreads();
   const int f = tid % TC;
   const int t = tid / TC;
-  smem_read_pass<G, NS, 1, DIR>(X + f * REG, t, a.tw_local, v);
+  group_passes_rest<G, NS, DIR, 0, GG::THREADS>(X + f * REG, t, a.tw_local, v);
 #pragma unroll
   for (int B = 0; B < R1; ++B) {
     const int64_t e = B * COLS1 + t;
@@ -136,7 +136,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
   using G = typename TG::GG::G;
   constexpr int TC = TG::TC, REG = TG::REG, T = G::T;
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
-  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  constexpr int R1 = G::R(G::P - 1), COLS1 = G::COLS(G::P - 1);  // the last pass
   const GroupArgs &a = ta.g;
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
@@ -213,7 +213,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     // ---- pass 1: exchange -> registers (lanes over f), codelet, HBM store ----
     const int f = tid % TC;
     const int t = tid / TC;
-    smem_read_pass<G, NS, 1, DIR>(X + f * REG, t, a.tw_local, v);
+    group_passes_rest<G, NS, DIR, 0, TG::THREADS>(X + f * REG, t, a.tw_local, v);
     __syncthreads();  // stage free: fetch the tile two items ahead
     if (tid == 0 && item + NST * stride < total) {
       fence_proxy_async();

@@ -72,6 +72,32 @@ std::vector<float> block_twiddles(int log2n) {
   return out;
 }
 
+// the same [A][m] tables for a K3 group's NS-point sub-FFT plan (GroupPlan)
+std::vector<float> group_twiddles(int log2ns) {
+  std::vector<float> out;
+  auto emit = [&](auto geom) {
+    using G = decltype(geom);
+    for (int p = 1; p < G::P; ++p) {
+      const int64_t R = G::R(p), cols = G::COLS(p), s = R * cols;
+      for (int64_t A = 0; A < R; ++A)
+        for (int64_t m = 0; m < cols; ++m) {
+          double re, im;
+          unit_root(s, A * m, &re, &im);
+          out.push_back(static_cast<float>(re));
+          out.push_back(static_cast<float>(im));
+        }
+    }
+  };
+  switch (log2ns) {
+  case 7: emit(BlockGeom<128, 0, GroupPlan<128>>{}); break;
+  case 8: emit(BlockGeom<256, 0, GroupPlan<256>>{}); break;
+  case 9: emit(BlockGeom<512, 0, GroupPlan<512>>{}); break;
+  case 10: emit(BlockGeom<1024, 0, GroupPlan<1024>>{}); break;
+  default: throw PlanError("no group kernel for 2^" + std::to_string(log2ns));
+  }
+  return out;
+}
+
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0) {
   switch (log2ns) {
 #define FFTGEN_GG(L, NN)               \

@@ -207,7 +207,7 @@ ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
       }
     if (!found) {
       d.local_off = (int64_t)p.tw_block.size() / 2;
-      const auto t = block_twiddles(d.log2ns);
+      const auto t = group_twiddles(d.log2ns);
       p.tw_block.insert(p.tw_block.end(), t.begin(), t.end());
     }
     if (d.cols > 1) {

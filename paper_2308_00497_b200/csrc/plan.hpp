@@ -90,5 +90,6 @@ ExecPlan build_exec_plan(int64_t n, bool fourstep_14 = false);
 int block_num_passes(int log2n);
 void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k);
 std::vector<float> block_twiddles(int log2n);
+std::vector<float> group_twiddles(int log2ns);
 
 }  // namespace fftgen_b200
