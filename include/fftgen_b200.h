@@ -26,11 +26,14 @@
  *   split:       re at in0[b*dist + e], im at in1[b*dist + e]
  *                (dist = n: planar arrays; the reference ComplexBuffer's
  *                 [re n | im n] block per transform is in1 = in0 + n, dist = 2n)
- *   out-of-place (in and out must not overlap); kernels are enqueued on the
+ *   out-of-place, or exactly in place (out0 == in0, out1 == in1); partially
+ *   overlapping buffers are not supported.  Kernels are enqueued on the
  *   caller's stream; the plan owns its twiddle tables and scratch.
  *   Plan creation and destruction are thread-safe; a plan may be executed
  *   concurrently from several host threads on different streams only when
- *   it needs no scratch (fftgen_plan_scratch_bytes() == 0).
+ *   it needs no scratch (fftgen_plan_scratch_bytes() == 0) and the data are
+ *   16-byte aligned with dist * element size a multiple of 16 (otherwise
+ *   cluster plans fall back to the scratch-using two-launch path).
  */
 #ifndef FFTGEN_B200_H
 #define FFTGEN_B200_H
