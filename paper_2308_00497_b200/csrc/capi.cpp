@@ -150,14 +150,17 @@ GroupArgs make_group_args(const fftgen_plan *p, int g, const void *in0, const vo
   return a;
 }
 
+// l2: the intermediate is an L2-resident chunk slot (2-group plans)
 cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void *in0, const void *in1,
-                         void *out0, void *out1, int64_t idist, int64_t odist, int64_t batch, cudaStream_t s) {
+                         void *out0, void *out1, int64_t idist, int64_t odist, int64_t batch, cudaStream_t s,
+                         bool l2 = false) {
   const GroupDesc &d = p->ex.groups[g];
   const bool first = g == 0, last = g + 1 == (int)p->ex.groups.size();
   const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
   const GroupArgs a = make_group_args(p, g, in0, in1, out0, out1, idist, odist);
-  const int shape = last ? (split ? 3 : 2) : (first ? (split ? 1 : 0) : 4);
-  if (g < (int)p->group_tma_grid.size() && p->group_tma_grid[g] > 0) {
+  const int shape = l2 ? (last ? (split ? 8 : 7) : (split ? 6 : 5))
+                      : (last ? (split ? 3 : 2) : (first ? (split ? 1 : 0) : 4));
+  if (!l2 && g < (int)p->group_tma_grid.size() && p->group_tma_grid[g] > 0) {
     GroupTmaArgs ta{};
     ta.g = a;
     ta.items = batch * a.tiles_per_outer;
@@ -272,13 +275,13 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
         if (c >= 2 && (e = cudaStreamWaitEvent(p->xs[0], p->ev_b[slot], 0)) != cudaSuccess) return e;
         const float *i0 = (const float *)in0 + b0 * dist * esz;
         const float *i1 = in1 ? (const float *)in1 + b0 * dist : nullptr;
-        if ((e = launch_group(p, 0, direction, i0, i1, buf, nullptr, dist, n, cnt, p->xs[0])) != cudaSuccess)
+        if ((e = launch_group(p, 0, direction, i0, i1, buf, nullptr, dist, n, cnt, p->xs[0], true)) != cudaSuccess)
           return e;
         if ((e = cudaEventRecord(p->ev_a[slot], p->xs[0])) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(p->xs[1], p->ev_a[slot], 0)) != cudaSuccess) return e;
         float *o0 = (float *)out0 + b0 * dist * esz;
         float *o1 = out1 ? (float *)out1 + b0 * dist : nullptr;
-        if ((e = launch_group(p, 1, direction, buf, nullptr, o0, o1, n, dist, cnt, p->xs[1])) != cudaSuccess)
+        if ((e = launch_group(p, 1, direction, buf, nullptr, o0, o1, n, dist, cnt, p->xs[1], true)) != cudaSuccess)
           return e;
         if ((e = cudaEventRecord(p->ev_b[slot], p->xs[1])) != cudaSuccess) return e;
       }

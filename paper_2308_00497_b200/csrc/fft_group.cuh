@@ -185,7 +185,9 @@ fft_group_kernel(const GroupArgs a) {
   extern __shared__ float4 smem_f4[];
   const int64_t b = blockIdx.x / a.tiles_per_outer;
   const int64_t tt = blockIdx.x - b * a.tiles_per_outer;
-  group_tile<NS, LIN, LOUT, DIR, ROWS>(a, b * a.idist, b * a.odist, tt, reinterpret_cast<float2 *>(smem_f4));
+  // rows read from an L2-resident intermediate drop its lines once read
+  group_tile<NS, LIN, LOUT, DIR, ROWS, GroupGeom<NS>, 0, LIN == LAYOUT_L2 && ROWS>(
+      a, b * a.idist, b * a.odist, tt, reinterpret_cast<float2 *>(smem_f4));
 }
 
 }  // namespace fftgen_b200
