@@ -224,6 +224,20 @@ FFTGEN_FI void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *ba
 }
 FFTGEN_FI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Raw stage layout of transform f of a group.  Packed (dist == N, the
+// group's transforms are one contiguous run): interleaved at f * 8N, split re
+// at f * 4N and im at TP * 4N + f * 4N, so one bulk copy per plane moves the
+// whole group; otherwise transform f sits in its slot at f * SLOT.
+template <int N, int LAYOUT> struct RawAt {
+  using TG = TmaGeom<N>;
+  static FFTGEN_FI char *re(char *stage, int f, bool packed) {
+    return stage + (packed ? f * (LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N) : f * TG::SLOT);
+  }
+  static FFTGEN_FI char *im(char *stage, int f, bool packed) {  // split only
+    return packed ? stage + TG::TP * 4 * N + f * 4 * N : stage + f * TG::SLOT + 4 * N;
+  }
+};
+
 template <int N, int LAYOUT>
 FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t group) {
   using TG = TmaGeom<N>;
@@ -231,6 +245,16 @@ FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t
   const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
   mbar_expect_tx(bar, (uint32_t)cnt * 8 * N);
+  if (a.idist == N) {  // packed: one copy per plane for the whole group
+    if (LAYOUT == LAYOUT_SPLIT) {
+      bulk_g2s(stage, reinterpret_cast<const float *>(a.in0) + b0 * N, cnt * plane, bar);
+      bulk_g2s(RawAt<N, LAYOUT>::im(stage, 0, true), reinterpret_cast<const float *>(a.in1) + b0 * N,
+               cnt * plane, bar);
+    } else {
+      bulk_g2s(stage, reinterpret_cast<const float2 *>(a.in0) + b0 * N, cnt * plane, bar);
+    }
+    return;
+  }
   for (int f = 0; f < cnt; ++f) {
     char *dst = stage + f * TG::SLOT;
     const int64_t b = b0 + f;
@@ -253,11 +277,12 @@ FFTGEN_FI void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "m
 FFTGEN_FI void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 FFTGEN_FI void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Stage the last pass's outputs in the slot (raw layout) for a bulk store.
+// Stage the last pass's outputs in the raw layout (RawAt) for a bulk store.
 template <class G, int N, int LAYOUT>
-FFTGEN_FI void smem_write_out(char *slot, int t, const float2 *v) {
+FFTGEN_FI void smem_write_out(char *stage, int f, bool packed, int t, const float2 *v) {
   constexpr int q = G::P - 1;
   constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / R;
+  char *re = RawAt<N, LAYOUT>::re(stage, f, packed);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
@@ -265,10 +290,10 @@ FFTGEN_FI void smem_write_out(char *slot, int t, const float2 *v) {
     for (int B = 0; B < R; ++B) {
       const int e = (B * cols + m) * k + c;
       if constexpr (LAYOUT == LAYOUT_SPLIT) {
-        reinterpret_cast<float *>(slot)[e] = v[j * R + B].x;
-        reinterpret_cast<float *>(slot)[N + e] = v[j * R + B].y;
+        reinterpret_cast<float *>(re)[e] = v[j * R + B].x;
+        reinterpret_cast<float *>(RawAt<N, LAYOUT>::im(stage, f, packed))[e] = v[j * R + B].y;
       } else {
-        reinterpret_cast<float2 *>(slot)[e] = v[j * R + B];
+        reinterpret_cast<float2 *>(re)[e] = v[j * R + B];
       }
     }
   }
@@ -280,6 +305,16 @@ FFTGEN_FI void tma_store(const BlockArgs &a, char *stage, int64_t group) {
   const int64_t b0 = group * TG::TP;
   const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
+  if (a.odist == N) {  // packed
+    if (LAYOUT == LAYOUT_SPLIT) {
+      bulk_s2g(reinterpret_cast<float *>(a.out0) + b0 * N, stage, cnt * plane);
+      bulk_s2g(reinterpret_cast<float *>(a.out1) + b0 * N, RawAt<N, LAYOUT>::im(stage, 0, true), cnt * plane);
+    } else {
+      bulk_s2g(reinterpret_cast<float2 *>(a.out0) + b0 * N, stage, cnt * plane);
+    }
+    bulk_commit();
+    return;
+  }
   for (int f = 0; f < cnt; ++f) {
     char *src = stage + f * TG::SLOT;
     const int64_t b = b0 + f;
@@ -309,6 +344,7 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
   const int t = tid - f * G::T;
   const int64_t groups = (args.batch + TG::TP - 1) / TG::TP;
   const int64_t stride = gridDim.x;
+  const bool packed_in = args.idist == N, packed_out = args.odist == N;
 
   if (tid == 0) {
     for (int s = 0; s < TG::STAGES; ++s) mbar_init(&bars[s], 1);
@@ -334,10 +370,11 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
 
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
-      const float *re = reinterpret_cast<const float *>(slot), *im = re + N;
+      const float *re = reinterpret_cast<const float *>(RawAt<N, LAYOUT>::re(stage, f, packed_in));
+      const float *im = reinterpret_cast<const float *>(RawAt<N, LAYOUT>::im(stage, f, packed_in));
       pass0<G, DIR>(t, v, [&](int e) { return make_float2(re[e], im[e]); });
     } else {
-      const float2 *x = reinterpret_cast<const float2 *>(slot);
+      const float2 *x = reinterpret_cast<const float2 *>(RawAt<N, LAYOUT>::re(stage, f, packed_in));
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
@@ -362,7 +399,7 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
     __syncthreads();  // exchange fully consumed
     const int64_t b = g * TG::TP + f;
     if constexpr (STORE_TMA) {
-      smem_write_out<G, N, LAYOUT>(slot, t, v);
+      smem_write_out<G, N, LAYOUT>(stage, f, packed_out, t, v);
       fence_proxy_async();  // make generic-proxy writes visible to the bulk copy
       __syncthreads();
       if (tid == 0) {

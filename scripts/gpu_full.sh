@@ -2,4 +2,5 @@ mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python scripts/sweep.py --sizes 17,25 --layouts split,interleaved --steps 10 2>&1 | grep '"n"' | cut -c1-200
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench_default.json')); print(d['value'], d['roofline']['frac'], d['e2e']['value'], d['cpu_baseline']['value'], d['cpu_baseline'].get('aot_emit_c',{}).get('value'))"
