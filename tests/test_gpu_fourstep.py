@@ -340,3 +340,32 @@ def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layo
         xi = x[b].reshape(-1).double().cpu().numpy()
         want = orc.forward(xi, "stockham", 4, inverse=direction > 0)
         assert oracle.rel_l2(ph[b].reshape(-1).double().cpu().numpy(), want) < 3e-6, b
+
+
+@pytest.mark.parametrize("l2", [21, 22])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_three_group_inverse_vs_oracle(fg, orc, l2, layout):
+    """Inverse (conjugate-root) instances of the first / middle / last group
+    kernels of a 3-group plan against the oracle."""
+    n = 1 << l2
+    x = seeded_batch(orc, n, 1, seed0=9)
+    got = run(fg, n, layout, 1, x)
+    want = orc.forward(x, "stockham", 4, inverse=True)
+    assert oracle.rel_l2(got[0], want[0]) <= tol(n)
+
+
+@pytest.mark.parametrize("l2", [28, 30])
+def test_huge_roundtrip_inverse(fg, l2):
+    """inverse(forward(x)) / N == x at 2^28 (3 groups) and 2^30 (4 groups):
+    the inverse instances of every group shape on the largest plans."""
+    n = 1 << l2
+    g = torch.Generator(device="cuda").manual_seed(l2)
+    x = torch.rand(n, 2, device="cuda", generator=g) * 2 - 1
+    y = torch.empty_like(x)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=1))
+    plan.execute(x, y)
+    plan.execute(y, y, direction=fg.INVERSE)  # in place
+    torch.cuda.synchronize()
+    err = (torch.linalg.norm((y / n - x).double()) / torch.linalg.norm(x.double())).item()
+    assert err < 1e-6, err
+    plan.close()
