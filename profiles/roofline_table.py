@@ -1,0 +1,34 @@
+"""profiles/sweep_r1.jsonl -> profiles/roofline_r1.md (single-pass and
+pass-aware fractions of the measured HBM peak per size, layout, direction).
+
+    python profiles/roofline_table.py
+"""
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def passes(kernel: str, launches: int) -> int:
+    if "cluster" in kernel or "block" in kernel:
+        return 1
+    return launches  # K3: one HBM pass per group launch
+
+
+def main():
+    rows = [json.loads(l) for l in open(os.path.join(HERE, "sweep_r1.jsonl"))]
+    out = ["# Roofline per configuration (round 1, B200, `scripts/sweep.py`)", "",
+           "Single-pass fraction = 16·N·batch bytes / time / measured HBM peak (6549 GB/s);",
+           "pass-aware = single-pass × HBM passes of the plan (the multi-pass bound).", "",
+           "| N | layout | dir | batch | TFLOP/s | ms | kernel | passes | single-pass frac | pass-aware frac |",
+           "|---|---|---|---|---|---|---|---|---|---|"]
+    for d in rows:
+        p = passes(d["kernel"], d["launches"])
+        direction = "inv" if d["variant"] == "inverse" else "fwd"
+        out.append(f"| {d['n']} | {d['layout']} | {direction} | {d['batch']} | {d['TFLOPs']} | {d['ms']} | "
+                   f"`{d['kernel']}` | {p} | {d['frac']:.3f} | {min(1.5, d['frac'] * p):.3f} |")
+    open(os.path.join(HERE, "roofline_r1.md"), "w").write("\n".join(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
