@@ -60,6 +60,8 @@ bool block_tma_enabled(int log2n) {
     const char *env = std::getenv("FFTGEN_TMA1");
     return Tma1Geom<16384>::ENABLED && env && env[0] == '1';
   }
+  case 6: return TmaGeom<64>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
+  case 7: return TmaGeom<128>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
   case 8: return TmaGeom<256>::ENABLED;
   case 9: return TmaGeom<512>::ENABLED;
   case 10: return TmaGeom<1024>::ENABLED;
@@ -74,7 +76,8 @@ void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem) {
   *threads = *tp = *smem = 0;
   switch (log2n) {
 #define FFTGEN_TG(L, NN) case L: *threads = TmaGeom<NN>::THREADS; *tp = TmaGeom<NN>::TP; *smem = TmaGeom<NN>::BYTES; return;
-  FFTGEN_TG(8, 256) FFTGEN_TG(9, 512) FFTGEN_TG(10, 1024) FFTGEN_TG(11, 2048) FFTGEN_TG(12, 4096) FFTGEN_TG(13, 8192)
+  FFTGEN_TG(6, 64) FFTGEN_TG(7, 128) FFTGEN_TG(8, 256) FFTGEN_TG(9, 512) FFTGEN_TG(10, 1024) FFTGEN_TG(11, 2048)
+  FFTGEN_TG(12, 4096) FFTGEN_TG(13, 8192)
   case 14: *threads = Tma1Geom<16384>::THREADS; *tp = 1; *smem = Tma1Geom<16384>::BYTES; return;
 #undef FFTGEN_TG
   default: return;
@@ -84,6 +87,8 @@ void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem) {
 int block_tma_transforms_per_cta(int log2n) {
   switch (log2n) {
   case 14: return 1;
+  case 6: return TmaGeom<64>::TP;
+  case 7: return TmaGeom<128>::TP;
   case 8: return TmaGeom<256>::TP;
   case 9: return TmaGeom<512>::TP;
   case 10: return TmaGeom<1024>::TP;
