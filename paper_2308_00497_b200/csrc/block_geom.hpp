@@ -160,26 +160,32 @@ template <int N, class PL = BlockPlan<N>> struct SmemGeom {
 // transforms; the raw input of group i+1 is fetched by cp.async.bulk into one
 // of STAGES stage buffers while group i is computed.  After pass 0 has read a
 // stage's raw data, the same stage buffer holds the padded exchange.
+// Geometry, measured on B200 (scripts/ab_libs.sh, 1 GiB batches): a 64 KB
+// group per stage (TP = 64 KB / 8N transforms, one packed bulk copy per
+// plane) and two stages per CTA run at 0.94-1.00 of the measured HBM peak
+// for N = 256 .. 2048 (256: 0.94 / 1.00 split / interleaved vs 0.85 / 0.92
+// with 16 KB groups; 512: 0.95 / 1.00 vs 0.86 / 0.90; 1024: 0.98 / 0.98 vs
+// 0.88 / 0.89; 2048: 0.98 / 0.98 vs 0.86 / 0.87) -- the group's TMA copies
+// are large and the compute of one group covers the next one's load.  N =
+// 4096 keeps one transform per CTA, single-buffered, six warps more per SM
+// (0.95-0.97; 2 x 2 transforms: 0.95), and 8192 is one transform per stage.
 template <int N> struct TmaGeom {
   static constexpr bool ENABLED = N >= 64 && N <= 8192;
   static constexpr int T = BlockGeom<N>::T;
-  static constexpr int tp_threads = T >= 128 ? 1 : 128 / T;
-  static constexpr int tp_bytes = (32768 / (8 * N)) > 0 ? 32768 / (8 * N) : 1;
-  // N = 2048 runs one transform (one warp) per CTA (measured below)
-  static constexpr int TP = N == 2048 ? 1 : (tp_threads < tp_bytes ? tp_threads : tp_bytes);
+  static constexpr int tp_bytes = (65536 / (8 * N)) > 0 ? 65536 / (8 * N) : 1;
+#ifdef FFTGEN_K2_TP_N  // experiments: override TP for one N
+  static constexpr int TP = N == FFTGEN_K2_TP_N ? FFTGEN_K2_TP : (N == 4096 ? 1 : tp_bytes);
+#else
+  static constexpr int TP = N == 4096 ? 1 : tp_bytes;
+#endif
   using G = BlockGeom<N, TP>;
   static constexpr int THREADS = G::THREADS;
-  // Stages per CTA, measured on B200 (scripts/gpu_ab.sh, 1 GiB batches):
-  // N = 4096 runs best single-buffered at twice the CTAs per SM (split 0.96
-  // vs 0.86 of the measured HBM peak, interleaved 0.93 vs 0.85 -- more warps
-  // hide the codelets' dependency latency while other CTAs' TMA traffic keeps
-  // HBM busy); the other sizes keep double buffering (2^13: 0.86 vs 0.76).
-#ifdef FFTGEN_K2_STAGES
+#if defined(FFTGEN_K2_STAGES)
   static constexpr int STAGES = FFTGEN_K2_STAGES;
+#elif defined(FFTGEN_K2_S2_N)
+  static constexpr int STAGES = (N == 4096 && N != FFTGEN_K2_S2_N) ? 1 : 2;
 #else
-  // N = 2048 likewise with one-warp, one-transform CTAs (0.87 vs 0.85; the
-  // same change at 1024 loses: 0.87 vs 0.89).
-  static constexpr int STAGES = (N == 4096 || N == 2048) ? 1 : 2;
+  static constexpr int STAGES = N == 4096 ? 1 : 2;
 #endif
   static constexpr int RAW = 8 * N;                                   // bytes per transform
   static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes
