@@ -334,7 +334,7 @@ template <int N, int LAYOUT, int DIR, bool STORE_TMA>
 __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
   using TG = TmaGeom<N>;
   using G = typename TG::G;
-  static_assert(TG::STAGES == 1 || TG::STAGES == 2, "single or double buffering");
+  static_assert(TG::STAGES >= 1 && TG::STAGES <= 4, "1-4 stages");
   constexpr int NST = TG::STAGES;
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
@@ -363,10 +363,10 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
 
   int it = 0;
   for (int64_t g = blockIdx.x; g < groups; g += stride, ++it) {
-    const int s = NST == 2 ? (it & 1) : 0;
+    const int s = it % NST;
     char *stage = smem + s * TG::STAGE_BYTES;
     char *slot = stage + f * TG::SLOT;
-    mbar_wait(&bars[s], (NST == 2 ? (it >> 1) : it) & 1);
+    mbar_wait(&bars[s], (it / NST) & 1);
 
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
@@ -378,14 +378,15 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
-    if (NST == 2 && STORE_TMA && tid == 0 && it >= 1) {
-      // the other stage held group it-1, bulk-stored at the end of the last
-      // iteration: refill it with group it+1 once that store has drained
+    if (NST >= 2 && STORE_TMA && tid == 0 && it >= 1) {
+      // the previous stage held group it-1, bulk-stored at the end of the last
+      // iteration: refill it with group it-1+NST once that store has drained
       // shared memory (pass 0 above overlapped the drain)
-      const int64_t gn = g + stride;
+      const int64_t gn = g + (NST - 1) * stride;
       if (gn < groups) {
+        const int sp = (it - 1) % NST;
         bulk_wait_read0();
-        tma_issue<N, LAYOUT>(args, smem + (s ^ 1) * TG::STAGE_BYTES, &bars[(s ^ 1) & (NST - 1)], gn);
+        tma_issue<N, LAYOUT>(args, smem + sp * TG::STAGE_BYTES, &bars[sp], gn);
       }
     }
     float2 *sx = reinterpret_cast<float2 *>(slot);
