@@ -11,12 +11,15 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "kernels.hpp"
 #include "plan.hpp"
@@ -34,6 +37,13 @@ fftgen_status fail(fftgen_status st, const std::string &msg) {
 fftgen_status cuda_fail(cudaError_t e, const char *what) {
   return fail(FFTGEN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// NVTX range around each public execute (header-only NVTX3: a no-op unless a
+// profiler such as nsys / ncu --nvtx is attached)
+struct NvtxRange {
+  explicit NvtxRange(const fftgen_plan *p, const char *what);
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
   int prev = -1;
@@ -107,6 +117,12 @@ struct fftgen_plan {
   bool use_tma = true;
   bool use_tma_store = true;
 };
+
+NvtxRange::NvtxRange(const fftgen_plan *p, const char *what) {
+  char msg[96];
+  std::snprintf(msg, sizeof msg, "%s n=%lld batch=%lld", what, (long long)p->cfg.n, (long long)p->cfg.batch);
+  nvtxRangePushA(msg);
+}
 
 namespace {
 
@@ -596,6 +612,7 @@ fftgen_status fftgen_execute(const fftgen_plan *p, int direction, const void *in
                              void *out0, void *out1, int64_t dist, void *stream) {
   fftgen_status st = validate_exec(p, direction, in0, in1, out0, out1, dist);
   if (st != FFTGEN_OK) return st;
+  NvtxRange range(p, "fftgen_execute");
   DeviceGuard g(p->cfg.device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaError_t e = enqueue(p, direction, in0, in1, out0, out1, dist, p->cfg.batch, (cudaStream_t)stream);
@@ -609,6 +626,7 @@ fftgen_status fftgen_execute_host(const fftgen_plan *cp, int direction, const fl
   if (st != FFTGEN_OK) return st;
   auto *p = const_cast<fftgen_plan *>(cp);
   std::lock_guard<std::mutex> lk(p->mu);
+  NvtxRange range(p, "fftgen_execute_host");
   DeviceGuard g(p->cfg.device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   const int64_t n = p->cfg.n;
