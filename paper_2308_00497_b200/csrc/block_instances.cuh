@@ -29,10 +29,13 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
   *tma_blocks_per_sm = 0;
   if constexpr (Tma1Geom<N>::ENABLED) {
     constexpr int tsmem = Tma1Geom<N>::BYTES;
-    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tsmem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR, true>,
                                                       Tma1Geom<N>::THREADS, tsmem);
   } else if constexpr (TmaGeom<N>::ENABLED) {
     constexpr int tsmem = TmaGeom<N>::BYTES;
@@ -57,8 +60,10 @@ template <int N, int LAYOUT, int DIR>
 cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, bool store_tma, cudaStream_t s) {
   if constexpr (Tma1Geom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
-    (void)store_tma;
-    fft_block_tma1_kernel<N, LAYOUT, DIR><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
+    if (store_tma)
+      fft_block_tma1_kernel<N, LAYOUT, DIR, true><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
+    else
+      fft_block_tma1_kernel<N, LAYOUT, DIR, false><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
     return cudaGetLastError();
   } else if constexpr (TmaGeom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;

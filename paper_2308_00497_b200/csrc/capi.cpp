@@ -455,7 +455,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         delete p;
         return cuda_fail(e, "kernel attributes");
       }
-      p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
+      p->tma_grid = block_tma_enabled(p->ex.log2n, p->cfg.layout == FFTGEN_LAYOUT_SPLIT) ? per_sm * sms : 0;
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
     }
@@ -764,9 +764,12 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
     if (p->use_tma && p->tma_grid > 0) {
       block_tma_geom(p->ex.log2n, &threads, &tpb, &smem);
       const int64_t groups = (p->cfg.batch + tpb - 1) / tpb;
-      o << "kernel fft_block_tma_kernel<" << p->cfg.n << "> grid[" << std::min<int64_t>(groups, p->tma_grid)
-        << "] block[" << threads << "] smem=" << smem << "B transforms/group=" << tpb
-        << " (persistent, cp.async.bulk double-buffered; direct kernel if unaligned)\n";
+      const bool single = p->ex.log2n == 14;
+      o << "kernel fft_block_tma" << (single ? "1" : "") << "_kernel<" << p->cfg.n << "> grid["
+        << std::min<int64_t>(groups, p->tma_grid) << "] block[" << threads << "] smem=" << smem
+        << "B transforms/group=" << tpb
+        << (single ? " (persistent, cp.async.bulk single stage + plane exchange; direct kernel if unaligned)\n"
+                   : " (persistent, cp.async.bulk double-buffered; direct kernel if unaligned)\n");
     } else {
       block_launch_geom(p->ex.log2n, &threads, &tpb, &smem);
       o << "kernel fft_block_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + tpb - 1) / tpb << "] block["

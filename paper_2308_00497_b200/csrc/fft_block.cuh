@@ -485,11 +485,35 @@ FFTGEN_FI void plane_exchange_pass(float *X, int t, const float2 *__restrict__ t
   pass_compute<G, p, DIR>(t, tw, v);
 }
 
-template <int N, int LAYOUT, int DIR>
+// Stage half of the last pass's outputs in the plane X for a bulk store:
+// split -> plane COMP (re or im, N floats); interleaved -> output half COMP
+// (k == 1 in the last pass, so element (B*cols + m) is in half B / (R/2):
+// the register index alone picks the half, N/2 float2 = one plane).
+template <class G, int N, int LAYOUT, int COMP>
+FFTGEN_FI void plane_write_out(float *X, int t, const float2 *v) {
+  constexpr int q = G::P - 1;
+  constexpr int R = G::R(q), cols = G::COLS(q), J = G::RMAX / R;
+  static_assert(G::K(q) == 1, "last pass writes natural order");
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int m = t + j * G::T;
+    if constexpr (LAYOUT == LAYOUT_SPLIT) {
+#pragma unroll
+      for (int B = 0; B < R; ++B) X[B * cols + m] = COMP ? v[j * R + B].y : v[j * R + B].x;
+    } else {
+      float2 *X2 = reinterpret_cast<float2 *>(X);
+#pragma unroll
+      for (int B = COMP * (R / 2); B < (COMP + 1) * (R / 2); ++B) X2[(B - COMP * (R / 2)) * cols + m] = v[j * R + B];
+    }
+  }
+}
+
+template <int N, int LAYOUT, int DIR, bool STORE_TMA>
 __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel(const BlockArgs args) {
   using TG = Tma1Geom<N>;
   using G = typename TG::G;
   static_assert(G::TPB == 1 && G::P == 3, "single-stage variant is for one 3-pass transform per CTA");
+  static_assert(TG::PLANE >= 4 * N, "the plane holds half an output transform");
   extern __shared__ float4 smem_f4[];
   char *stage = reinterpret_cast<char *>(smem_f4);
   float *X = reinterpret_cast<float *>(stage + TG::RAW);
@@ -504,6 +528,14 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel
     } else {
       bulk_g2s(stage, reinterpret_cast<const float2 *>(args.in0) + b * args.idist, plane, bar);
     }
+  };
+  // one half of the output (split: one plane) from X to HBM
+  auto store_half = [&](int64_t b, int h) {
+    if (LAYOUT == LAYOUT_SPLIT)
+      bulk_s2g(reinterpret_cast<float *>(h ? args.out1 : args.out0) + b * args.odist, X, 4 * N);
+    else
+      bulk_s2g(reinterpret_cast<float2 *>(args.out0) + b * args.odist + h * (N / 2), X, 4 * N);
+    bulk_commit();
   };
   if (t == 0) {
     mbar_init(bar, 1);
@@ -522,6 +554,8 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel
       const float2 *x = reinterpret_cast<const float2 *>(stage);
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
+    // the previous transform's last bulk store has read X before it is rewritten
+    if (STORE_TMA && t == 0) bulk_wait_read0();
     __syncthreads();  // stage consumed: fetch the next transform behind passes 1-2
     if (t == 0 && b + gridDim.x < args.batch) {
       fence_proxy_async();
@@ -530,9 +564,26 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel
     plane_exchange_pass<G, N, 1, DIR>(X, t, args.tw, v);
     __syncthreads();
     plane_exchange_pass<G, N, 2, DIR>(X, t, args.tw, v);
-    store_last<G, LAYOUT>(args, b * args.odist, t, v);
-    __syncthreads();  // X is rewritten by the next iteration
+    if constexpr (STORE_TMA) {
+      __syncthreads();  // pass-2 reads of X done
+      plane_write_out<G, N, LAYOUT, 0>(X, t, v);
+      fence_proxy_async();
+      __syncthreads();
+      if (t == 0) {
+        store_half(b, 0);
+        bulk_wait_read0();
+      }
+      __syncthreads();
+      plane_write_out<G, N, LAYOUT, 1>(X, t, v);
+      fence_proxy_async();
+      __syncthreads();
+      if (t == 0) store_half(b, 1);
+    } else {
+      store_last<G, LAYOUT>(args, b * args.odist, t, v);
+      __syncthreads();  // X is rewritten by the next iteration
+    }
   }
+  if (STORE_TMA && t == 0) bulk_wait0();
 }
 
 }  // namespace fftgen_b200

@@ -27,7 +27,7 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm);
 // persistent TMA-pipelined variant (fft_block_tma_kernel); grid = CTAs
 cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, bool store_tma,
                              cudaStream_t s);
-bool block_tma_enabled(int log2n);
+bool block_tma_enabled(int log2n, bool split);
 int block_tma_transforms_per_cta(int log2n);
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem);
 void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);

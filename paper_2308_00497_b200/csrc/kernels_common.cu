@@ -54,11 +54,11 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
   return cudaSuccess;
 }
 
-bool block_tma_enabled(int log2n) {
+bool block_tma_enabled(int log2n, bool split) {
   switch (log2n) {
-  case 14: {
+  case 14: {  // single-stage variant: default for split (0.58 vs 0.54), FFTGEN_TMA1=0/1 forces
     const char *env = std::getenv("FFTGEN_TMA1");
-    return Tma1Geom<16384>::ENABLED && env && env[0] == '1';
+    return Tma1Geom<16384>::ENABLED && (env ? env[0] == '1' : split);
   }
   case 6: return TmaGeom<64>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
   case 7: return TmaGeom<128>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
