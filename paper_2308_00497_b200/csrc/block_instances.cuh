@@ -29,14 +29,13 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
   *tma_blocks_per_sm = 0;
   if constexpr (Tma1Geom<N>::ENABLED) {
     constexpr int tsmem = Tma1Geom<N>::BYTES;
-    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fft_block_tma1_kernel<N, LAYOUT, DIR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tsmem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR, true>,
-                                                      Tma1Geom<N>::THREADS, tsmem);
+    for (auto fn : {fft_block_tma1_kernel<N, LAYOUT, DIR, false, false>, fft_block_tma1_kernel<N, LAYOUT, DIR, true, false>,
+                    fft_block_tma1_kernel<N, LAYOUT, DIR, false, true>, fft_block_tma1_kernel<N, LAYOUT, DIR, true, true>}) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR, true, true>, Tma1Geom<N>::THREADS, tsmem);
   } else if constexpr (TmaGeom<N>::ENABLED) {
     constexpr int tsmem = TmaGeom<N>::BYTES;
     e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR, false>,
@@ -57,13 +56,16 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
 }
 
 template <int N, int LAYOUT, int DIR>
-cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, bool store_tma, cudaStream_t s) {
+cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, int flags, cudaStream_t s) {
+  const bool store_tma = flags & BLOCK_TMA_STORE;
   if constexpr (Tma1Geom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
-    if (store_tma)
-      fft_block_tma1_kernel<N, LAYOUT, DIR, true><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
-    else
-      fft_block_tma1_kernel<N, LAYOUT, DIR, false><<<grid, Tma1Geom<N>::THREADS, Tma1Geom<N>::BYTES, s>>>(a);
+    constexpr int th = Tma1Geom<N>::THREADS, sm = Tma1Geom<N>::BYTES;
+    const bool ex1 = !(flags & BLOCK_TMA1_PLANE_EX1);
+    if (store_tma && ex1) fft_block_tma1_kernel<N, LAYOUT, DIR, true, true><<<grid, th, sm, s>>>(a);
+    else if (store_tma) fft_block_tma1_kernel<N, LAYOUT, DIR, true, false><<<grid, th, sm, s>>>(a);
+    else if (ex1) fft_block_tma1_kernel<N, LAYOUT, DIR, false, true><<<grid, th, sm, s>>>(a);
+    else fft_block_tma1_kernel<N, LAYOUT, DIR, false, false><<<grid, th, sm, s>>>(a);
     return cudaGetLastError();
   } else if constexpr (TmaGeom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
@@ -104,9 +106,9 @@ cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, bool store_tma, cud
   cudaError_t block_prepare_##SUFFIX(int log2n, int *tma_blocks_per_sm) {                     \
     FFTGEN_BLOCK_SWITCH(block_prepare_n, LAYOUT, DIR, tma_blocks_per_sm)                      \
   }                                                                                           \
-  cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, bool store_tma, \
+  cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, int flags, \
                                         cudaStream_t s) {                                     \
-    FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, store_tma, s)               \
+    FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, flags, s)               \
   }
 
 }  // namespace fftgen_b200

@@ -116,6 +116,7 @@ struct fftgen_plan {
   int tma_grid = 0;
   bool use_tma = true;
   bool use_tma_store = true;
+  bool tma1_plane_ex1 = false;  // FFTGEN_TMA1_EX1=0
 };
 
 NvtxRange::NvtxRange(const fftgen_plan *p, const char *what) {
@@ -221,7 +222,10 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
       const int64_t groups = (batch + tp - 1) / tp;
       const int grid = (int)std::min<int64_t>(groups, p->tma_grid);
-      return block_tma_launch(p->ex.log2n, layout, direction, a, grid, p->use_tma_store && out_aligned, s);
+      return block_tma_launch(p->ex.log2n, layout, direction, a, grid,
+                              (p->use_tma_store && out_aligned ? BLOCK_TMA_STORE : 0) |
+                                  (p->tma1_plane_ex1 ? BLOCK_TMA1_PLANE_EX1 : 0),
+                              s);
     }
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
@@ -455,9 +459,13 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
         delete p;
         return cuda_fail(e, "kernel attributes");
       }
-      p->tma_grid = block_tma_enabled(p->ex.log2n, p->cfg.layout == FFTGEN_LAYOUT_SPLIT) ? per_sm * sms : 0;
+      p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
+      // 2^14 split: the direct 4-byte stores beat the two-half bulk-store
+      // epilogue through the exchange plane (0.66 vs 0.63; interleaved 0.66 / 0.67)
+      p->use_tma_store = !(p->ex.log2n == 14 && p->cfg.layout == FFTGEN_LAYOUT_SPLIT);
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
+      if (const char *env = std::getenv("FFTGEN_TMA1_EX1")) p->tma1_plane_ex1 = env[0] == '0';
     }
     auto bail = [&](fftgen_status st, const std::string &msg) {
       fftgen_plan_destroy(p);

@@ -24,10 +24,13 @@ struct BlockArgs {
 // K2: one CTA per TPB whole transforms, N = 2^log2n <= 2^14.
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
 cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm);
-// persistent TMA-pipelined variant (fft_block_tma_kernel); grid = CTAs
-cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, bool store_tma,
+// persistent TMA-pipelined variant (fft_block_tma_kernel); grid = CTAs;
+// flags: BLOCK_TMA_STORE (bulk-store epilogue), BLOCK_TMA1_PLANE_EX1 (2^14:
+// both exchanges plane-wise instead of the first one through the stage)
+constexpr int BLOCK_TMA_STORE = 1, BLOCK_TMA1_PLANE_EX1 = 2;
+cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, int flags,
                              cudaStream_t s);
-bool block_tma_enabled(int log2n, bool split);
+bool block_tma_enabled(int log2n);
 int block_tma_transforms_per_cta(int log2n);
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem);
 void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);

@@ -20,10 +20,10 @@ cudaError_t block_prepare_i_f(int, int *);
 cudaError_t block_prepare_i_b(int, int *);
 cudaError_t block_prepare_s_f(int, int *);
 cudaError_t block_prepare_s_b(int, int *);
-cudaError_t block_tma_launch_i_f(int, const BlockArgs &, int, bool, cudaStream_t);
-cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, bool, cudaStream_t);
-cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, bool, cudaStream_t);
-cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, bool, cudaStream_t);
+cudaError_t block_tma_launch_i_f(int, const BlockArgs &, int, int, cudaStream_t);
+cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, int, cudaStream_t);
+cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, int, cudaStream_t);
+cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, int, cudaStream_t);
 
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
@@ -31,13 +31,13 @@ cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cud
   return dir < 0 ? block_launch_s_f(log2n, a, s) : block_launch_s_b(log2n, a, s);
 }
 
-cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, bool store_tma,
+cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, int flags,
                              cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
-    return dir < 0 ? block_tma_launch_i_f(log2n, a, grid, store_tma, s)
-                   : block_tma_launch_i_b(log2n, a, grid, store_tma, s);
-  return dir < 0 ? block_tma_launch_s_f(log2n, a, grid, store_tma, s)
-                 : block_tma_launch_s_b(log2n, a, grid, store_tma, s);
+    return dir < 0 ? block_tma_launch_i_f(log2n, a, grid, flags, s)
+                   : block_tma_launch_i_b(log2n, a, grid, flags, s);
+  return dir < 0 ? block_tma_launch_s_f(log2n, a, grid, flags, s)
+                 : block_tma_launch_s_b(log2n, a, grid, flags, s);
 }
 
 // Sets the smem attributes of all four (layout, direction) instances and
@@ -54,11 +54,11 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
   return cudaSuccess;
 }
 
-bool block_tma_enabled(int log2n, bool split) {
+bool block_tma_enabled(int log2n) {
   switch (log2n) {
-  case 14: {  // single-stage variant: default for split (0.58 vs 0.54), FFTGEN_TMA1=0/1 forces
+  case 14: {  // single-stage variant (0.63 / 0.67 vs 0.52 / 0.56 direct); FFTGEN_TMA1=0 disables
     const char *env = std::getenv("FFTGEN_TMA1");
-    return Tma1Geom<16384>::ENABLED && (env ? env[0] == '1' : split);
+    return Tma1Geom<16384>::ENABLED && !(env && env[0] == '0');
   }
   case 6: return TmaGeom<64>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
   case 7: return TmaGeom<128>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");

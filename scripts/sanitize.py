@@ -12,12 +12,13 @@ def main():
     import torch
     import paper_2308_00497_b200 as fg
 
-    cases = [(64, 5), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 2),  # K2 direct / TMA
+    cases = [(64, 5), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 150),  # K2 direct / TMA
              (1 << 15, 3), (1 << 16, 2), (1 << 18, 1), (1 << 21, 1)]          # K5, K3 (+TMA groups)
     # opt-in paths: (env, n, batch)
     optin = [({"FFTGEN_PHASED": "1", "FFTGEN_PHASE_SLOT_MB": "1"}, 1 << 16, 5),
              ({"FFTGEN_PHASED": "2", "FFTGEN_PHASE_SLOT_MB": "1"}, 1 << 16, 5),
-             ({"FFTGEN_CLUSTER14": "1"}, 1 << 14, 3), ({"FFTGEN_TMA1": "1"}, 1 << 14, 3),
+             ({"FFTGEN_CLUSTER14": "1"}, 1 << 14, 3), ({"FFTGEN_TMA1": "0"}, 1 << 14, 3),
+             ({"FFTGEN_TMA1_EX1": "0", "FFTGEN_DISABLE_TMA_STORE": "0"}, 1 << 14, 150),
              ({"FFTGEN_GROUP_TMA": "1"}, 1 << 16, 2), ({"FFTGEN_L2_CHUNK_BYTES": "1048576",
                                                         "FFTGEN_DISABLE_CLUSTER": "1"}, 1 << 15, 9)]
     runs = [({}, n, b) for n, b in cases] + (optin if os.environ.get("SANITIZE_OPTIN") else [])

@@ -293,6 +293,27 @@ def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
         check(a, orc.forward(x, "stockham", 4), n)
 
 
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_tma1_exchange_variants_bitwise_equal(orc, layout, monkeypatch):
+    """2^14 single-stage kernel: float2 first exchange through the stage
+    (FFTGEN_TMA1_EX1=1, default) and both exchanges plane-wise run the same
+    arithmetic; with and without the bulk-store epilogue."""
+    n = 16384
+    monkeypatch.setenv("FFTGEN_TMA1", "1")
+    x = seeded_batch(orc, n, 301)
+    outs = []
+    for ex1 in ("1", "0"):
+        monkeypatch.setenv("FFTGEN_TMA1_EX1", ex1)
+        for store in ("0", "1"):
+            monkeypatch.setenv("FFTGEN_DISABLE_TMA_STORE", store)
+            for d in (-1, 1):
+                outs.append(run(n, layout, d, x))
+    for i in range(2, len(outs)):
+        assert np.array_equal(outs[i], outs[i % 2]), i
+    check(outs[0], orc.forward(x, "stockham", 4), n)
+    check(outs[1], orc.forward(x, "stockham", 4, inverse=True), n)
+
+
 def test_unaligned_dist_uses_direct_path(orc):
     # dist*4 bytes not a multiple of 16 -> no cp.async.bulk; still correct
     n = 4096
