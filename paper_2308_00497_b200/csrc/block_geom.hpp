@@ -184,6 +184,8 @@ template <int N> struct TmaGeom {
   static constexpr int STAGES = FFTGEN_K2_STAGES;
 #elif defined(FFTGEN_K2_S2_N)
   static constexpr int STAGES = (N == 4096 && N != FFTGEN_K2_S2_N) ? 1 : 2;
+#elif defined(FFTGEN_K2_S1_N)
+  static constexpr int STAGES = (N == 4096 || N == FFTGEN_K2_S1_N) ? 1 : 2;
 #elif defined(FFTGEN_K2_S3_N)
   static constexpr int STAGES = N == FFTGEN_K2_S3_N ? 3 : (N == 4096 ? 1 : 2);
 #else
