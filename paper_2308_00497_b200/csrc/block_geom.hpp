@@ -199,17 +199,19 @@ template <int N> struct TmaGeom {
 };
 
 // -------------------------------------------------------------------------
-// Single-stage TMA variant for the largest smem-resident size (N = 2^14): the
-// raw input stage (8N bytes) is refilled by cp.async.bulk as soon as pass 0
-// has consumed it, while passes 1-2 exchange through ONE padded fp32 plane
-// (re, then im), so stage + plane fit one SM (192 KB).
-// Measured on B200 (N = 2^14, 1 GiB batches): split 15.24 vs 15.21 TFLOP/s
-// for the direct kernel, interleaved 15.79 vs 16.75 -- the plane-wise
-// exchange doubles the barriers and shared-memory instructions of a kernel
-// that is no longer latency-bound, so the direct kernel stays the default.
-// FFTGEN_TMA1=1 enables it.
+// Single-stage TMA variant for the largest smem-resident size (N = 2^14): one
+// raw input stage (8N bytes) plus one padded fp32 plane.  Pass 0 reads the
+// stage, exchange 1 runs as float2 through the stage (+ the head of the
+// plane), the next transform's cp.async.bulk is issued into the stage, and
+// exchange 2 goes through the plane (re, then im) behind it.  Measured on
+// B200 (1 GiB batches): 0.66 / 0.67 of HBM (split / interleaved) vs 0.52 /
+// 0.56 for the direct kernel.  FFTGEN_TMA1=0 disables it;
+// -DFFTGEN_TMA1_N=8192 also uses it at 2^13 (experiment).
+#ifndef FFTGEN_TMA1_N
+#define FFTGEN_TMA1_N 16384
+#endif
 template <int N> struct Tma1Geom {
-  static constexpr bool ENABLED = N == 16384;
+  static constexpr bool ENABLED = N == 16384 || N == FFTGEN_TMA1_N;
   using G = BlockGeom<N>;
   static constexpr int THREADS = G::THREADS;
   static constexpr int RAW = 8 * N;
@@ -217,6 +219,7 @@ template <int N> struct Tma1Geom {
   static constexpr int r1 = BoundaryPad<N, 1, 4>::region;
   static constexpr int PLANE = ((r0 > r1 ? r0 : r1) * 4 + 127) / 128 * 128;
   static constexpr int BYTES = RAW + PLANE + 128;
+  static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 0 ? (228 * 1024) / (BYTES + 1024) : 1;
 };
 
 // -------------------------------------------------------------------------

@@ -772,7 +772,7 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
     if (p->use_tma && p->tma_grid > 0) {
       block_tma_geom(p->ex.log2n, &threads, &tpb, &smem);
       const int64_t groups = (p->cfg.batch + tpb - 1) / tpb;
-      const bool single = p->ex.log2n == 14;
+      const bool single = block_tma1(p->ex.log2n);
       o << "kernel fft_block_tma" << (single ? "1" : "") << "_kernel<" << p->cfg.n << "> grid["
         << std::min<int64_t>(groups, p->tma_grid) << "] block[" << threads << "] smem=" << smem
         << "B transforms/group=" << tpb

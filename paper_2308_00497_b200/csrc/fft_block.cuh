@@ -512,7 +512,7 @@ FFTGEN_FI void plane_write_out(float *X, int t, const float2 *v) {
 // next transform's load issued after it, instead of both exchanges plane-wise
 // with the load issued after pass 0.
 template <int N, int LAYOUT, int DIR, bool STORE_TMA, bool EX1>
-__global__ void __launch_bounds__(Tma1Geom<N>::THREADS, 1) fft_block_tma1_kernel(const BlockArgs args) {
+__global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS) fft_block_tma1_kernel(const BlockArgs args) {
   using TG = Tma1Geom<N>;
   using G = typename TG::G;
   static_assert(G::TPB == 1 && G::P == 3, "single-stage variant is for one 3-pass transform per CTA");

@@ -31,6 +31,7 @@ constexpr int BLOCK_TMA_STORE = 1, BLOCK_TMA1_PLANE_EX1 = 2;
 cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, int flags,
                              cudaStream_t s);
 bool block_tma_enabled(int log2n);
+bool block_tma1(int log2n);  // the size runs the single-stage fft_block_tma1_kernel
 int block_tma_transforms_per_cta(int log2n);
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem);
 void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);

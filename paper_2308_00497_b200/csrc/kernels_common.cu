@@ -54,20 +54,47 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
   return cudaSuccess;
 }
 
+namespace {
+template <int N> bool tma_enabled_n() {
+  if constexpr (Tma1Geom<N>::ENABLED) {  // single-stage variant; FFTGEN_TMA1=0 disables
+    const char *env = std::getenv("FFTGEN_TMA1");
+    return !(env && env[0] == '0');
+  } else if constexpr (N == 64 || N == 128) {  // measured slower than direct; opt-in
+    return TmaGeom<N>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
+  } else {
+    return TmaGeom<N>::ENABLED;
+  }
+}
+template <int N> void tma_geom_n(int64_t *threads, int64_t *tp, int64_t *smem) {
+  if constexpr (Tma1Geom<N>::ENABLED) {
+    *threads = Tma1Geom<N>::THREADS, *tp = 1, *smem = Tma1Geom<N>::BYTES;
+  } else if constexpr (TmaGeom<N>::ENABLED) {
+    *threads = TmaGeom<N>::THREADS, *tp = TmaGeom<N>::TP, *smem = TmaGeom<N>::BYTES;
+  } else {
+    *threads = *tp = *smem = 0;
+  }
+}
+}  // namespace
+
 bool block_tma_enabled(int log2n) {
   switch (log2n) {
-  case 14: {  // single-stage variant (0.63 / 0.67 vs 0.52 / 0.56 direct); FFTGEN_TMA1=0 disables
-    const char *env = std::getenv("FFTGEN_TMA1");
-    return Tma1Geom<16384>::ENABLED && !(env && env[0] == '0');
+  case 6: return tma_enabled_n<64>();
+  case 7: return tma_enabled_n<128>();
+  case 8: return tma_enabled_n<256>();
+  case 9: return tma_enabled_n<512>();
+  case 10: return tma_enabled_n<1024>();
+  case 11: return tma_enabled_n<2048>();
+  case 12: return tma_enabled_n<4096>();
+  case 13: return tma_enabled_n<8192>();
+  case 14: return tma_enabled_n<16384>();
+  default: return false;
   }
-  case 6: return TmaGeom<64>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
-  case 7: return TmaGeom<128>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
-  case 8: return TmaGeom<256>::ENABLED;
-  case 9: return TmaGeom<512>::ENABLED;
-  case 10: return TmaGeom<1024>::ENABLED;
-  case 11: return TmaGeom<2048>::ENABLED;
-  case 12: return TmaGeom<4096>::ENABLED;
-  case 13: return TmaGeom<8192>::ENABLED;
+}
+
+bool block_tma1(int log2n) {
+  switch (log2n) {
+  case 13: return Tma1Geom<8192>::ENABLED;
+  case 14: return Tma1Geom<16384>::ENABLED;
   default: return false;
   }
 }
@@ -75,28 +102,23 @@ bool block_tma_enabled(int log2n) {
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem) {
   *threads = *tp = *smem = 0;
   switch (log2n) {
-#define FFTGEN_TG(L, NN) case L: *threads = TmaGeom<NN>::THREADS; *tp = TmaGeom<NN>::TP; *smem = TmaGeom<NN>::BYTES; return;
-  FFTGEN_TG(6, 64) FFTGEN_TG(7, 128) FFTGEN_TG(8, 256) FFTGEN_TG(9, 512) FFTGEN_TG(10, 1024) FFTGEN_TG(11, 2048)
-  FFTGEN_TG(12, 4096) FFTGEN_TG(13, 8192)
-  case 14: *threads = Tma1Geom<16384>::THREADS; *tp = 1; *smem = Tma1Geom<16384>::BYTES; return;
-#undef FFTGEN_TG
+  case 6: return tma_geom_n<64>(threads, tp, smem);
+  case 7: return tma_geom_n<128>(threads, tp, smem);
+  case 8: return tma_geom_n<256>(threads, tp, smem);
+  case 9: return tma_geom_n<512>(threads, tp, smem);
+  case 10: return tma_geom_n<1024>(threads, tp, smem);
+  case 11: return tma_geom_n<2048>(threads, tp, smem);
+  case 12: return tma_geom_n<4096>(threads, tp, smem);
+  case 13: return tma_geom_n<8192>(threads, tp, smem);
+  case 14: return tma_geom_n<16384>(threads, tp, smem);
   default: return;
   }
 }
 
 int block_tma_transforms_per_cta(int log2n) {
-  switch (log2n) {
-  case 14: return 1;
-  case 6: return TmaGeom<64>::TP;
-  case 7: return TmaGeom<128>::TP;
-  case 8: return TmaGeom<256>::TP;
-  case 9: return TmaGeom<512>::TP;
-  case 10: return TmaGeom<1024>::TP;
-  case 11: return TmaGeom<2048>::TP;
-  case 12: return TmaGeom<4096>::TP;
-  case 13: return TmaGeom<8192>::TP;
-  default: return 0;
-  }
+  int64_t th, tp, sm;
+  block_tma_geom(log2n, &th, &tp, &sm);
+  return (int)tp;
 }
 
 // ---- fp64 <-> fp32 for the interpret() drop-in ---------------------------
