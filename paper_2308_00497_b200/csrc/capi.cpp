@@ -84,6 +84,7 @@ struct fftgen_plan {
   float2 *d_tw = nullptr;
   // K3 four-step: device-generated group twiddles and intermediate buffers
   float2 *d_twg = nullptr;
+  float2 *d_tws = nullptr;  // K7: 2^14 block-plan tables, then w_N^e for e < N
   float2 *d_scratch = nullptr;
   float2 *d_fallback = nullptr;  // full-batch scratch of cluster / phased plans, on first unaligned execute
   size_t scratch_bytes = 0;
@@ -91,6 +92,9 @@ struct fftgen_plan {
   // K3 groups: persistent TMA variant (resident CTAs per group, 0 = off)
   std::vector<int> group_tma_grid;
   bool use_cluster = false;
+  bool use_split = false;  // K7 split-cluster kernel (fft_split.cuh)
+  int split_clusters = 0;
+  int64_t split_twn_off = 0;  // float2 offset of the w_N table in d_tws
   // K6: 2-group plans in one cooperative launch, intermediate in two L2 slots
   bool use_phased = false;
   int phased_grid = 0, phased_variant = 0;
@@ -235,6 +239,20 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const int64_t esz = split ? 4 : 8;
     const bool rows_aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                               (dist * esz) % 16 == 0;
+    if (p->use_split && rows_aligned) {
+      // radix-C DIF step across a C-CTA cluster + one 2^14-point transform per CTA
+      SplitArgs sa{};
+      sa.in0 = in0;
+      sa.in1 = in1;
+      sa.out0 = out0;
+      sa.out1 = out1;
+      sa.idist = dist;
+      sa.odist = dist;
+      sa.batch = batch;
+      sa.tw = p->d_tws;
+      sa.tw_n = p->d_tws + p->split_twn_off;
+      return split_launch(p->ex.log2n, layout, direction, sa, p->split_clusters, s);
+    }
     if (p->use_cluster && rows_aligned) {
       // persistent clusters, one transform per cluster at a time; group-0
       // tiles arrive as TMA tensor boxes, the intermediate moves through DSMEM
@@ -312,7 +330,7 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       return cudaSuccess;
     }
     float2 *scratch = p->d_scratch;
-    if (p->use_cluster || p->use_phased) {
+    if (p->use_cluster || p->use_phased || p->use_split) {
       // TMA tiles need 16-byte aligned rows: unaligned data takes the
       // two-launch path, whose full-batch scratch is allocated on first use
       auto *mp = const_cast<fftgen_plan *>(p);
@@ -374,7 +392,7 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
     char *slot_ptr = (char *)p->d_stage + (i % K) * slot;
     // two-launch four-step plans share one scratch buffer: keep their chunks
     // stream-ordered (the K5 cluster path has no scratch)
-    const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster) ? 0 : (i % K);
+    const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster && !p->use_split) ? 0 : (i % K);
     if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) return cuda_fail(e, "host pipeline");
   }
   for (auto &s : p->streams)
@@ -543,6 +561,28 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           return bail(FFTGEN_ERR_CUDA, std::string("cluster kernel attributes: ") + cudaGetErrorString(e));
         p->use_cluster = p->max_clusters > 0;
       }
+      // K7 split-cluster kernel (FFTGEN_SPLIT=1): 2^15 / 2^16 in one HBM pass
+      const char *sp = std::getenv("FFTGEN_SPLIT");
+      if (sp && sp[0] == '1' && split_supported(p->ex.log2n)) {
+        if ((e = split_prepare(p->ex.log2n, &p->split_clusters)) != cudaSuccess)
+          return bail(FFTGEN_ERR_CUDA, std::string("split kernel attributes: ") + cudaGetErrorString(e));
+        if (p->split_clusters > 0) {
+          std::vector<float> t = block_twiddles(14);
+          p->split_twn_off = (int64_t)t.size() / 2;
+          for (int64_t i = 0; i < cfg->n; ++i) {
+            double re, im;
+            unit_root(cfg->n, i, &re, &im);
+            t.push_back(static_cast<float>(re));
+            t.push_back(static_cast<float>(im));
+          }
+          if ((e = cudaMalloc(&p->d_tws, t.size() * sizeof(float))) != cudaSuccess)
+            return bail(FFTGEN_ERR_NOMEM, std::string("split twiddles: ") + cudaGetErrorString(e));
+          if ((e = cudaMemcpy(p->d_tws, t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
+            return bail(FFTGEN_ERR_CUDA, std::string("split twiddle upload: ") + cudaGetErrorString(e));
+          p->use_split = true;
+          p->use_cluster = false;
+        }
+      }
       // K6 phased kernel (opt-in, FFTGEN_PHASED=1).  Measured on B200 it keeps
       // DRAM bytes at exactly 16 N per transform (the intermediate never leaves
       // L2), but runs below the two-launch K3 path: 2^16 0.29 vs 0.43, 2^18
@@ -551,7 +591,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       // SM (3.5 us per 64 KB tile at 2^16), not by HBM, so halving the HBM
       // bytes of a tile does not shorten it.
       const char *ph = std::getenv("FFTGEN_PHASED");
-      if (gs.size() == 2 && !p->use_cluster && phased_supported(gs[0].log2ns, gs[1].log2ns) && ph &&
+      if (gs.size() == 2 && !p->use_cluster && !p->use_split && phased_supported(gs[0].log2ns, gs[1].log2ns) && ph &&
           (ph[0] == '1' || ph[0] == '2')) {
         int bps = 0, sms = 0;
         p->phased_variant = ph[0] - '0';
@@ -572,7 +612,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
             return bail(FFTGEN_ERR_NOMEM, "chunk counters");
         }
       }
-      p->scratch_bytes = p->use_cluster ? 0
+      p->scratch_bytes = (p->use_cluster || p->use_split) ? 0
                          : p->use_phased ? (size_t)p->phased_slots * (size_t)p->phased_chunk * (size_t)cfg->n * sizeof(float2)
                                          : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
                                            sizeof(float2);
@@ -600,6 +640,7 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     DeviceGuard g(p->cfg.device);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
+    if (p->d_tws) cudaFree(p->d_tws);
     if (p->d_scratch) cudaFree(p->d_scratch);
     if (p->d_done) cudaFree(p->d_done);
     if (p->d_fallback) cudaFree(p->d_fallback);
@@ -752,7 +793,7 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return (p->use_cluster || p->use_phased) ? 1 : (int)p->ex.groups.size();
+  default: return (p->use_cluster || p->use_phased || p->use_split) ? 1 : (int)p->ex.groups.size();
   }
 }
 
@@ -789,7 +830,15 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_FOURSTEP) {
-    if (p->use_cluster) {
+    if (p->use_split) {
+      int64_t threads, smem, csize;
+      split_geom(p->ex.log2n, &threads, &smem, &csize);
+      o << "split: 1 fft_split_kernel<" << csize << "> launch grid["
+        << std::min<int64_t>(p->cfg.batch, p->split_clusters) * csize << "] cluster[" << csize << "] block["
+        << threads << "] smem=" << smem << "B co-resident clusters=" << p->split_clusters
+        << " (persistent; radix-" << csize << " DIF step through DSMEM, one 2^14-point transform per CTA, "
+        << "stride-" << csize << " stores, no scratch; two-launch path if unaligned)\n";
+    } else if (p->use_cluster) {
       int64_t threads, smem;
       const int64_t csize = p->cluster_size;
       cluster_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, p->cluster_size, &threads, &smem);

@@ -110,6 +110,21 @@ struct ClusterArgs {
   const float2 *tw_q;       // group 1: [A0][m] = w_N^{A0 (NS1/R0) m}
   const float2 *tw_p;       // group 1: [c][m]  = w_N^{c m}
 };
+// K7: N = C * 2^14 as a radix-C DIF step across a C-CTA cluster plus one
+// 2^14-point transform per CTA (fft_split.cuh); one HBM pass.
+struct SplitArgs {
+  const void *in0, *in1;
+  void *out0, *out1;
+  int64_t idist, odist;
+  int64_t batch;
+  const float2 *tw;    // 2^14-point block-plan pass tables (block_twiddles(14))
+  const float2 *tw_n;  // w_N^e, e in [0, N)
+};
+bool split_supported(int log2n);
+// *max_clusters: co-resident clusters (the persistent grid)
+cudaError_t split_prepare(int log2n, int *max_clusters);
+cudaError_t split_launch(int log2n, int layout, int dir, const SplitArgs &a, int max_clusters, cudaStream_t s);
+void split_geom(int log2n, int64_t *threads, int64_t *smem, int64_t *csize);
 // default cluster size C of the (NS0, NS1) split for a layout, 0 = none
 int cluster_default_size(int log2ns0, int log2ns1, int layout);
 // *max_clusters: co-resident clusters (the persistent grid)

@@ -284,6 +284,7 @@ cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, 
 #include <cudaTypedefs.h>
 
 #include "cluster_instances.cuh"
+#include "fft_split.cuh"
 
 namespace fftgen_b200 {
 
@@ -359,6 +360,33 @@ cudaError_t cluster_encode_maps(int l0, int l1, int csize, int layout, ClusterAr
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
   return cudaSuccess;
+}
+
+cudaError_t split_launch_f(int, int, const SplitArgs &, int, cudaStream_t);
+cudaError_t split_launch_b(int, int, const SplitArgs &, int, cudaStream_t);
+cudaError_t split_prepare_f(int, int *);
+cudaError_t split_prepare_b(int, int *);
+
+bool split_supported(int log2n) { return log2n == 15 || log2n == 16; }
+
+cudaError_t split_prepare(int log2n, int *max_clusters) {
+  int a = 0, b = 0;
+  cudaError_t e = split_prepare_f(log2n, &a);
+  if (e == cudaSuccess) e = split_prepare_b(log2n, &b);
+  *max_clusters = a < b ? a : b;
+  return e;
+}
+
+cudaError_t split_launch(int log2n, int layout, int dir, const SplitArgs &a, int max_clusters, cudaStream_t s) {
+  return dir < 0 ? split_launch_f(log2n, layout, a, max_clusters, s) : split_launch_b(log2n, layout, a, max_clusters, s);
+}
+
+void split_geom(int log2n, int64_t *threads, int64_t *smem, int64_t *csize) {
+  *threads = *smem = *csize = 0;
+  if (!split_supported(log2n)) return;
+  *threads = SplitGeom<2>::THREADS;
+  *smem = SplitGeom<2>::BYTES;
+  *csize = int64_t(1) << (log2n - 14);
 }
 
 cudaError_t cluster_prepare(int l0, int l1, int c, int *max_clusters) {

@@ -369,3 +369,69 @@ def test_huge_roundtrip_inverse(fg, l2):
     err = (torch.linalg.norm((y / n - x).double()) / torch.linalg.norm(x.double())).item()
     assert err < 1e-6, err
     plan.close()
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+@pytest.mark.parametrize("direction", [-1, 1])
+@pytest.mark.parametrize("l2", [15, 16])
+def test_split_cluster_kernel_matches_oracle(fg, orc, l2, layout, direction, monkeypatch):
+    """K7 (fft_split.cuh): radix-C DIF step across a C-CTA cluster, one
+    2^14-point transform per CTA.  A batch above the co-resident cluster count
+    exercises the persistent loop (raw slice refills, z mbarrier phases)."""
+    monkeypatch.setenv("FFTGEN_SPLIT", "1")
+    n = 1 << l2
+    batch = 5
+    x = seeded_batch(orc, n, batch, seed0=11)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+    assert "fft_split_kernel" in plan.describe() and plan.launches() == 1
+    plan.close()
+    got = run(fg, n, layout, direction, x)
+    want = orc.forward(x, "stockham", 4, inverse=direction > 0, threads=4)
+    for b in range(batch):
+        err = oracle.rel_l2(got[b], want[b])
+        assert err <= tol(n) and err < 3e-6, (n, b, err)
+
+
+@pytest.mark.parametrize("l2", [15, 16])
+def test_split_cluster_kernel_long_batch(fg, orc, l2, monkeypatch):
+    """Many transforms per cluster: forward then inverse round trip on a batch
+    several times the co-resident cluster count, plus oracle spot checks."""
+    monkeypatch.setenv("FFTGEN_SPLIT", "1")
+    n = 1 << l2
+    batch = 300
+    g = torch.Generator(device="cuda").manual_seed(l2)
+    x = (torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1).contiguous()
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="interleaved", batch=batch))
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    plan.execute(x, y, direction=-1)
+    plan.execute(y, z, direction=1)
+    torch.cuda.synchronize()
+    err = ((z / n - x).norm() / x.norm()).item()
+    assert err < 1e-6, err
+    for b in (0, 137, batch - 1):
+        xi = x[b].reshape(-1).double().cpu().numpy()
+        want = orc.forward(xi[None], "stockham", 4, threads=4)[0]
+        assert oracle.rel_l2(y[b].reshape(-1).double().cpu().numpy(), want) <= tol(n), b
+    plan.close()
+
+
+def test_split_cluster_unaligned_falls_back(fg, orc, monkeypatch):
+    monkeypatch.setenv("FFTGEN_SPLIT", "1")
+    n = 1 << 15
+    x = seeded_batch(orc, n, 2, seed0=3)
+    dist = n + 1
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="split", batch=2))
+    xs = np.zeros((2, dist, 2))
+    xs[:, :n, 0], xs[:, :n, 1] = x[:, 0::2], x[:, 1::2]
+    re = torch.from_numpy(xs[..., 0].astype(np.float32)).cuda()
+    im = torch.from_numpy(xs[..., 1].astype(np.float32)).cuda()
+    ore, oim = torch.zeros_like(re), torch.zeros_like(im)
+    plan.execute(re, ore, im, oim, direction=-1, dist=dist)
+    torch.cuda.synchronize()
+    got = np.empty((2, 2 * n))
+    got[:, 0::2], got[:, 1::2] = ore[:, :n].double().cpu().numpy(), oim[:, :n].double().cpu().numpy()
+    want = orc.forward(x, "stockham", 4)
+    for b in range(2):
+        assert oracle.rel_l2(got[b], want[b]) <= tol(n)
+    plan.close()
