@@ -49,6 +49,9 @@ template <> struct GroupPlan<1024> : PlanT<3, 8, 8, 16> {};
 #endif
 
 // TP = transforms per CTA.  0 -> the direct kernel's default (128 threads).
+#ifndef FFTGEN_TW_FACTOR_COLS
+#define FFTGEN_TW_FACTOR_COLS 1024
+#endif
 template <int N, int TP_ = 0, class PL_ = BlockPlan<N>> struct BlockGeom {
   using PL = PL_;
   static constexpr int P = PL::P;
@@ -72,6 +75,17 @@ template <int N, int TP_ = 0, class PL_ = BlockPlan<N>> struct BlockGeom {
     return o;
   }
   static constexpr int TW_LEN = P > 1 ? TW_OFF(P) : 0;
+  // A pass whose [A][m] table has >= 1024 columns (the last pass of N = 2^14:
+  // 128 KB, beyond what L1 keeps next to a 199 KB shared-memory carve-out)
+  // reads w_s^{A m} = w_s^{A 32 (m >> 5)} * w_s^{A (m & 31)} from two
+  // 32-column tables appended after the pass tables (TW_LEN): 8 KB in L1.
+  FFTGEN_HD static constexpr bool TW_FACTORED(int p) { return p >= 1 && COLS(p) >= FFTGEN_TW_FACTOR_COLS; }
+  FFTGEN_HD static constexpr int TW_FOFF(int p) {  // factor tables of pass p
+    int o = TW_LEN;
+    for (int q = 1; q < p; ++q)
+      if (TW_FACTORED(q)) o += 2 * 32 * PL::r(q);
+    return o;
+  }
 };
 
 // -------------------------------------------------------------------------
@@ -204,8 +218,9 @@ template <int N> struct TmaGeom {
 // stage, exchange 1 runs as float2 through the stage (+ the head of the
 // plane), the next transform's cp.async.bulk is issued into the stage, and
 // exchange 2 goes through the plane (re, then im) behind it.  Measured on
-// B200 (1 GiB batches): 0.66 / 0.67 of HBM (split / interleaved) vs 0.52 /
-// 0.56 for the direct kernel.  FFTGEN_TMA1=0 disables it;
+// B200 (1 GiB batches, bulk-store epilogue, factored last-pass twiddles):
+// 0.67 / 0.70 of HBM (split / interleaved) vs 0.50 / 0.54 for the direct
+// kernel.  FFTGEN_TMA1=0 disables it;
 // -DFFTGEN_TMA1_N=8192 also uses it at 2^13 (experiment).
 #ifndef FFTGEN_TMA1_N
 #define FFTGEN_TMA1_N 16384

@@ -479,9 +479,6 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       }
       p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
-      // 2^14 split: the direct 4-byte stores beat the two-half bulk-store
-      // epilogue through the exchange plane (0.66 vs 0.63; interleaved 0.66 / 0.67)
-      p->use_tma_store = !(p->ex.log2n == 14 && p->cfg.layout == FFTGEN_LAYOUT_SPLIT);
       if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
       if (const char *env = std::getenv("FFTGEN_TMA1_EX1")) p->tma1_plane_ex1 = env[0] == '0';
     }

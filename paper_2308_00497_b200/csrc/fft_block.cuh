@@ -74,6 +74,17 @@ FFTGEN_FI void pass0(int t, float2 *v, Load &&load) {
   }
 }
 
+// twiddle w_s^{A m} of pass p (forward sign; mul_tw conjugates for inverse)
+template <class G, int p> FFTGEN_FI float2 pass_tw(const float2 *__restrict__ tw, int A, int m) {
+  if constexpr (G::TW_FACTORED(p)) {
+    const float2 *f = tw + G::TW_FOFF(p);
+    const float2 hi = __ldg(f + A * 32 + (m >> 5)), lo = __ldg(f + (G::R(p) + A) * 32 + (m & 31));
+    return cmul(hi, lo.x, lo.y);
+  } else {
+    return __ldg(tw + G::TW_OFF(p) + A * G::COLS(p) + m);
+  }
+}
+
 template <class G, int N, int p>
 FFTGEN_FI void smem_write(float2 *sx, int t, const float2 *v) {
   constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R;
@@ -88,16 +99,14 @@ FFTGEN_FI void smem_write(float2 *sx, int t, const float2 *v) {
 
 template <class G, int N, int p, int DIR>
 FFTGEN_FI void smem_read_pass(const float2 *sx, int t, const float2 *__restrict__ tw, float2 *v) {
-  constexpr int R = G::R(p), k = G::K(p), cols = G::COLS(p), J = G::RMAX / R;
+  constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R;
   constexpr Pad pd = BoundaryPad<N, p - 1, 8, typename G::PL>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
-    const float2 *twp = tw + G::TW_OFF(p) + m;
     v[j * R] = sx[padded((m * R) * k + c, pd)];
 #pragma unroll
-    for (int A = 1; A < R; ++A)
-      v[j * R + A] = mul_tw<DIR>(sx[padded((m * R + A) * k + c, pd)], __ldg(twp + A * cols));
+    for (int A = 1; A < R; ++A) v[j * R + A] = mul_tw<DIR>(sx[padded((m * R + A) * k + c, pd)], pass_tw<G, p>(tw, A, m));
     reg_fft<R, DIR>(v + j * R);
   }
 }
@@ -462,13 +471,12 @@ FFTGEN_FI void plane_read(const float *X, int t, float2 *v) {
 
 template <class G, int p, int DIR>
 FFTGEN_FI void pass_compute(int t, const float2 *__restrict__ tw, float2 *v) {
-  constexpr int R = G::R(p), k = G::K(p), cols = G::COLS(p), J = G::RMAX / R;
+  constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k;
-    const float2 *twp = tw + G::TW_OFF(p) + m;
 #pragma unroll
-    for (int A = 1; A < R; ++A) v[j * R + A] = mul_tw<DIR>(v[j * R + A], __ldg(twp + A * cols));
+    for (int A = 1; A < R; ++A) v[j * R + A] = mul_tw<DIR>(v[j * R + A], pass_tw<G, p>(tw, A, m));
     reg_fft<R, DIR>(v + j * R);
   }
 }

@@ -56,18 +56,29 @@ void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem)
 // [A][m] tables of w_s^{A m} for passes 1..P-1, fp64 -> fp32 (forward sign).
 std::vector<float> block_twiddles(int log2n) {
   std::vector<float> out;
+  auto push = [&](int64_t s, int64_t e) {
+    double re, im;
+    unit_root(s, e, &re, &im);
+    out.push_back(static_cast<float>(re));
+    out.push_back(static_cast<float>(im));
+  };
   const int np = block_num_passes(log2n);
   for (int p = 1; p < np; ++p) {
     int64_t R, cols, k;
     block_pass(log2n, p, &R, &cols, &k);
-    const int64_t s = R * cols;
     for (int64_t A = 0; A < R; ++A)
-      for (int64_t m = 0; m < cols; ++m) {
-        double re, im;
-        unit_root(s, A * m, &re, &im);
-        out.push_back(static_cast<float>(re));
-        out.push_back(static_cast<float>(im));
-      }
+      for (int64_t m = 0; m < cols; ++m) push(R * cols, A * m);
+  }
+  // factor tables of the passes with >= 1024 columns (BlockGeom::TW_FACTORED):
+  // [A][h] = w_s^{A 32 h}, then [A][l] = w_s^{A l}, h, l < 32
+  for (int p = 1; p < np; ++p) {
+    int64_t R, cols, k;
+    block_pass(log2n, p, &R, &cols, &k);
+    if (cols < FFTGEN_TW_FACTOR_COLS) continue;
+    for (int64_t A = 0; A < R; ++A)
+      for (int64_t h = 0; h < 32; ++h) push(R * cols, A * 32 * h);
+    for (int64_t A = 0; A < R; ++A)
+      for (int64_t l = 0; l < 32; ++l) push(R * cols, A * l);
   }
   return out;
 }
