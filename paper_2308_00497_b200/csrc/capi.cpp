@@ -518,8 +518,11 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           return bail(FFTGEN_ERR_NOMEM, std::string("group twiddles: ") + cudaGetErrorString(e));
         for (const GroupDesc &d : p->ex.groups) {
           if (d.cols <= 1) continue;
+          // P is [c][m] for column groups (lanes share m) and [m][c] for the
+          // rows group (lanes walk c within a row: coalesced twiddle loads)
           if ((e = gen_twiddles(p->d_twg + d.q_off, d.r0, d.cols, d.ns / d.r0, d.s, 0)) != cudaSuccess ||
-              (e = gen_twiddles(p->d_twg + d.p_off, d.ns / d.r0, d.cols, 1, d.s, 0)) != cudaSuccess)
+              (e = d.rows ? gen_twiddles(p->d_twg + d.p_off, d.cols, d.ns / d.r0, 1, d.s, 0)
+                          : gen_twiddles(p->d_twg + d.p_off, d.ns / d.r0, d.cols, 1, d.s, 0)) != cudaSuccess)
             return bail(FFTGEN_ERR_CUDA, std::string("twiddle generation: ") + cudaGetErrorString(e));
         }
       }

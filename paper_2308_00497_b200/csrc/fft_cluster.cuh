@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
         const int c = t1 + j * CG::T1;
 #pragma unroll
         for (int A0 = 0; A0 < R10; ++A0) v[j * R10 + A0] = rowp[A0 * K10 + c];
-        const float2 pw = __ldg(a.tw_p + c * NS0 + m);
+        const float2 pw = __ldg(a.tw_p + m * K10 + c);  // [m][c]: the rows group's P table
 #pragma unroll
         for (int A0 = 0; A0 < R10; ++A0) {
           const float2 x = mul_tw<DIR>(v[j * R10 + A0], pw);

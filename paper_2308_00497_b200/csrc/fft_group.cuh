@@ -146,7 +146,7 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
         v[j * R0 + A0] = SIO<LIN>::load(a.in0, a.in1, off);
       }
       if (tw) {
-        const float2 pw = __ldg(a.tw_p + c * a.cols + m);
+        const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
 #pragma unroll
         for (int A0 = 0; A0 < R0; ++A0) {
           float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);

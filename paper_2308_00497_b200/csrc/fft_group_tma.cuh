@@ -105,7 +105,7 @@ FFTGEN_FI void tile_from_stage(const GroupArgs &a, char *stage, int64_t ob, int6
         }
       }
       if (tw) {
-        const float2 pw = __ldg(a.tw_p + c * a.cols + m);
+        const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
 #pragma unroll
         for (int A0 = 0; A0 < R0; ++A0) {
           float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
@@ -196,7 +196,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
           }
         }
         if (tw) {
-          const float2 pw = __ldg(a.tw_p + c * a.cols + m);
+          const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
 #pragma unroll
           for (int A0 = 0; A0 < R0; ++A0) {
             float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);

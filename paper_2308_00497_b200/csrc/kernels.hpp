@@ -48,7 +48,7 @@ struct GroupArgs {
   int64_t tiles_per_outer; // CTAs per transform
   const float2 *tw_local;  // NS-point block-plan pass tables
   const float2 *tw_q;      // [A0][m] = w_s^{A0 (NS/R0) m}   (cols > 1)
-  const float2 *tw_p;      // [c][m]  = w_s^{c m}
+  const float2 *tw_p;      // [c][m] = w_s^{c m}; [m][c] for the rows group (k == 1)
 };
 
 // K6: both groups of a 2-group plan in one persistent cooperative launch;
@@ -108,7 +108,7 @@ struct ClusterArgs {
   const float2 *tw_local0;  // NS0-point block-plan pass table
   const float2 *tw_local1;  // NS1-point block-plan pass table
   const float2 *tw_q;       // group 1: [A0][m] = w_N^{A0 (NS1/R0) m}
-  const float2 *tw_p;       // group 1: [c][m]  = w_N^{c m}
+  const float2 *tw_p;       // group 1 (rows): [m][c] = w_N^{c m}
 };
 // K7: N = C * 2^14 as a radix-C DIF step across a C-CTA cluster plus one
 // 2^14-point transform per CTA (fft_split.cuh); one HBM pass.
