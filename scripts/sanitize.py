@@ -19,6 +19,7 @@ def main():
              ({"FFTGEN_PHASED": "2", "FFTGEN_PHASE_SLOT_MB": "1"}, 1 << 16, 5),
              ({"FFTGEN_CLUSTER14": "1"}, 1 << 14, 3), ({"FFTGEN_TMA1": "0"}, 1 << 14, 3),
              ({"FFTGEN_TMA1_EX1": "0", "FFTGEN_DISABLE_TMA_STORE": "0"}, 1 << 14, 150),
+             ({"FFTGEN_SPLIT": "1"}, 1 << 15, 5), ({"FFTGEN_SPLIT": "1"}, 1 << 16, 3),
              ({"FFTGEN_GROUP_TMA": "1"}, 1 << 16, 2), ({"FFTGEN_L2_CHUNK_BYTES": "1048576",
                                                         "FFTGEN_DISABLE_CLUSTER": "1"}, 1 << 15, 9)]
     runs = [({}, n, b) for n, b in cases] + (optin if os.environ.get("SANITIZE_OPTIN") else [])
