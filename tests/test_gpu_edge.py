@@ -45,7 +45,7 @@ def test_in_place_execution(fg, orc, n):
     check_rows(orc, ref, torch.stack([re, im], -1), n, inverse=True)
 
 
-@pytest.mark.parametrize("n", [4096, 1 << 15, 1 << 16, 1 << 18])
+@pytest.mark.parametrize("n", [4096, 16384, 1 << 15, 1 << 16, 1 << 18])
 def test_cuda_graph_capture_and_replay(fg, orc, n):
     batch = 64
     x = rand((batch, n, 2), 2)
@@ -63,6 +63,34 @@ def test_cuda_graph_capture_and_replay(fg, orc, n):
     g.replay()
     torch.cuda.synchronize()
     check_rows(orc, x, y, n, rows=(0, 17, batch - 1))
+
+
+@pytest.mark.parametrize("n", [1 << 15, 1 << 16])
+def test_split_cluster_in_place_and_graph(fg, orc, n, monkeypatch):
+    """Opt-in K7: in-place is safe because every CTA of a cluster has read its
+    raw slices (cluster barrier) before any output of that transform is
+    written; the persistent launch also replays from a CUDA graph."""
+    monkeypatch.setenv("FFTGEN_SPLIT", "1")
+    batch = 200
+    x = rand((batch, n, 2), 6)
+    ref = x.clone()
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    assert "fft_split_kernel" in plan.describe()
+    plan.execute(x, x)
+    torch.cuda.synchronize()
+    check_rows(orc, ref, x, n, rows=(0, 99, batch - 1))
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.execute(ref, y, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.execute(ref, y, stream=s)
+    y.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    check_rows(orc, ref, y, n, rows=(1, batch - 2))
 
 
 @pytest.mark.parametrize("n", [1 << 15, 1 << 17])
