@@ -367,12 +367,20 @@ template <class F>
 fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &&stage) {
   const int64_t batch = p->cfg.batch;
   constexpr int K = fftgen_plan::kHostSlots;
-  // ~64 MiB per chunk and slot.  Measured on B200 at N=4096 split (4 GiB of
-  // PCIe traffic per execute): 2 slots x 64 MiB 47.8 ms, 4 slots x 32 MiB
-  // 50.2 ms, against a 94.6 GB/s concurrent H2D+D2H ceiling (45.4 ms).
-  const int64_t target = int64_t(64) << 20;
+  // 128 MiB per chunk and slot (in + out), the first and last four chunks
+  // ramping 1/16 .. 1/2 of that so the pipeline fills and drains quickly.
+  // Measured on B200 at N=4096 split (4 GiB of PCIe traffic per execute,
+  // scripts/gpu_e2e_ab.sh): 128 MiB + ramp 4: 347-349 GFLOP/s; 64 MiB: 342-344;
+  // 256 MiB: 345; 512 MiB + ramp 6: 330; 4 slots x 32 MiB: 50.2 vs 47.8 ms.
+  // FFTGEN_HOST_CHUNK_MB / FFTGEN_HOST_RAMP override.
+  int64_t target = int64_t(128) << 20;
+  if (const char *env = std::getenv("FFTGEN_HOST_CHUNK_MB")) target = std::max<int64_t>(1, std::atoll(env)) << 20;
   int64_t chunk = std::max<int64_t>(1, target / (int64_t)slot_bytes_per_transform);
   chunk = std::min(chunk, batch);
+  // ramp: the first chunks are 1/2^RAMP, 1/2^(RAMP-1), ... of a full chunk, so
+  // the pipeline fills (H2D of chunk 0 alone) and drains sooner
+  int ramp = 4;
+  if (const char *env = std::getenv("FFTGEN_HOST_RAMP")) ramp = std::max(0, std::min(6, std::atoi(env)));
   const size_t slot = (size_t)chunk * slot_bytes_per_transform;
   cudaError_t e;
   if (p->stage_bytes < K * slot) {
@@ -387,8 +395,13 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
     if (!s && (e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess)
       return cuda_fail(e, "cudaStreamCreate");
   int i = 0;
-  for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++i) {
-    const int64_t cnt = std::min(chunk, batch - b0);
+  for (int64_t b0 = 0, cnt = 0; b0 < batch; b0 += cnt, ++i) {
+    const int64_t want = i < ramp ? std::max<int64_t>(1, chunk >> (ramp - i)) : chunk;
+    const int64_t left = batch - b0;
+    // ramp down symmetrically: the last chunks shrink like the first ones grew
+    int64_t tail = want;
+    for (int r = 1; r <= ramp && left <= (chunk >> r) * 2 && (chunk >> r) > 0; ++r) tail = chunk >> r;
+    cnt = std::min(std::min(want, tail), left);
     char *slot_ptr = (char *)p->d_stage + (i % K) * slot;
     // two-launch four-step plans share one scratch buffer: keep their chunks
     // stream-ordered (the K5 cluster path has no scratch)

@@ -129,7 +129,7 @@ def test_unaligned_pointers_fall_back_to_direct_kernel(fg, orc):
 
 def test_smaller_batch_than_planned_via_host_path(fg, orc):
     """execute_host chunks a plan's batch; the last chunk is ragged."""
-    n, batch = 1 << 16, 257  # 64 MiB staging -> chunk 64 transforms, last chunk of 1
+    n, batch = 1 << 16, 257  # 128 MiB chunks of 128 transforms, ramped head and tail
     x = np.random.default_rng(0).uniform(-1, 1, (batch, n * 2)).astype(np.float32)
     y = np.empty_like(x)
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
