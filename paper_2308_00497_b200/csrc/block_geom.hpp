@@ -107,8 +107,10 @@ template <int N, int ELEM = 8, class PL = BlockPlan<N>> struct PadSearch {
   static constexpr int WAVE = 128 / ELEM;  // lanes served per shared-memory wavefront
   // Representative registers x and butterflies j suffice: the access
   // patterns are affine in both.
-  static constexpr int cost(int p, Pad pd) {
+  // stride: float2 between the transforms of a CTA (<= 0: padded(N - 1) + 1)
+  static constexpr int cost(int p, Pad pd, int stride = 0) {
     const int T = G::T;
+    const int S = stride > 0 ? stride : padded(N - 1, pd) + 1;
     int worst = 0;
     for (int side = 0; side < 2; ++side) {
       const int q = p + side;
@@ -126,7 +128,7 @@ template <int N, int ELEM = 8, class PL = BlockPlan<N>> struct PadSearch {
               const int t = l % T, f = l / T;  // T < 32: other transforms
               const int u = t + j * T, m = u / k, c = u % k;
               const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
-              const int b = (padded(idx, pd) + f * (padded(N - 1, pd) + 1)) % WAVE;
+              const int b = (padded(idx, pd) + f * S) % WAVE;
               cnt[b]++;
               deg = cnt[b] > deg ? cnt[b] : deg;
             }
@@ -161,11 +163,34 @@ template <int N, int p, int ELEM = 8, class PL = BlockPlan<N>> struct BoundaryPa
   static constexpr int wavefronts = BlockGeom<N, 0, PL>::P > 1 ? PadSearch<N, ELEM, PL>::cost(p, value) : 0;
 };
 
+// When a half-warp spans several transforms (T < 16 threads per transform),
+// the transform stride itself decides which bank pairs they share: search
+// the smallest extra stride F in [0, 16) that minimises the worst simulated
+// access of every pass boundary (N = 64: 8-way -> conflict-free).
+template <int N, class PL> struct StrideSearch {
+  using G = BlockGeom<N, 0, PL>;
+  template <int p> static constexpr int boundary_cost(int stride) {
+    if constexpr (p + 1 < G::P) return PadSearch<N, 8, PL>::cost(p, BoundaryPad<N, p, 8, PL>::value, stride);
+    else return 0;
+  }
+  static constexpr int worst(int stride) {
+    const int c0 = boundary_cost<0>(stride), c1 = boundary_cost<1>(stride);
+    return c0 > c1 ? c0 : c1;
+  }
+  static constexpr int best(int base) {
+    int bf = 0, bw = worst(base);
+    for (int F = 1; F < 16; ++F)
+      if (worst(base + F) < bw) bw = worst(base + F), bf = F;
+    return bf;
+  }
+};
+
 template <int N, class PL = BlockPlan<N>> struct SmemGeom {
   using G = BlockGeom<N, 0, PL>;
   static constexpr int r0 = BoundaryPad<N, 0, 8, PL>::region;
   static constexpr int r1 = G::P > 2 ? BoundaryPad<N, 1, 8, PL>::region : 0;
-  static constexpr int REGION = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;  // float2 per transform
+  static constexpr int BASE = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;
+  static constexpr int REGION = (G::P > 1 && G::T < 16) ? BASE + StrideSearch<N, PL>::best(BASE) : BASE;  // float2 per transform
   static constexpr int BYTES = G::TPB * REGION * 8;
 };
 
@@ -261,7 +286,7 @@ template <int NS, int MAXT = 512> struct GroupGeom {
   static constexpr int TC = TC_BYTES * T > MAXT ? MAXT / T : TC_BYTES;  // <= MAXT threads
   using G = BlockGeom<NS, TC, PL>;
   static constexpr int THREADS = G::THREADS;
-  static constexpr int EX = SmemGeom<NS, PL>::REGION > NS ? SmemGeom<NS, PL>::REGION : NS;
+  static constexpr int EX = SmemGeom<NS, PL>::BASE > NS ? SmemGeom<NS, PL>::BASE : NS;
   static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
   static constexpr int BYTES = TC * REG * 8;
   // resident CTAs the register budget must allow: 16-point codelets fit 64

@@ -57,8 +57,8 @@ template <int NS0, int NS1, int C> struct ClusterGeom {
   static_assert(THREADS <= 1024 && THREADS0 % 32 == 0 && THREADS1 % 32 == 0, "CTA shape");
   static_assert(G0::P == 2 && G1::P == 2 && G0::K(1) == 1 && G1::K(1) == 1, "2-pass sub-FFTs");
   // padded per-column stride of the sub-FFT exchanges (odd: lanes over f hit distinct banks)
-  static constexpr int EX0 = SmemGeom<NS0>::REGION > NS0 ? SmemGeom<NS0>::REGION : NS0;
-  static constexpr int EX1 = SmemGeom<NS1>::REGION > NS1 ? SmemGeom<NS1>::REGION : NS1;
+  static constexpr int EX0 = SmemGeom<NS0>::BASE > NS0 ? SmemGeom<NS0>::BASE : NS0;
+  static constexpr int EX1 = SmemGeom<NS1>::BASE > NS1 ? SmemGeom<NS1>::BASE : NS1;
   static constexpr int REG0 = EX0 | 1, REG1 = EX1 | 1;
   // receive rows: a half-warp of the group-1 reader covers 16 / T1 rows when
   // T1 < 16, so shift consecutive rows by T1 bank pairs
