@@ -45,6 +45,27 @@ def test_in_place_execution(fg, orc, n):
     check_rows(orc, ref, torch.stack([re, im], -1), n, inverse=True)
 
 
+@pytest.mark.parametrize("n", [1024, 4096, 8192, 16384, 1 << 15])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_in_place_persistent_kernels_many_transforms(fg, orc, n, layout):
+    """In-place with several transforms per persistent CTA / cluster: the
+    prefetch of transform b + grid never reads what the bulk stores of
+    transform b write."""
+    batch = 450
+    x = rand((batch, n, 2), 7)
+    ref = x.clone()
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout=layout))
+    if layout == "interleaved":
+        plan.execute(x, x)
+        y = x
+    else:
+        re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+        plan.execute(re, re, im, im)
+        y = torch.stack([re, im], -1)
+    torch.cuda.synchronize()
+    check_rows(orc, ref, y, n, rows=(0, 147, 148, 296, batch - 1))
+
+
 @pytest.mark.parametrize("n", [4096, 16384, 1 << 15, 1 << 16, 1 << 18])
 def test_cuda_graph_capture_and_replay(fg, orc, n):
     batch = 64
