@@ -253,7 +253,8 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       sa.tw_n = p->d_tws + p->split_twn_off;
       return split_launch(p->ex.log2n, layout, direction, sa, p->split_clusters, s);
     }
-    if (p->use_cluster && rows_aligned) {
+    const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
+    if (p->use_cluster && rows_aligned && out_aligned) {
       // persistent clusters, one transform per cluster at a time; group-0
       // tiles arrive as TMA tensor boxes, the intermediate moves through DSMEM
       ClusterArgs c{};

@@ -50,6 +50,12 @@ namespace fftgen_b200 {
 #ifndef FFTGEN_K5_PIPE
 #define FFTGEN_K5_PIPE 2
 #endif
+// group-1 results leave as one TMA tensor box per CTA (staged in X) instead
+// of register stores (1), or not (0); 2 = per layout as measured at 2^15:
+// split 0.486 vs 0.463, interleaved 0.485 vs 0.490
+#ifndef FFTGEN_K5_TMA_STORE
+#define FFTGEN_K5_TMA_STORE 2
+#endif
 
 template <int NS0, int NS1, int C> struct ClusterGeom {
   static constexpr int N = NS0 * NS1;
@@ -124,6 +130,13 @@ FFTGEN_FI void tma_load_3d(void *dst, const void *tmap, int c0, int c1, int c2, 
       : "memory");
 }
 
+// 3-D tensor TMA store: smem box -> global (bulk group)
+FFTGEN_FI void tma_store_3d(const void *tmap, const void *src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 // group-0 tile of transform b -> S (rows [A][f]; split: re plane then im plane)
 template <class CG, int LIN>
 FFTGEN_FI void cluster_tile_issue(const ClusterArgs &a, char *S, uint64_t *bar, int64_t b, int r) {
@@ -166,6 +179,7 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
   const uint32_t xs_local = smem_u32(X);
 
   constexpr bool PIPE = FFTGEN_K5_PIPE == 2 ? LIN == LAYOUT_SPLIT : FFTGEN_K5_PIPE != 0;
+  constexpr bool TSTORE = FFTGEN_K5_TMA_STORE == 2 ? LOUT == LAYOUT_SPLIT : FFTGEN_K5_TMA_STORE != 0;
   const int f0 = tid % CG::TC0, t0 = tid / CG::TC0;
   // group 0, pass 0 of the tile in S (the it-th arrival): raw rows [A][f] ->
   // registers -> codelets -> padded exchange in S
@@ -245,19 +259,48 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
     __syncthreads();  // all rows read: X becomes the padded exchange
     if (tid < CG::THREADS1) smem_write<G1, NS1, 0>(X + f1 * CG::REG1, t1, v);
     __syncthreads();
-    if (tid < CG::THREADS1) {
-      const int f = tid % CG::TC1, t = tid / CG::TC1;
-      smem_read_pass<G1, NS1, 1, DIR>(X + f * CG::REG1, t, a.tw_local1, v);
+    const int f = tid % CG::TC1, t = tid / CG::TC1;
+    if (tid < CG::THREADS1) smem_read_pass<G1, NS1, 1, DIR>(X + f * CG::REG1, t, a.tw_local1, v);
+    if constexpr (TSTORE) {
+      // output rows e of this CTA's TC1 columns m: box [e][f] in X, one tensor store
+      static_assert(NS1 * CG::TC1 <= CG::XLEN, "the output box fits X");
+      __syncthreads();  // every pass-1 read of X done
+      if (tid < CG::THREADS1) {
+#pragma unroll
+        for (int B = 0; B < R11; ++B) {
+          const int e = B * COLS11 + t;
+          if constexpr (LOUT == LAYOUT_SPLIT) {
+            float *xf = reinterpret_cast<float *>(X);
+            xf[e * CG::TC1 + f] = v[B].x;
+            xf[NS1 * CG::TC1 + e * CG::TC1 + f] = v[B].y;
+          } else {
+            X[e * CG::TC1 + f] = v[B];
+          }
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        constexpr int W = LOUT == LAYOUT_SPLIT ? 1 : 2;
+        tma_store_3d(a.omap[0], X, r * CG::TC1 * W, 0, (int)b);
+        if constexpr (LOUT == LAYOUT_SPLIT)
+          tma_store_3d(a.omap[1], reinterpret_cast<const float *>(X) + NS1 * CG::TC1, r * CG::TC1, 0, (int)b);
+        bulk_commit();
+        bulk_wait_read0();  // X is read before the peers may refill it
+      }
+      (void)ob;
+    } else if (tid < CG::THREADS1) {
       const int64_t m = (int64_t)r * CG::TC1 + f;
 #pragma unroll
       for (int B = 0; B < R11; ++B)
         SIO<LOUT>::store(a.out0, a.out1, ob + (int64_t)(B * COLS11 + t) * NS0 + m, v[B]);
     }
-    // the stores above consumed every X read of this thread: X is free
+    // every X read of this thread is done: X is free
     cluster_arrive_relaxed();
     if (!PIPE && b + stride < a.batch) g0_front(it + 1);
   }
   if (it > 0) cluster_wait();  // complete the last barrier phase before exit
+  if (TSTORE && tid == 0) bulk_wait0();
 }
 
 }  // namespace fftgen_b200

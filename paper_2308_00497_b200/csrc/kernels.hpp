@@ -101,6 +101,9 @@ struct ClusterArgs {
   // TMA tensor maps (CUtensorMap, 128 B each) of the input planes viewed as
   // [batch][NS0][NS1] (re / interleaved, im): group-0 tiles are 2-D boxes
   alignas(64) unsigned char tmap[2][128];
+  // output planes viewed as [batch][NS1][NS0]: group-1 results leave as
+  // boxes {TC1 columns, NS1 rows} (FFTGEN_K5_TMA_STORE)
+  alignas(64) unsigned char omap[2][128];
   const void *in0, *in1;
   void *out0, *out1;
   int64_t idist, odist;

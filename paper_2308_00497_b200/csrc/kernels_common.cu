@@ -359,6 +359,18 @@ cudaError_t cluster_encode_maps(int l0, int l1, int csize, int layout, ClusterAr
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
   }
+  // outputs: rows e of NS0 elements, boxes {TC1 columns, NS1 rows}
+  const int64_t tc1 = ns0 / csize;
+  cuuint64_t odims[3] = {(cuuint64_t)(ns0 * w), (cuuint64_t)ns1, (cuuint64_t)a.batch};
+  cuuint64_t ostrides[2] = {(cuuint64_t)(ns0 * w * 4), (cuuint64_t)(a.odist * w * 4)};
+  cuuint32_t obox[3] = {(cuuint32_t)(tc1 * w), (cuuint32_t)ns1, 1};
+  void *oplanes[2] = {a.out0, split ? a.out1 : a.out0};
+  for (int i = 0; i < (split ? 2 : 1); ++i) {
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(a.omap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, oplanes[i],
+                     odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  }
   return cudaSuccess;
 }
 
