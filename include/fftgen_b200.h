@@ -27,13 +27,16 @@
  *                (dist = n: planar arrays; the reference ComplexBuffer's
  *                 [re n | im n] block per transform is in1 = in0 + n, dist = 2n)
  *   out-of-place, or exactly in place (out0 == in0, out1 == in1); partially
- *   overlapping buffers are not supported.  Kernels are enqueued on the
- *   caller's stream; the plan owns its twiddle tables and scratch.
- *   Plan creation and destruction are thread-safe; a plan may be executed
- *   concurrently from several host threads on different streams only when
- *   it needs no scratch (fftgen_plan_scratch_bytes() == 0) and the data are
- *   16-byte aligned with dist * element size a multiple of 16 (otherwise
- *   cluster plans fall back to the scratch-using two-launch path).
+ *   overlapping input and output ranges are rejected with FFTGEN_ERR_EXEC.
+ *   Kernels are enqueued on the caller's stream; the plan owns its twiddle
+ *   tables and scratch.  Plan creation and destruction are thread-safe; a
+ *   plan may be executed concurrently from several host threads on
+ *   different streams only when it needs no scratch
+ *   (fftgen_plan_scratch_bytes() == 0) and the data are 16-byte aligned with
+ *   dist * element size a multiple of 16 (otherwise cluster plans fall back
+ *   to the two-launch path, whose scratch is allocated by the first such
+ *   execute; during CUDA-graph capture that first execute fails with
+ *   FFTGEN_ERR_EXEC instead of allocating).
  */
 #ifndef FFTGEN_B200_H
 #define FFTGEN_B200_H
@@ -45,13 +48,14 @@
 extern "C" {
 #endif
 
-#define FFTGEN_B200_ABI_VERSION 1
+#define FFTGEN_B200_ABI_VERSION 2
 
 typedef struct fftgen_plan fftgen_plan;
 
-/* Status codes.  fftgen.hpp maps them back onto the reference's exception
+/* Status codes.  fftgen_b200.hpp maps them back onto the reference's exception
  * classes (error.hpp:16-71): PLAN -> PlanError, DIMENSION -> DimensionError,
- * FUSE -> FuseError, EXEC/CUDA/NOMEM -> ExecError, INVALID -> DimensionError. */
+ * FUSE -> FuseError, LOWER -> LowerError, BOUNDS -> BoundsError, GPUMAP ->
+ * GpuMapError, EXEC/CUDA/NOMEM -> ExecError, INVALID -> DimensionError. */
 typedef enum {
   FFTGEN_OK = 0,
   FFTGEN_ERR_PLAN = 1,      /* non-power-of-two n, bad radix, size cap      (PlanError) */
@@ -60,12 +64,29 @@ typedef enum {
   FFTGEN_ERR_FUSE = 4,      /* radix above the kernel cap 64                (FuseError) */
   FFTGEN_ERR_INVALID = 5,   /* NULL handle or config                        */
   FFTGEN_ERR_CUDA = 6,      /* CUDA runtime failure (device, launch)        */
-  FFTGEN_ERR_NOMEM = 7      /* device allocation failed                     */
+  FFTGEN_ERR_NOMEM = 7,     /* device allocation failed                     */
+  FFTGEN_ERR_LOWER = 8,     /* rejected schedule option (vector width,
+                               tile size)                                   (LowerError) */
+  FFTGEN_ERR_BOUNDS = 9,    /* a buffer is shorter than the plan's access
+                               range (batch, dist)                          (BoundsError) */
+  FFTGEN_ERR_GPUMAP = 10    /* no sm_100a launch geometry for the plan on
+                               this device (kernel attributes, occupancy)   (GpuMapError) */
 } fftgen_status;
 
 enum { FFTGEN_LAYOUT_INTERLEAVED = 0, FFTGEN_LAYOUT_SPLIT = 1 };     /* ComplexLayout, loopir.hpp:187 */
 enum { FFTGEN_ALG_COOLEY_TUKEY = 0, FFTGEN_ALG_STOCKHAM = 1 };       /* Algorithm, driver.hpp:21 */
 enum { FFTGEN_FORWARD = -1, FFTGEN_INVERSE = 1 };
+enum { FFTGEN_VEC_NONE = 0, FFTGEN_VEC_INNER = 1, FFTGEN_VEC_OUTER = 2 };  /* VecMode, driver.hpp:23 */
+enum { FFTGEN_TILE_NONE = 0, FFTGEN_TILE_EXACT = 1, FFTGEN_TILE_CACHE = 2 }; /* TilePolicy, loopir.hpp:240-248 */
+
+/* Kernel-selection tuning bits (fftgen_config.tuning).  0 selects the
+ * measured-fastest kernels; the bits reproduce the
+ * alternatives for A/B measurement and for the bitwise-equality tests. */
+enum {
+  FFTGEN_TUNE_NO_TMA = 1,        /* N <= 2^14: the direct block kernel; four-step groups: plain tiles */
+  FFTGEN_TUNE_NO_TMA_STORE = 2,  /* block kernels: register stores instead of bulk stores */
+  FFTGEN_TUNE_GROUP_TMA_ALL = 4  /* every four-step group as the persistent TMA-tile kernel */
+};
 
 typedef struct {
   int64_t n;          /* transform size, power of two >= 1                    (PipelineConfig.n) */
@@ -77,6 +98,25 @@ typedef struct {
   int32_t layout;     /* FFTGEN_LAYOUT_*                                  (PipelineConfig.layout) */
   int32_t device;     /* CUDA device ordinal                                   */
   int64_t batch;      /* transforms per execute, >= 1                          */
+  /* The reference's CPU loop-IR schedule (PipelineConfig.vec / vector_width /
+   * interleaved_opt / tile, driver.hpp:26-35).  Validated like
+   * vectorize() / tile() (transforms.cpp: LowerError for a vector width that
+   * is not a power of two <= 64 or a non-positive tile size) and otherwise
+   * result-neutral: the reference guarantees vectorized, tiled and scalar
+   * programs agree bitwise, and the sm_100a passes have their own schedule. */
+  int32_t vec;             /* FFTGEN_VEC_*                    (default NONE) */
+  int32_t vector_width;    /* lanes                           (default 8)    */
+  int32_t interleaved_opt; /* 0 / 1                           (default 0)    */
+  int32_t tile_kind;       /* FFTGEN_TILE_*                   (default NONE) */
+  int64_t tile_value;      /* tile size or cache byte budget                 */
+  /* Kernel selection (B200 extension, not in the reference) */
+  uint32_t tuning;         /* FFTGEN_TUNE_* bits, 0 = measured defaults      */
+  int32_t cluster_size;    /* single-pass cluster kernel for N = 2^15 / 2^16:
+                              0 = measured default, -1 = never (two launches),
+                              or a compiled size (4, 8, 16)                  */
+  int32_t host_chunk_mb;   /* fftgen_execute_host chunk (in + out per slot),
+                              0 = 128 MiB                                    */
+  int32_t reserved0;
 } fftgen_config;
 
 /* Fills the PipelineConfig defaults (driver.hpp:26-35) plus batch=1, device=0. */

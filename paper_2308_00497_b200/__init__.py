@@ -67,13 +67,35 @@ class ExecError(FftgenError):
     """Runtime failure while executing (error.hpp:56-59)."""
 
 
+class LowerError(FftgenError):
+    """A schedule option was rejected (error.hpp:50-53)."""
+
+
+class BoundsError(FftgenError):
+    """A buffer is shorter than the plan's access range (error.hpp:62-65)."""
+
+
+class GpuMapError(FftgenError):
+    """No launch geometry for the plan on this device (error.hpp:68-71)."""
+
+
 _STATUS = {1: PlanError, 2: DimensionError, 3: ExecError, 4: FuseError, 5: DimensionError,
-           6: ExecError, 7: ExecError}
+           6: ExecError, 7: ExecError, 8: LowerError, 9: BoundsError, 10: GpuMapError}
+
+# fftgen_config.tuning bits (include/fftgen_b200.h)
+TUNE_NO_TMA = 1
+TUNE_NO_TMA_STORE = 2
+TUNE_GROUP_TMA_ALL = 4
+VEC_MODES = {"none": 0, "inner": 1, "outer": 2}
 
 
 class _Config(C.Structure):
     _fields_ = [("n", C.c_int64), ("algorithm", C.c_int32), ("radix", C.c_int32),
-                ("layout", C.c_int32), ("device", C.c_int32), ("batch", C.c_int64)]
+                ("layout", C.c_int32), ("device", C.c_int32), ("batch", C.c_int64),
+                ("vec", C.c_int32), ("vector_width", C.c_int32), ("interleaved_opt", C.c_int32),
+                ("tile_kind", C.c_int32), ("tile_value", C.c_int64),
+                ("tuning", C.c_uint32), ("cluster_size", C.c_int32), ("host_chunk_mb", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 def build(jobs: int = 8, quiet: bool = True) -> str:
@@ -88,6 +110,9 @@ def _load() -> C.CDLL:
         raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {CSRC}` "
                           "(or __graft_entry__.build()); there is no CPU fallback")
     L = C.CDLL(LIB_PATH)
+    L.fftgen_abi_version.restype = C.c_int
+    if L.fftgen_abi_version() != 2:
+        raise ImportError(f"{LIB_PATH} has ABI {L.fftgen_abi_version()}, this binding needs 2: rebuild it")
     vp, i64, i64p = C.c_void_p, C.c_int64, C.POINTER(C.c_int64)
     L.fftgen_config_init.argtypes = [C.POINTER(_Config)]
     L.fftgen_config_init.restype = None
@@ -125,13 +150,25 @@ def _check(status: int) -> None:
 
 @dataclass
 class PipelineConfig:
-    """Mirror of fftgen::PipelineConfig (driver.hpp:26-35) plus batch/device."""
+    """Mirror of fftgen::PipelineConfig (driver.hpp:26-35) plus batch/device.
+
+    vec / vector_width / interleaved_opt / tile are the reference's CPU
+    loop-IR schedule: validated like vectorize()/tile() (LowerError) and
+    result-neutral.  tuning / cluster_size / host_chunk_mb select among the
+    sm_100a kernels (0 = the measured defaults)."""
     n: int = 0
     algorithm: str = "cooley-tukey"
     radix: int = 2
     layout: str = "interleaved"
     batch: int = 1
     device: int = 0
+    vec: str = "none"
+    vector_width: int = 8
+    interleaved_opt: bool = False
+    tile: Optional[tuple] = None          # ("exact", size) or ("cache", bytes)
+    tuning: int = 0
+    cluster_size: int = 0
+    host_chunk_mb: int = 0
 
 
 def _ptr(x) -> int:
@@ -158,6 +195,16 @@ class Plan:
         c.layout = LAYOUTS[cfg.layout] if isinstance(cfg.layout, str) else int(cfg.layout)
         c.batch = int(cfg.batch)
         c.device = int(cfg.device)
+        c.vec = VEC_MODES[cfg.vec] if isinstance(cfg.vec, str) else int(cfg.vec)
+        c.vector_width = int(cfg.vector_width)
+        c.interleaved_opt = int(bool(cfg.interleaved_opt))
+        if cfg.tile is not None:
+            kind, value = cfg.tile
+            c.tile_kind = {"exact": 1, "cache": 2}[kind]
+            c.tile_value = int(value)
+        c.tuning = int(cfg.tuning)
+        c.cluster_size = int(cfg.cluster_size)
+        c.host_chunk_mb = int(cfg.host_chunk_mb)
         h = C.c_void_p()
         _check(lib.fftgen_plan_create(C.byref(h), C.byref(c)))
         self._h = h
@@ -183,6 +230,55 @@ class Plan:
         self.close()
 
     # ---- execution ------------------------------------------------------
+    def _check_buffers(self, bufs, dist: int, device: bool) -> None:
+        """Device / dtype / layout / size of every buffer against the plan's
+        access range: transform b, element e at b*dist + e (BoundsError when
+        a buffer is shorter, like the reference's check_bounds)."""
+        need = (self.batch - 1) * dist + self.n  # elements (complex for interleaved)
+        for name, a in bufs:
+            if a is None:
+                continue
+            if hasattr(a, "data_ptr"):  # torch tensor
+                import torch
+                if device:
+                    if a.device.type != "cuda" or a.device.index != self.config.device:
+                        raise ExecError(f"{name} is on {a.device}, plan is on cuda:{self.config.device}")
+                elif a.device.type != "cpu":
+                    raise ExecError(f"{name} must be a host (CPU) tensor, got {a.device}")
+                if a.dtype == torch.complex64:
+                    elems = a.numel()
+                elif a.dtype == torch.float32:
+                    elems = a.numel() // (1 if self.split else 2)
+                else:
+                    raise ExecError(f"{name} must be float32 or complex64, got {a.dtype}")
+                if self.split and a.dtype != torch.float32:
+                    raise ExecError(f"split layout takes float32 planes, {name} is {a.dtype}")
+                per = 1 if (self.split or a.dtype == torch.complex64) else 2  # storage scalars per element
+                if not a.is_contiguous():
+                    # strided views are fine when they ARE the plan's addressing:
+                    # one transform per leading index, dist elements apart
+                    if a.dim() < 2 or not a[0].is_contiguous() or a.stride(0) != dist * per:
+                        raise ExecError(f"{name} is a strided view that does not match dist={dist} "
+                                        f"(stride {tuple(a.stride())})")
+                avail = a.untyped_storage().nbytes() - a.storage_offset() * a.element_size()
+                elems = avail // (a.element_size() * per)
+            elif isinstance(a, np.ndarray):
+                if device:
+                    raise ExecError(f"{name} is a host array; use execute_host")
+                if a.dtype == np.complex64:
+                    elems = a.size
+                elif a.dtype == np.float32:
+                    elems = a.size // (1 if self.split else 2)
+                else:
+                    raise DimensionError(f"host buffers must be float32 or complex64, {name} is {a.dtype}")
+                if not a.flags.c_contiguous:
+                    raise DimensionError(f"{name} must be C-contiguous")
+            else:
+                continue  # raw address: the caller vouches for it
+            if elems < need:
+                raise BoundsError(f"{name} holds {elems} elements, the plan reads/writes {need} "
+                                  f"(batch {self.batch}, dist {dist}, n {self.n})")
+
     def execute(self, in0, out0, in1=None, out1=None, direction: int = FORWARD,
                 dist: Optional[int] = None, stream=None) -> None:
         """Device execute.  Interleaved: float32 tensors (batch, dist, 2) or
@@ -190,6 +286,7 @@ class Plan:
         torch.cuda.Stream, a raw cudaStream_t int, or None (current stream)."""
         if dist is None:
             dist = self.n
+        self._check_buffers((("in0", in0), ("in1", in1), ("out0", out0), ("out1", out1)), dist, True)
         if stream is None:
             try:
                 import torch
@@ -201,14 +298,14 @@ class Plan:
         _check(lib.fftgen_execute(self._h, direction, _ptr(in0), _ptr(in1), _ptr(out0), _ptr(out1),
                                   int(dist), int(stream)))
 
-    def execute_host(self, in0: np.ndarray, out0: np.ndarray, in1=None, out1=None,
+    def execute_host(self, in0, out0, in1=None, out1=None,
                      direction: int = FORWARD, dist: Optional[int] = None) -> None:
         """Host fp32 buffers (numpy or pinned CPU tensors); pipelined H2D/compute/D2H."""
-        for a in (in0, out0, in1, out1):
-            if isinstance(a, np.ndarray) and (a.dtype != np.float32 or not a.flags.c_contiguous):
-                raise DimensionError("host buffers must be C-contiguous float32")
+        if dist is None:
+            dist = self.n
+        self._check_buffers((("in0", in0), ("in1", in1), ("out0", out0), ("out1", out1)), dist, False)
         _check(lib.fftgen_execute_host(self._h, direction, _ptr(in0), _ptr(in1), _ptr(out0), _ptr(out1),
-                                       int(dist if dist is not None else self.n)))
+                                       int(dist)))
 
     def interpret(self, x: np.ndarray, direction: int = FORWARD) -> np.ndarray:
         """fp64 ComplexBuffer storage in/out: (batch, 2n) doubles in the plan layout."""
@@ -279,11 +376,25 @@ def twiddle_multiply(block, row_offset: int, col_offset: int, n: int, direction:
     """In place on a CUDA complex64 (rows, cols) block (or float32 (rows, cols, 2)):
     block[r, c] *= w_n^{(row_offset + r)(col_offset + c)} -- the four-step
     twiddle diagonal D^N (formula.hpp:44-49) on one rank's block."""
+    import torch
+    if block.device.type != "cuda":
+        raise ExecError(f"twiddle_multiply needs a CUDA tensor, got {block.device}")
+    if block.dtype == torch.complex64:
+        if block.dim() != 2 or block.stride(1) != 1:
+            raise ExecError("complex64 block must be 2-D with unit column stride")
+        ld = block.stride(0)
+    elif block.dtype == torch.float32:
+        if block.dim() != 3 or block.shape[2] != 2 or block.stride(2) != 1 or block.stride(1) != 2 \
+                or block.stride(0) % 2:
+            raise ExecError("float32 block must be (rows, cols, 2) with interleaved (re, im) pairs")
+        ld = block.stride(0) // 2
+    else:
+        raise ExecError(f"twiddle_multiply takes complex64 or float32 (rows, cols, 2), got {block.dtype}")
     rows, cols = block.shape[0], block.shape[1]
-    ld = block.stride(0) if block.dtype.is_complex else block.stride(0) // 2
     if stream is None:
-        import torch
         stream = torch.cuda.current_stream(block.device).cuda_stream
+    elif hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
     _check(lib.fftgen_twiddle_multiply(direction, _ptr(block), rows, cols, ld, row_offset, col_offset, n,
                                        int(stream)))
 

@@ -40,13 +40,10 @@ template <> struct BlockPlan<4096> : PlanT<2, 64, 64, 1> {};
 template <> struct BlockPlan<8192> : PlanT<3, 32, 16, 16> {};
 template <> struct BlockPlan<16384> : PlanT<3, 32, 32, 16> {};
 
-// Plans of the K3 group sub-FFTs (default: the block plan of the same size).
+// Plans of the K3 group sub-FFTs: the block plan of the same size.  (Three
+// 8/16-point register passes for NS = 512 / 1024 measured slower on B200:
+// 2^18 0.31 vs 0.41, 2^20 0.29 vs 0.37 of the single-pass roofline.)
 template <int N> struct GroupPlan : BlockPlan<N> {};
-#ifdef FFTGEN_GROUP3
-// three 8/16-point register passes: 64-register codelets, four CTAs per SM
-template <> struct GroupPlan<512> : PlanT<3, 8, 8, 8> {};
-template <> struct GroupPlan<1024> : PlanT<3, 8, 8, 16> {};
-#endif
 
 // TP = transforms per CTA.  0 -> the direct kernel's default (128 threads).
 #ifndef FFTGEN_TW_FACTOR_COLS
@@ -212,24 +209,12 @@ template <int N> struct TmaGeom {
   static constexpr bool ENABLED = N >= 64 && N <= 8192;
   static constexpr int T = BlockGeom<N>::T;
   static constexpr int tp_bytes = (65536 / (8 * N)) > 0 ? 65536 / (8 * N) : 1;
-#ifdef FFTGEN_K2_TP_N  // experiments: override TP for one N
-  static constexpr int TP = N == FFTGEN_K2_TP_N ? FFTGEN_K2_TP : (N == 4096 ? 1 : tp_bytes);
-#else
   static constexpr int TP = N == 4096 ? 1 : tp_bytes;
-#endif
   using G = BlockGeom<N, TP>;
   static constexpr int THREADS = G::THREADS;
-#if defined(FFTGEN_K2_STAGES)
-  static constexpr int STAGES = FFTGEN_K2_STAGES;
-#elif defined(FFTGEN_K2_S2_N)
-  static constexpr int STAGES = (N == 4096 && N != FFTGEN_K2_S2_N) ? 1 : 2;
-#elif defined(FFTGEN_K2_S1_N)
-  static constexpr int STAGES = (N == 4096 || N == FFTGEN_K2_S1_N) ? 1 : 2;
-#elif defined(FFTGEN_K2_S3_N)
-  static constexpr int STAGES = N == FFTGEN_K2_S3_N ? 3 : (N == 4096 ? 1 : 2);
-#else
+  // (three stages: 2^13 0.69 vs 0.86, 2^10 0.88 vs 0.98; single-buffered
+  // 2^13: 0.77 / 0.81 vs 0.86 / 0.86)
   static constexpr int STAGES = N == 4096 ? 1 : 2;
-#endif
   static constexpr int RAW = 8 * N;                                   // bytes per transform
   static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes
   static constexpr int SLOT = ((RAW > XCH ? RAW : XCH) + 127) / 128 * 128;
@@ -245,13 +230,10 @@ template <int N> struct TmaGeom {
 // exchange 2 goes through the plane (re, then im) behind it.  Measured on
 // B200 (1 GiB batches, bulk-store epilogue, factored last-pass twiddles):
 // 0.67 / 0.70 of HBM (split / interleaved) vs 0.50 / 0.54 for the direct
-// kernel.  FFTGEN_TMA1=0 disables it;
-// -DFFTGEN_TMA1_N=8192 also uses it at 2^13 (experiment).
-#ifndef FFTGEN_TMA1_N
-#define FFTGEN_TMA1_N 16384
-#endif
+// kernel (at 2^13: 0.80 / 0.82 vs 0.86 / 0.86 for the double-buffered TMA
+// kernel, so 2^13 keeps that one).
 template <int N> struct Tma1Geom {
-  static constexpr bool ENABLED = N == 16384 || N == FFTGEN_TMA1_N;
+  static constexpr bool ENABLED = N == 16384;
   using G = BlockGeom<N>;
   static constexpr int THREADS = G::THREADS;
   static constexpr int RAW = 8 * N;

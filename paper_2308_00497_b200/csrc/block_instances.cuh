@@ -29,13 +29,12 @@ cudaError_t block_prepare_n(int *tma_blocks_per_sm) {
   *tma_blocks_per_sm = 0;
   if constexpr (Tma1Geom<N>::ENABLED) {
     constexpr int tsmem = Tma1Geom<N>::BYTES;
-    for (auto fn : {fft_block_tma1_kernel<N, LAYOUT, DIR, false, false>, fft_block_tma1_kernel<N, LAYOUT, DIR, true, false>,
-                    fft_block_tma1_kernel<N, LAYOUT, DIR, false, true>, fft_block_tma1_kernel<N, LAYOUT, DIR, true, true>}) {
+    for (auto fn : {fft_block_tma1_kernel<N, LAYOUT, DIR, false>, fft_block_tma1_kernel<N, LAYOUT, DIR, true>}) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tsmem);
       if (e != cudaSuccess) return e;
     }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR, true, true>, Tma1Geom<N>::THREADS, tsmem);
+        tma_blocks_per_sm, fft_block_tma1_kernel<N, LAYOUT, DIR, true>, Tma1Geom<N>::THREADS, tsmem);
   } else if constexpr (TmaGeom<N>::ENABLED) {
     constexpr int tsmem = TmaGeom<N>::BYTES;
     e = cudaFuncSetAttribute(fft_block_tma_kernel<N, LAYOUT, DIR, false>,
@@ -61,11 +60,8 @@ cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, int flags, cudaStre
   if constexpr (Tma1Geom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;
     constexpr int th = Tma1Geom<N>::THREADS, sm = Tma1Geom<N>::BYTES;
-    const bool ex1 = !(flags & BLOCK_TMA1_PLANE_EX1);
-    if (store_tma && ex1) fft_block_tma1_kernel<N, LAYOUT, DIR, true, true><<<grid, th, sm, s>>>(a);
-    else if (store_tma) fft_block_tma1_kernel<N, LAYOUT, DIR, true, false><<<grid, th, sm, s>>>(a);
-    else if (ex1) fft_block_tma1_kernel<N, LAYOUT, DIR, false, true><<<grid, th, sm, s>>>(a);
-    else fft_block_tma1_kernel<N, LAYOUT, DIR, false, false><<<grid, th, sm, s>>>(a);
+    if (store_tma) fft_block_tma1_kernel<N, LAYOUT, DIR, true><<<grid, th, sm, s>>>(a);
+    else fft_block_tma1_kernel<N, LAYOUT, DIR, false><<<grid, th, sm, s>>>(a);
     return cudaGetLastError();
   } else if constexpr (TmaGeom<N>::ENABLED) {
     if (grid <= 0 || a.batch <= 0) return cudaSuccess;

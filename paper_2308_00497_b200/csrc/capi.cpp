@@ -68,6 +68,8 @@ template <class F> fftgen_status guarded(F &&f) {
     return fail(FFTGEN_ERR_DIMENSION, e.what());
   } catch (const ExecError &e) {
     return fail(FFTGEN_ERR_EXEC, e.what());
+  } catch (const LowerError &e) {
+    return fail(FFTGEN_ERR_LOWER, e.what());
   } catch (const std::bad_alloc &) {
     return fail(FFTGEN_ERR_NOMEM, "host allocation failed");
   } catch (const std::exception &e) {
@@ -84,30 +86,15 @@ struct fftgen_plan {
   float2 *d_tw = nullptr;
   // K3 four-step: device-generated group twiddles and intermediate buffers
   float2 *d_twg = nullptr;
-  float2 *d_tws = nullptr;  // K7: 2^14 block-plan tables, then w_N^e for e < N
   float2 *d_scratch = nullptr;
-  float2 *d_fallback = nullptr;  // full-batch scratch of cluster / phased plans, on first unaligned execute
-  size_t scratch_bytes = 0;
-  // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
+  float2 *d_fallback = nullptr;  // scratch of cluster plans, on the first unaligned execute
+  size_t scratch_bytes = 0, fallback_bytes = 0;
   // K3 groups: persistent TMA variant (resident CTAs per group, 0 = off)
   std::vector<int> group_tma_grid;
+  // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
   bool use_cluster = false;
-  bool use_split = false;  // K7 split-cluster kernel (fft_split.cuh)
-  int split_clusters = 0;
-  int64_t split_twn_off = 0;  // float2 offset of the w_N table in d_tws
-  // K6: 2-group plans in one cooperative launch, intermediate in two L2 slots
-  bool use_phased = false;
-  int phased_grid = 0, phased_variant = 0;
-  int64_t phased_lag = 1, phased_slots = 3;
-  int64_t phased_chunk = 0;
-  int *d_done = nullptr;  // per-chunk completed tiles of group 0 and group 1
   int max_clusters = 0, cluster_size = 0;
   std::mutex scratch_mu;  // lazy two-launch scratch of cluster plans (unaligned data)
-  // L2-resident chunked execution of 2-group plans (0 = off)
-  int64_t chunk = 0;
-  cudaStream_t xs[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_a[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr},
-              ev_join[2] = {nullptr, nullptr};
   // host-buffer pipeline scratch (lazily allocated, guarded by mu)
   std::mutex mu;
   void *d_stage = nullptr;
@@ -120,7 +107,6 @@ struct fftgen_plan {
   int tma_grid = 0;
   bool use_tma = true;
   bool use_tma_store = true;
-  bool tma1_plane_ex1 = false;  // FFTGEN_TMA1_EX1=0
 };
 
 NvtxRange::NvtxRange(const fftgen_plan *p, const char *what) {
@@ -131,22 +117,53 @@ NvtxRange::NvtxRange(const fftgen_plan *p, const char *what) {
 
 namespace {
 
+// Do the strided ranges {a + b*step + [0, width)} and {c + b*step + [0, width)},
+// b in [0, count), share a byte?  (Both sides use the plan's dist.)
+bool strided_overlap(uintptr_t a, uintptr_t c, int64_t step, int64_t width, int64_t count) {
+  const int64_t d = (int64_t)(c - a);  // wraps like the pointers do
+  const int64_t span = (count - 1) * step;
+  if (d >= span + width || -d >= span + width) return false;  // disjoint extents
+  // b2 - b1 = j in (-count, count): is |d + j step| < width for some j?
+  const int64_t j0 = step > 0 ? -d / step : 0;
+  for (int64_t j = j0 - 1; j <= j0 + 1; ++j)
+    if (j > -count && j < count) {
+      const int64_t r = d + j * step;
+      if (r < width && -r < width) return true;
+    }
+  return false;
+}
+
 fftgen_status validate_exec(const fftgen_plan *p, int direction, const void *in0, const void *in1,
                             const void *out0, const void *out1, int64_t dist) {
   if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
   if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
     return fail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
   if (!in0 || !out0) return fail(FFTGEN_ERR_EXEC, "NULL data pointer");
-  if (p->cfg.layout == FFTGEN_LAYOUT_SPLIT && (!in1 || !out1))
+  const bool split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+  if (split && (!in1 || !out1))
     return fail(FFTGEN_ERR_EXEC, "split layout needs both re (in0/out0) and im (in1/out1) pointers");
   if (dist < p->cfg.n)
     return fail(FFTGEN_ERR_DIMENSION, "dist " + std::to_string(dist) + " is smaller than n " +
                                           std::to_string(p->cfg.n));
   // element alignment: float2 for interleaved, float for split
-  const uintptr_t al = p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 4 : 8;
+  const uintptr_t al = split ? 4 : 8;
   for (const void *q : {in0, in1, out0, out1})
     if (q && (uintptr_t)q % al != 0)
       return fail(FFTGEN_ERR_EXEC, "data pointer not aligned to its " + std::to_string(al) + "-byte element");
+  // exactly in place (out_i == in_i) is supported; any other shared byte
+  // between an output plane and an input or the other output plane is not
+  const int64_t esz = split ? 4 : 8, step = dist * esz, width = p->cfg.n * esz, cnt = p->cfg.batch;
+  const void *ins[2] = {in0, split ? in1 : nullptr}, *outs[2] = {out0, split ? out1 : nullptr};
+  for (int o = 0; o < 2; ++o) {
+    if (!outs[o]) continue;
+    for (int i = 0; i < 2; ++i)
+      if (ins[i] && !(i == o && ins[i] == outs[o]) &&
+          strided_overlap((uintptr_t)ins[i], (uintptr_t)outs[o], step, width, cnt))
+        return fail(FFTGEN_ERR_EXEC, "output plane " + std::to_string(o) + " partially overlaps input plane " +
+                                         std::to_string(i) + " (only exactly in-place execution is supported)");
+    if (o == 1 && strided_overlap((uintptr_t)outs[0], (uintptr_t)outs[1], step, width, cnt))
+      return fail(FFTGEN_ERR_EXEC, "the re and im output planes overlap");
+  }
   return FFTGEN_OK;
 }
 
@@ -227,9 +244,7 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
       const int64_t groups = (batch + tp - 1) / tp;
       const int grid = (int)std::min<int64_t>(groups, p->tma_grid);
       return block_tma_launch(p->ex.log2n, layout, direction, a, grid,
-                              (p->use_tma_store && out_aligned ? BLOCK_TMA_STORE : 0) |
-                                  (p->tma1_plane_ex1 ? BLOCK_TMA1_PLANE_EX1 : 0),
-                              s);
+                              p->use_tma_store && out_aligned ? BLOCK_TMA_STORE : 0, s);
     }
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
@@ -239,20 +254,6 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const int64_t esz = split ? 4 : 8;
     const bool rows_aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                               (dist * esz) % 16 == 0;
-    if (p->use_split && rows_aligned) {
-      // radix-C DIF step across a C-CTA cluster + one 2^14-point transform per CTA
-      SplitArgs sa{};
-      sa.in0 = in0;
-      sa.in1 = in1;
-      sa.out0 = out0;
-      sa.out1 = out1;
-      sa.idist = dist;
-      sa.odist = dist;
-      sa.batch = batch;
-      sa.tw = p->d_tws;
-      sa.tw_n = p->d_tws + p->split_twn_off;
-      return split_launch(p->ex.log2n, layout, direction, sa, p->split_clusters, s);
-    }
     const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
     if (p->use_cluster && rows_aligned && out_aligned) {
       // persistent clusters, one transform per cluster at a time; group-0
@@ -274,72 +275,21 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
         return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
                               p->max_clusters, s);
     }
-    if (p->use_phased) {
-      // one cooperative launch; chunks stream through two L2-resident slots
-      PhasedArgs pa{};
-      pa.g0 = make_group_args(p, 0, in0, in1, p->d_scratch, nullptr, dist, n);
-      pa.g1 = make_group_args(p, 1, p->d_scratch, nullptr, out0, out1, n, dist);
-      pa.batch = batch;
-      pa.chunk = std::min<int64_t>(p->phased_chunk, batch);
-      pa.done = p->d_done;
-      pa.variant = p->phased_variant;
-      pa.lag = p->phased_lag;
-      pa.slots = p->phased_slots;
-      int64_t threads, smem, t0, t1;
-      phased_geom(gs[0].log2ns, gs[1].log2ns, p->phased_variant, &threads, &smem, &t0, &t1);
-      const int64_t nchunks = (batch + pa.chunk - 1) / pa.chunk;
-      if (p->phased_variant == 2 ||
-          (encode_tile_maps(pa.g0, gs[0].log2ns, split ? 1 : 0, batch, gs[1].ns / t0, pa.tmap0) &&
-           encode_tile_maps(pa.g1, gs[1].log2ns, 2, p->phased_slots * pa.chunk, gs[0].ns / t1,
-                            reinterpret_cast<unsigned char(*)[128]>(pa.tmap1)))) {
-        cudaError_t e = cudaMemsetAsync(p->d_done, 0, 2 * nchunks * sizeof(int), s);
-        if (e != cudaSuccess) return e;
-        const int grid = (int)std::min<int64_t>(p->phased_grid, batch * (t0 + t1));
-        return phased_launch(gs[0].log2ns, gs[1].log2ns, layout, direction, pa, grid, s);
-      }
-    }
-    if (gs.size() == 2 && p->chunk > 0 && batch >= 2 * p->chunk) {
-      // L2-resident chunking: group 0 of chunk c on xs[0], group 1 on xs[1];
-      // the intermediate of a chunk (<= 2 slots live) is read back from L2.
-      cudaError_t e;
-      if ((e = cudaEventRecord(p->ev_fork, s)) != cudaSuccess) return e;
-      for (auto &x : p->xs)
-        if ((e = cudaStreamWaitEvent(x, p->ev_fork, 0)) != cudaSuccess) return e;
-      const int64_t esz = split ? 1 : 2;  // floats per element of a user plane
-      int64_t c = 0;
-      for (int64_t b0 = 0; b0 < batch; b0 += p->chunk, ++c) {
-        const int64_t cnt = std::min<int64_t>(p->chunk, batch - b0);
-        const int slot = (int)(c & 1);
-        float2 *buf = p->d_scratch + (size_t)slot * p->chunk * n;
-        if (c >= 2 && (e = cudaStreamWaitEvent(p->xs[0], p->ev_b[slot], 0)) != cudaSuccess) return e;
-        const float *i0 = (const float *)in0 + b0 * dist * esz;
-        const float *i1 = in1 ? (const float *)in1 + b0 * dist : nullptr;
-        if ((e = launch_group(p, 0, direction, i0, i1, buf, nullptr, dist, n, cnt, p->xs[0], true)) != cudaSuccess)
-          return e;
-        if ((e = cudaEventRecord(p->ev_a[slot], p->xs[0])) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(p->xs[1], p->ev_a[slot], 0)) != cudaSuccess) return e;
-        float *o0 = (float *)out0 + b0 * dist * esz;
-        float *o1 = out1 ? (float *)out1 + b0 * dist : nullptr;
-        if ((e = launch_group(p, 1, direction, buf, nullptr, o0, o1, n, dist, cnt, p->xs[1], true)) != cudaSuccess)
-          return e;
-        if ((e = cudaEventRecord(p->ev_b[slot], p->xs[1])) != cudaSuccess) return e;
-      }
-      for (int i = 0; i < 2; ++i) {
-        if ((e = cudaEventRecord(p->ev_join[i], p->xs[i])) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(s, p->ev_join[i], 0)) != cudaSuccess) return e;
-      }
-      return cudaSuccess;
-    }
     float2 *scratch = p->d_scratch;
-    if (p->use_cluster || p->use_phased || p->use_split) {
+    if (p->use_cluster) {
       // TMA tiles need 16-byte aligned rows: unaligned data takes the
       // two-launch path, whose full-batch scratch is allocated on first use
+      // (never inside a CUDA-graph capture, where cudaMalloc would break it)
       auto *mp = const_cast<fftgen_plan *>(p);
       std::lock_guard<std::mutex> lk(mp->scratch_mu);
-      const size_t need = (size_t)p->ex.scratch_buffers * (size_t)p->cfg.batch * (size_t)n * sizeof(float2);
       if (!mp->d_fallback) {
-        cudaError_t e = cudaMalloc(&mp->d_fallback, need);
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaError_t e = cudaStreamIsCapturing(s, &cs);
         if (e != cudaSuccess) return e;
+        if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+        const size_t need = (size_t)p->ex.scratch_buffers * (size_t)p->cfg.batch * (size_t)n * sizeof(float2);
+        if ((e = cudaMalloc(&mp->d_fallback, need)) != cudaSuccess) return e;
+        mp->fallback_bytes = need;
       }
       scratch = mp->d_fallback;
     }
@@ -373,15 +323,13 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
   // Measured on B200 at N=4096 split (4 GiB of PCIe traffic per execute,
   // scripts/gpu_e2e_ab.sh): 128 MiB + ramp 4: 347-349 GFLOP/s; 64 MiB: 342-344;
   // 256 MiB: 345; 512 MiB + ramp 6: 330; 4 slots x 32 MiB: 50.2 vs 47.8 ms.
-  // FFTGEN_HOST_CHUNK_MB / FFTGEN_HOST_RAMP override.
-  int64_t target = int64_t(128) << 20;
-  if (const char *env = std::getenv("FFTGEN_HOST_CHUNK_MB")) target = std::max<int64_t>(1, std::atoll(env)) << 20;
+  // fftgen_config.host_chunk_mb overrides the chunk.
+  const int64_t target = int64_t(p->cfg.host_chunk_mb > 0 ? p->cfg.host_chunk_mb : 128) << 20;
   int64_t chunk = std::max<int64_t>(1, target / (int64_t)slot_bytes_per_transform);
   chunk = std::min(chunk, batch);
   // ramp: the first chunks are 1/2^RAMP, 1/2^(RAMP-1), ... of a full chunk, so
   // the pipeline fills (H2D of chunk 0 alone) and drains sooner
-  int ramp = 4;
-  if (const char *env = std::getenv("FFTGEN_HOST_RAMP")) ramp = std::max(0, std::min(6, std::atoi(env)));
+  constexpr int ramp = 4;
   const size_t slot = (size_t)chunk * slot_bytes_per_transform;
   cudaError_t e;
   if (p->stage_bytes < K * slot) {
@@ -406,12 +354,18 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
     char *slot_ptr = (char *)p->d_stage + (i % K) * slot;
     // two-launch four-step plans share one scratch buffer: keep their chunks
     // stream-ordered (the K5 cluster path has no scratch)
-    const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster && !p->use_split) ? 0 : (i % K);
-    if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) return cuda_fail(e, "host pipeline");
+    const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster) ? 0 : (i % K);
+    if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) {
+      // drain what was already enqueued: no copy may still touch the
+      // caller's host buffers once this call has returned
+      for (auto &st : p->streams) cudaStreamSynchronize(st);
+      return cuda_fail(e, "host pipeline");
+    }
   }
+  fftgen_status st = FFTGEN_OK;
   for (auto &s : p->streams)
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
-  return FFTGEN_OK;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess && st == FFTGEN_OK) st = cuda_fail(e, "cudaStreamSynchronize");
+  return st;
 }
 
 fftgen_status copy_text(const std::string &s, char *buf, size_t cap) {
@@ -433,6 +387,10 @@ void fftgen_config_init(fftgen_config *cfg) {
   cfg->algorithm = FFTGEN_ALG_COOLEY_TUKEY;  // PipelineConfig defaults (driver.hpp:26-35)
   cfg->radix = 2;
   cfg->layout = FFTGEN_LAYOUT_INTERLEAVED;
+  cfg->vec = FFTGEN_VEC_NONE;
+  cfg->vector_width = 8;
+  cfg->interleaved_opt = 0;
+  cfg->tile_kind = FFTGEN_TILE_NONE;
   cfg->device = 0;
   cfg->batch = 1;
 }
@@ -449,6 +407,9 @@ const char *fftgen_error_string(fftgen_status s) {
   case FFTGEN_ERR_INVALID: return "invalid argument";
   case FFTGEN_ERR_CUDA: return "CUDA error";
   case FFTGEN_ERR_NOMEM: return "out of device memory";
+  case FFTGEN_ERR_LOWER: return "LowerError";
+  case FFTGEN_ERR_BOUNDS: return "BoundsError";
+  case FFTGEN_ERR_GPUMAP: return "GpuMapError";
   }
   return "unknown status";
 }
@@ -464,11 +425,11 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     if (cfg->algorithm != FFTGEN_ALG_COOLEY_TUKEY && cfg->algorithm != FFTGEN_ALG_STOCKHAM)
       throw PlanError("unknown algorithm " + std::to_string(cfg->algorithm));
     if (cfg->batch < 1) throw DimensionError("batch must be >= 1, got " + std::to_string(cfg->batch));
-    // same validation order as compile_pipeline -> plan_* -> fuse
+    // same validation order as compile_pipeline: plan_* -> fuse -> tile -> vectorize
     auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);
     auto radices = stockham_radices(cfg->n, cfg->radix);
-    const char *c14 = std::getenv("FFTGEN_CLUSTER14");
-    ExecPlan ex = build_exec_plan(cfg->n, c14 && c14[0] != '0');
+    check_schedule(cfg->vec, cfg->vector_width, cfg->tile_kind, cfg->tile_value);
+    ExecPlan ex = build_exec_plan(cfg->n);
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -478,53 +439,53 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
                                        std::to_string(ndev) + " visible)");
     DeviceGuard g(cfg->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    int sms = 0;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
+      return cuda_fail(e, "device attributes");
 
     auto *p = new fftgen_plan();
     p->cfg = *cfg;
     p->ex = std::move(ex);
     p->ops = std::move(ops);
     p->radices = std::move(radices);
-    if (p->ex.strategy == STRAT_BLOCK) {
-      int per_sm = 0, sms = 0;
-      if ((e = block_prepare(p->ex.log2n, &per_sm)) != cudaSuccess ||
-          (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess) {
-        delete p;
-        return cuda_fail(e, "kernel attributes");
-      }
-      p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
-      if (const char *env = std::getenv("FFTGEN_DISABLE_TMA")) p->use_tma = env[0] == '0';
-      if (const char *env = std::getenv("FFTGEN_DISABLE_TMA_STORE")) p->use_tma_store = env[0] == '0';
-      if (const char *env = std::getenv("FFTGEN_TMA1_EX1")) p->tma1_plane_ex1 = env[0] == '0';
-    }
     auto bail = [&](fftgen_status st, const std::string &msg) {
       fftgen_plan_destroy(p);
       return fail(st, msg);
     };
+    const uint32_t tune = cfg->tuning;
+    if (p->ex.strategy == STRAT_BLOCK) {
+      int per_sm = 0;
+      if ((e = block_prepare(p->ex.log2n, &per_sm)) != cudaSuccess)
+        return bail(FFTGEN_ERR_GPUMAP, std::string("block kernel attributes: ") + cudaGetErrorString(e));
+      p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
+      p->use_tma = !(tune & FFTGEN_TUNE_NO_TMA);
+      p->use_tma_store = !(tune & FFTGEN_TUNE_NO_TMA_STORE);
+    }
+    cudaStream_t ps = nullptr;  // private stream for the plan's own uploads
+    if ((e = cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking)) != cudaSuccess)
+      return bail(FFTGEN_ERR_CUDA, std::string("stream creation: ") + cudaGetErrorString(e));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{ps};
     if (p->ex.strategy == STRAT_FOURSTEP) {
       for (const GroupDesc &d : p->ex.groups)
         if ((e = group_prepare(d.log2ns)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, std::string("group kernel attributes: ") + cudaGetErrorString(e));
+          return bail(FFTGEN_ERR_GPUMAP, std::string("group kernel attributes: ") + cudaGetErrorString(e));
       // Persistent TMA group kernels where they measured faster (B200,
       // scripts/gpu_ab.sh, 32 KB tiles for NS <= 256): first-group columns at
       // NS >= 512, whose 64 KB tiles leave one CTA of 256 threads per SM without
       // a prefetch (2^18 split 0.40 vs 0.35, 2^20 0.35 vs 0.32 of the single-pass
       // roofline); the 4-CTA 32 KB plain tiles win below (2^16 split 0.43 vs
-      // 0.41) and for rows.  FFTGEN_GROUP_TMA=0 / 1 forces none / all.
-      const char *gt = std::getenv("FFTGEN_GROUP_TMA");
-      const int force = gt ? (gt[0] == '0' ? 0 : 1) : -1;
-      if (force != 0) {
-        int sms = 0;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, "device attributes");
-        for (size_t g = 0; g < p->ex.groups.size(); ++g) {
-          const GroupDesc &d = p->ex.groups[g];
-          const bool first = g == 0;
-          const bool want = force == 1 || (!d.rows && first && d.log2ns >= 9);
-          int bps = 0;
-          if (want && (e = group_tma_prepare(d.log2ns, &bps)) != cudaSuccess)
-            return bail(FFTGEN_ERR_CUDA, std::string("group TMA kernel attributes: ") + cudaGetErrorString(e));
-          p->group_tma_grid.push_back(want ? bps * sms : 0);
-        }
+      // 0.41) and for rows.  FFTGEN_TUNE_NO_TMA / _GROUP_TMA_ALL force none / all.
+      for (size_t gi = 0; gi < p->ex.groups.size(); ++gi) {
+        const GroupDesc &d = p->ex.groups[gi];
+        const bool want = !(tune & FFTGEN_TUNE_NO_TMA) &&
+                          ((tune & FFTGEN_TUNE_GROUP_TMA_ALL) || group_prefers_tma(d.log2ns, gi == 0, d.rows));
+        int bps = 0;
+        if (want && (e = group_tma_prepare(d.log2ns, &bps)) != cudaSuccess)
+          return bail(FFTGEN_ERR_GPUMAP, std::string("group TMA kernel attributes: ") + cudaGetErrorString(e));
+        p->group_tma_grid.push_back(want ? bps * sms : 0);
       }
       // K4: Q[A0][m] = w_s^{A0 (NS/R0) m}, P[c][m] = w_s^{c m}, generated on the device in fp64
       if (p->ex.tw_group_len > 0) {
@@ -534,102 +495,35 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
           if (d.cols <= 1) continue;
           // P is [c][m] for column groups (lanes share m) and [m][c] for the
           // rows group (lanes walk c within a row: coalesced twiddle loads)
-          if ((e = gen_twiddles(p->d_twg + d.q_off, d.r0, d.cols, d.ns / d.r0, d.s, 0)) != cudaSuccess ||
-              (e = d.rows ? gen_twiddles(p->d_twg + d.p_off, d.cols, d.ns / d.r0, 1, d.s, 0)
-                          : gen_twiddles(p->d_twg + d.p_off, d.ns / d.r0, d.cols, 1, d.s, 0)) != cudaSuccess)
+          if ((e = gen_twiddles(p->d_twg + d.q_off, d.r0, d.cols, d.ns / d.r0, d.s, ps)) != cudaSuccess ||
+              (e = d.rows ? gen_twiddles(p->d_twg + d.p_off, d.cols, d.ns / d.r0, 1, d.s, ps)
+                          : gen_twiddles(p->d_twg + d.p_off, d.ns / d.r0, d.cols, 1, d.s, ps)) != cudaSuccess)
             return bail(FFTGEN_ERR_CUDA, std::string("twiddle generation: ") + cudaGetErrorString(e));
         }
       }
-      if (p->ex.groups.size() == 2) {
-        // opt-in: chunk of intermediate per slot; two slots live in L2
-        int64_t chunk_bytes = 0;
-        if (const char *env = std::getenv("FFTGEN_L2_CHUNK_BYTES")) chunk_bytes = std::atoll(env);
-        const int64_t per_tf = cfg->n * (int64_t)sizeof(float2);
-        p->chunk = chunk_bytes > 0 ? std::max<int64_t>(1, chunk_bytes / per_tf) : 0;
-        if (p->chunk > 0 && cfg->batch >= 2 * p->chunk) {
-          for (auto &x : p->xs)
-            if ((e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking)) != cudaSuccess)
-              return bail(FFTGEN_ERR_CUDA, "stream creation");
-          cudaEvent_t *evs[] = {&p->ev_fork, &p->ev_a[0], &p->ev_a[1], &p->ev_b[0], &p->ev_b[1],
-                                &p->ev_join[0], &p->ev_join[1]};
-          for (cudaEvent_t *ev : evs)
-            if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess)
-              return bail(FFTGEN_ERR_CUDA, "event creation");
-        } else {
-          p->chunk = 0;
-        }
-      }
       const auto &gs = p->ex.groups;
-      const char *no_cluster = std::getenv("FFTGEN_DISABLE_CLUSTER");
-      // K5 where measured faster than K3 (cluster_default_size); FFTGEN_CLUSTER_SIZE=C
-      // forces any compiled (NS0, NS1, C) shape
+      // K5 where measured faster than K3 (cluster_default_size); config
+      // cluster_size forces a compiled (NS0, NS1, C) shape or (-1) never
       int csize = gs.size() == 2 ? cluster_default_size(gs[0].log2ns, gs[1].log2ns, cfg->layout) : 0;
-      if (const char *env = std::getenv("FFTGEN_CLUSTER_SIZE"); env && gs.size() == 2) {
+      if (cfg->cluster_size < 0) {
+        csize = 0;
+      } else if (cfg->cluster_size > 0) {
         int64_t t = 0, sm = 0;
-        cluster_geom(gs[0].log2ns, gs[1].log2ns, std::atoi(env), &t, &sm);
-        if (t > 0) csize = std::atoi(env);
+        if (gs.size() == 2) cluster_geom(gs[0].log2ns, gs[1].log2ns, cfg->cluster_size, &t, &sm);
+        if (t == 0)
+          return bail(FFTGEN_ERR_GPUMAP, "no cluster kernel of size " + std::to_string(cfg->cluster_size) +
+                                             " for n = " + std::to_string(cfg->n));
+        csize = cfg->cluster_size;
       }
-      if (csize > 0 && !(no_cluster && no_cluster[0] != '0')) {
+      if (csize > 0) {
         p->cluster_size = csize;
         if ((e = cluster_prepare(gs[0].log2ns, gs[1].log2ns, csize, &p->max_clusters)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, std::string("cluster kernel attributes: ") + cudaGetErrorString(e));
+          return bail(FFTGEN_ERR_GPUMAP, std::string("cluster kernel attributes: ") + cudaGetErrorString(e));
         p->use_cluster = p->max_clusters > 0;
       }
-      // K7 split-cluster kernel (FFTGEN_SPLIT=1): 2^15 / 2^16 in one HBM pass
-      const char *sp = std::getenv("FFTGEN_SPLIT");
-      if (sp && sp[0] == '1' && split_supported(p->ex.log2n)) {
-        if ((e = split_prepare(p->ex.log2n, &p->split_clusters)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, std::string("split kernel attributes: ") + cudaGetErrorString(e));
-        if (p->split_clusters > 0) {
-          std::vector<float> t = block_twiddles(14);
-          p->split_twn_off = (int64_t)t.size() / 2;
-          for (int64_t i = 0; i < cfg->n; ++i) {
-            double re, im;
-            unit_root(cfg->n, i, &re, &im);
-            t.push_back(static_cast<float>(re));
-            t.push_back(static_cast<float>(im));
-          }
-          if ((e = cudaMalloc(&p->d_tws, t.size() * sizeof(float))) != cudaSuccess)
-            return bail(FFTGEN_ERR_NOMEM, std::string("split twiddles: ") + cudaGetErrorString(e));
-          if ((e = cudaMemcpy(p->d_tws, t.data(), t.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
-            return bail(FFTGEN_ERR_CUDA, std::string("split twiddle upload: ") + cudaGetErrorString(e));
-          p->use_split = true;
-          p->use_cluster = false;
-        }
-      }
-      // K6 phased kernel (opt-in, FFTGEN_PHASED=1).  Measured on B200 it keeps
-      // DRAM bytes at exactly 16 N per transform (the intermediate never leaves
-      // L2), but runs below the two-launch K3 path: 2^16 0.29 vs 0.43, 2^18
-      // 0.28 vs 0.41, 2^20 0.25 vs 0.35 of the single-pass roofline.  K3's
-      // passes are bound by the per-tile processing rate of one 16-warp CTA per
-      // SM (3.5 us per 64 KB tile at 2^16), not by HBM, so halving the HBM
-      // bytes of a tile does not shorten it.
-      const char *ph = std::getenv("FFTGEN_PHASED");
-      if (gs.size() == 2 && !p->use_cluster && !p->use_split && phased_supported(gs[0].log2ns, gs[1].log2ns) && ph &&
-          (ph[0] == '1' || ph[0] == '2')) {
-        int bps = 0, sms = 0;
-        p->phased_variant = ph[0] - '0';
-        if ((e = phased_prepare(gs[0].log2ns, gs[1].log2ns, p->phased_variant, &bps)) != cudaSuccess ||
-            (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device)) != cudaSuccess)
-          return bail(FFTGEN_ERR_CUDA, std::string("phased kernel attributes: ") + cudaGetErrorString(e));
-        if (bps > 0) {
-          int64_t slot_mb = 16;
-          if (const char *env = std::getenv("FFTGEN_PHASE_SLOT_MB")) slot_mb = std::max<int64_t>(1, std::atoll(env));
-          p->phased_chunk = std::min<int64_t>(cfg->batch, std::max<int64_t>(1, (slot_mb << 20) / (cfg->n * 8)));
-          if (const char *env = std::getenv("FFTGEN_PHASE_LAG")) p->phased_lag = std::max<int64_t>(1, std::atoll(env));
-          p->phased_slots = p->phased_lag + 2;
-          p->phased_grid = bps * sms;
-          p->use_phased = true;
-          p->chunk = 0;
-          const int64_t nchunks = (cfg->batch + p->phased_chunk - 1) / p->phased_chunk;
-          if ((e = cudaMalloc(&p->d_done, 2 * nchunks * sizeof(int))) != cudaSuccess)
-            return bail(FFTGEN_ERR_NOMEM, "chunk counters");
-        }
-      }
-      p->scratch_bytes = (p->use_cluster || p->use_split) ? 0
-                         : p->use_phased ? (size_t)p->phased_slots * (size_t)p->phased_chunk * (size_t)cfg->n * sizeof(float2)
-                                         : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
-                                           sizeof(float2);
+      p->scratch_bytes = p->use_cluster ? 0
+                                        : (size_t)p->ex.scratch_buffers * (size_t)cfg->batch * (size_t)cfg->n *
+                                              sizeof(float2);
       if (p->scratch_bytes > 0 && (e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
                                           " bytes): " + cudaGetErrorString(e));
@@ -638,10 +532,13 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     if (!tw.empty()) {
       if ((e = cudaMalloc(&p->d_tw, tw.size() * sizeof(float))) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, std::string("twiddle table: ") + cudaGetErrorString(e));
-      if ((e = cudaMemcpy(p->d_tw, tw.data(), tw.size() * sizeof(float), cudaMemcpyHostToDevice)) != cudaSuccess)
+      if ((e = cudaMemcpyAsync(p->d_tw, tw.data(), tw.size() * sizeof(float), cudaMemcpyHostToDevice, ps)) !=
+          cudaSuccess)
         return bail(FFTGEN_ERR_CUDA, std::string("twiddle upload: ") + cudaGetErrorString(e));
     }
-    if ((e = cudaDeviceSynchronize()) != cudaSuccess)
+    // the tables are complete before any stream can use the plan; only the
+    // plan's own stream is waited on (no device-wide synchronisation)
+    if ((e = cudaStreamSynchronize(ps)) != cudaSuccess)
       return bail(FFTGEN_ERR_CUDA, std::string("plan creation: ") + cudaGetErrorString(e));
     *out = p;
     return FFTGEN_OK;
@@ -654,14 +551,8 @@ fftgen_status fftgen_plan_destroy(fftgen_plan *p) {
     DeviceGuard g(p->cfg.device);
     if (p->d_tw) cudaFree(p->d_tw);
     if (p->d_twg) cudaFree(p->d_twg);
-    if (p->d_tws) cudaFree(p->d_tws);
     if (p->d_scratch) cudaFree(p->d_scratch);
-    if (p->d_done) cudaFree(p->d_done);
     if (p->d_fallback) cudaFree(p->d_fallback);
-    for (auto &x : p->xs)
-      if (x) cudaStreamDestroy(x);
-    for (cudaEvent_t ev : {p->ev_fork, p->ev_a[0], p->ev_a[1], p->ev_b[0], p->ev_b[1], p->ev_join[0], p->ev_join[1]})
-      if (ev) cudaEventDestroy(ev);
     if (p->d_stage) cudaFree(p->d_stage);
     for (auto &s : p->streams)
       if (s) cudaStreamDestroy(s);
@@ -679,6 +570,9 @@ fftgen_status fftgen_execute(const fftgen_plan *p, int direction, const void *in
   DeviceGuard g(p->cfg.device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaError_t e = enqueue(p, direction, in0, in1, out0, out1, dist, p->cfg.batch, (cudaStream_t)stream);
+  if (e == cudaErrorStreamCaptureUnsupported)
+    return fail(FFTGEN_ERR_EXEC, "unaligned execute of a cluster plan needs the two-launch scratch: run it once "
+                                 "outside stream capture first (16-byte aligned data never needs it)");
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return FFTGEN_OK;
 }
@@ -807,11 +701,11 @@ int fftgen_plan_launches(const fftgen_plan *p) {
   switch (p->ex.strategy) {
   case STRAT_IDENTITY: return p->cfg.layout == FFTGEN_LAYOUT_SPLIT ? 2 : 1;
   case STRAT_BLOCK: return 1;
-  default: return (p->use_cluster || p->use_phased || p->use_split) ? 1 : (int)p->ex.groups.size();
+  default: return p->use_cluster ? 1 : (int)p->ex.groups.size();
   }
 }
 
-size_t fftgen_plan_scratch_bytes(const fftgen_plan *p) { return p ? p->scratch_bytes : 0; }
+size_t fftgen_plan_scratch_bytes(const fftgen_plan *p) { return p ? p->scratch_bytes + p->fallback_bytes : 0; }
 
 fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) {
   if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
@@ -844,15 +738,7 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << (i == 0 ? " (HBM load)" : " (smem)") << (i + 1 == p->ex.passes.size() ? " (HBM store)" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_FOURSTEP) {
-    if (p->use_split) {
-      int64_t threads, smem, csize;
-      split_geom(p->ex.log2n, &threads, &smem, &csize);
-      o << "split: 1 fft_split_kernel<" << csize << "> launch grid["
-        << std::min<int64_t>(p->cfg.batch, p->split_clusters) * csize << "] cluster[" << csize << "] block["
-        << threads << "] smem=" << smem << "B co-resident clusters=" << p->split_clusters
-        << " (persistent; radix-" << csize << " DIF step through DSMEM, one 2^14-point transform per CTA, "
-        << "stride-" << csize << " stores, no scratch; two-launch path if unaligned)\n";
-    } else if (p->use_cluster) {
+    if (p->use_cluster) {
       int64_t threads, smem;
       const int64_t csize = p->cluster_size;
       cluster_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, p->cluster_size, &threads, &smem);
@@ -860,15 +746,6 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << "> launch grid[" << p->cfg.batch * csize << "] cluster[" << csize << "] block[" << threads
         << "] smem=" << smem << "B co-resident clusters=" << p->max_clusters
         << " (persistent; one transform per cluster, intermediate in DSMEM, no scratch)\n";
-    } else if (p->use_phased) {
-      int64_t threads, smem, t0, t1;
-      phased_geom(p->ex.groups[0].log2ns, p->ex.groups[1].log2ns, p->phased_variant, &threads, &smem, &t0, &t1);
-      o << "phased: 1 " << (p->phased_variant == 2 ? "fft_stream_kernel<" : "fft_phased_kernel<") << p->ex.groups[0].ns << "," << p->ex.groups[1].ns
-        << "> cooperative launch grid[" << p->phased_grid << "] block[" << threads << "] smem=" << smem
-        << "B chunk=" << p->phased_chunk << " transforms, lag " << p->phased_lag << ", " << p->phased_slots
-        << " L2 slots = " << p->scratch_bytes
-        << " B (both groups streamed through L2 with per-chunk dependencies, TMA tiles, intermediate "
-           "discarded after use)\n";
     } else
       o << "four-step: " << p->ex.groups.size() << " fft_group_kernel launches, scratch " << p->scratch_bytes
         << " B\n";

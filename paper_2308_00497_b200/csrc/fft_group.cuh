@@ -36,8 +36,10 @@
 namespace fftgen_b200 {
 
 // Interleaved scratch between groups (LAYOUT_SCRATCH) streams like the user
-// buffers: measured on B200, keeping it L2-resident through chunked
-// execution (FFTGEN_L2_CHUNK_BYTES) lost to the extra launches and tails.
+// buffers: measured on B200, keeping it L2-resident (two-stream chunked
+// execution, or both groups in one cooperative launch with per-chunk
+// dependencies) kept DRAM traffic at 16 N but lost to the extra launches,
+// tails and barriers (2^16: 0.29-0.45 vs 0.46-0.51 of the single-pass roofline).
 constexpr int LAYOUT_SCRATCH = 2;
 
 template <int L> struct SIO;
@@ -55,17 +57,6 @@ template <> struct SIO<LAYOUT_SCRATCH> {
   }
   static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
     __stcs(reinterpret_cast<float2 *>(p0) + off, v);
-  }
-};
-// L2-resident intermediate of the phased kernel: L2-only loads (no stale L1
-// lines across phases) and write-back stores that stay in L2.
-constexpr int LAYOUT_L2 = 3;
-template <> struct SIO<LAYOUT_L2> {
-  static FFTGEN_FI float2 load(const void *p0, const void *, int64_t off) {
-    return __ldcg(reinterpret_cast<const float2 *>(p0) + off);
-  }
-  static FFTGEN_FI void store(void *p0, void *, int64_t off, float2 v) {
-    __stcg(reinterpret_cast<float2 *>(p0) + off, v);
   }
 };
 template <> struct SIO<LAYOUT_SPLIT> {
@@ -104,11 +95,7 @@ FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ t
   }
 }
 
-// DISCARD (rows tiles): once pass 0 has read the tile, its 128-byte L2 lines
-// are dropped without write-back (discard.global.L2) -- the tile is an
-// L2-resident intermediate no one reads again.
-template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0,
-          bool DISCARD = false>
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0>
 FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
   using G = typename GG::G;
   constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
@@ -158,11 +145,6 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
     smem_write<G, NS, 0>(smem + f * REG, t, v);
   }
   compute_sync<BARID, GG::THREADS>();
-  if constexpr (DISCARD && ROWS) {
-    const char *base = reinterpret_cast<const char *>(reinterpret_cast<const float2 *>(a.in0) + ib + m0 * NS);
-    for (int l = tid; l < TC * NS * 8 / 128; l += GG::THREADS)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + l * 128) : "memory");
-  }
 
   // ---- pass 1: smem -> registers (lanes over f), codelet, HBM store ------
   {
@@ -185,8 +167,7 @@ fft_group_kernel(const GroupArgs a) {
   extern __shared__ float4 smem_f4[];
   const int64_t b = blockIdx.x / a.tiles_per_outer;
   const int64_t tt = blockIdx.x - b * a.tiles_per_outer;
-  // rows read from an L2-resident intermediate drop its lines once read
-  group_tile<NS, LIN, LOUT, DIR, ROWS, GroupGeom<NS>, 0, LIN == LAYOUT_L2 && ROWS>(
+  group_tile<NS, LIN, LOUT, DIR, ROWS, GroupGeom<NS>, 0>(
       a, b * a.idist, b * a.odist, tt, reinterpret_cast<float2 *>(smem_f4));
 }
 

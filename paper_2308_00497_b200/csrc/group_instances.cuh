@@ -25,8 +25,6 @@ cudaError_t group_prepare_t() {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, GroupGeom<NS>::BYTES);
 }
 
-// shape: 5..8 = the same first / last groups with an L2-resident
-// intermediate (st.global.cg stores; L2-only loads and discard.global.L2);
 // shape: 0 = (interleaved -> scratch, columns), 1 = (split -> scratch, columns),
 //        2 = (scratch -> interleaved, rows),     3 = (scratch -> split, rows),
 //        4 = (scratch -> scratch, columns)
@@ -38,10 +36,6 @@ cudaError_t group_launch_ns(int shape, const GroupArgs &a, int64_t grid, cudaStr
   case 2: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>(a, grid, s);
   case 3: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>(a, grid, s);
   case 4: return group_launch_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>(a, grid, s);
-  case 5: return group_launch_t<NS, LAYOUT_INTERLEAVED, LAYOUT_L2, DIR, false>(a, grid, s);
-  case 6: return group_launch_t<NS, LAYOUT_SPLIT, LAYOUT_L2, DIR, false>(a, grid, s);
-  case 7: return group_launch_t<NS, LAYOUT_L2, LAYOUT_INTERLEAVED, DIR, true>(a, grid, s);
-  case 8: return group_launch_t<NS, LAYOUT_L2, LAYOUT_SPLIT, DIR, true>(a, grid, s);
   default: return cudaErrorInvalidValue;
   }
 }
@@ -53,10 +47,6 @@ cudaError_t group_prepare_ns() {
   if ((e = group_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_SCRATCH, DIR, false>()) != cudaSuccess) return e;
   if ((e = group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_INTERLEAVED, DIR, true>()) != cudaSuccess) return e;
   if ((e = group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SPLIT, DIR, true>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_INTERLEAVED, LAYOUT_L2, DIR, false>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_SPLIT, LAYOUT_L2, DIR, false>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_L2, LAYOUT_INTERLEAVED, DIR, true>()) != cudaSuccess) return e;
-  if ((e = group_prepare_t<NS, LAYOUT_L2, LAYOUT_SPLIT, DIR, true>()) != cudaSuccess) return e;
   return group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>();
 }
 

@@ -25,9 +25,8 @@ struct BlockArgs {
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
 cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm);
 // persistent TMA-pipelined variant (fft_block_tma_kernel); grid = CTAs;
-// flags: BLOCK_TMA_STORE (bulk-store epilogue), BLOCK_TMA1_PLANE_EX1 (2^14:
-// both exchanges plane-wise instead of the first one through the stage)
-constexpr int BLOCK_TMA_STORE = 1, BLOCK_TMA1_PLANE_EX1 = 2;
+// flags: BLOCK_TMA_STORE (bulk-store epilogue)
+constexpr int BLOCK_TMA_STORE = 1;
 cudaError_t block_tma_launch(int log2n, int layout, int dir, const BlockArgs &a, int grid, int flags,
                              cudaStream_t s);
 bool block_tma_enabled(int log2n);
@@ -50,27 +49,6 @@ struct GroupArgs {
   const float2 *tw_q;      // [A0][m] = w_s^{A0 (NS/R0) m}   (cols > 1)
   const float2 *tw_p;      // [c][m] = w_s^{c m}; [m][c] for the rows group (k == 1)
 };
-
-// K6: both groups of a 2-group plan in one persistent cooperative launch;
-// chunks of `chunk` transforms alternate between two L2-resident slots
-// (fft_phased.cuh).  g0: user in -> slots, g1: slots -> user out.
-struct PhasedArgs {
-  alignas(64) unsigned char tmap0[2][128];  // group-0 input planes (columns view)
-  alignas(64) unsigned char tmap1[128];     // the slots (rows view, slots*chunk transforms)
-  GroupArgs g0, g1;
-  int64_t batch, chunk;
-  int *done;  // [2][nchunks] tiles completed per chunk (group 0, group 1), zeroed per launch
-  int variant;  // 1: TMA tiles (fft_phased_kernel), 2: plain tiles (fft_stream_kernel)
-  int64_t lag;    // group 1 of chunk c runs in segment c + lag of the tile sequence
-  int64_t slots;  // L2-resident intermediate slots (>= lag + 2)
-};
-bool phased_supported(int log2ns0, int log2ns1);
-// *blocks_per_sm: co-resident CTAs per SM (the cooperative grid)
-cudaError_t phased_prepare(int log2ns0, int log2ns1, int variant, int *blocks_per_sm);
-cudaError_t phased_launch(int log2ns0, int log2ns1, int layout, int dir, const PhasedArgs &pa, int grid,
-                          cudaStream_t s);
-void phased_geom(int log2ns0, int log2ns1, int variant, int64_t *threads, int64_t *smem, int64_t *tiles0,
-                 int64_t *tiles1);
 
 // shape: 0 interleaved->scratch columns, 1 split->scratch columns,
 //        2 scratch->interleaved rows,     3 scratch->split rows, 4 scratch->scratch columns
@@ -113,21 +91,6 @@ struct ClusterArgs {
   const float2 *tw_q;       // group 1: [A0][m] = w_N^{A0 (NS1/R0) m}
   const float2 *tw_p;       // group 1 (rows): [m][c] = w_N^{c m}
 };
-// K7: N = C * 2^14 as a radix-C DIF step across a C-CTA cluster plus one
-// 2^14-point transform per CTA (fft_split.cuh); one HBM pass.
-struct SplitArgs {
-  const void *in0, *in1;
-  void *out0, *out1;
-  int64_t idist, odist;
-  int64_t batch;
-  const float2 *tw;    // 2^14-point block-plan pass tables (block_twiddles(14))
-  const float2 *tw_n;  // w_N^e, e in [0, N)
-};
-bool split_supported(int log2n);
-// *max_clusters: co-resident clusters (the persistent grid)
-cudaError_t split_prepare(int log2n, int *max_clusters);
-cudaError_t split_launch(int log2n, int layout, int dir, const SplitArgs &a, int max_clusters, cudaStream_t s);
-void split_geom(int log2n, int64_t *threads, int64_t *smem, int64_t *csize);
 // default cluster size C of the (NS0, NS1) split for a layout, 0 = none
 int cluster_default_size(int log2ns0, int log2ns1, int layout);
 // *max_clusters: co-resident clusters (the persistent grid)

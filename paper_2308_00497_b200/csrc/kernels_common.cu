@@ -4,7 +4,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "fft_block.cuh"
 #include "kernels.hpp"
@@ -55,16 +54,9 @@ cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm) {
 }
 
 namespace {
-template <int N> bool tma_enabled_n() {
-  if constexpr (Tma1Geom<N>::ENABLED) {  // single-stage variant; FFTGEN_TMA1=0 disables
-    const char *env = std::getenv("FFTGEN_TMA1");
-    return !(env && env[0] == '0');
-  } else if constexpr (N == 64 || N == 128) {  // measured slower than direct; opt-in
-    return TmaGeom<N>::ENABLED && std::getenv("FFTGEN_TMA_SMALL");
-  } else {
-    return TmaGeom<N>::ENABLED;
-  }
-}
+// persistent TMA variants exist for 256 <= N <= 2^14; N = 64 / 128 run the
+// direct kernel (measured on B200: TMA 0.76-0.90 vs direct 0.79-0.99)
+template <int N> bool tma_enabled_n() { return Tma1Geom<N>::ENABLED || (TmaGeom<N>::ENABLED && N >= 256); }
 template <int N> void tma_geom_n(int64_t *threads, int64_t *tp, int64_t *smem) {
   if constexpr (Tma1Geom<N>::ENABLED) {
     *threads = Tma1Geom<N>::THREADS, *tp = 1, *smem = Tma1Geom<N>::BYTES;
@@ -284,7 +276,6 @@ cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, 
 #include <cudaTypedefs.h>
 
 #include "cluster_instances.cuh"
-#include "fft_split.cuh"
 
 namespace fftgen_b200 {
 
@@ -299,10 +290,9 @@ cudaError_t cluster_prepare_b(int, int, int, int *);
 //   2^16 C=16: split 12.9 vs 12.6, interleaved 13.7 vs 14.4 (K3 with the TMA
 //              first group: split 0.764 ms vs 0.835 ms for K5)
 //   2^17 C=16: split 10.4 vs 12.0, interleaved 10.7 vs 13.2 (shape dropped: 2^17 now splits 2^9 x 2^8)
-// 2^14 (FFTGEN_CLUSTER14 plans) C=4: 14.6 vs 17.0 for the K2 block kernel.
+// 2^14 C=4: 14.6 vs 17.0 for the K2 block kernel (shape dropped).
 int cluster_default_size(int l0, int l1, int /*layout*/) {
   switch (l0 * 16 + l1) {
-  case 7 * 16 + 7: return 4;
   case 7 * 16 + 8: return 8;
   case 8 * 16 + 8: return 0;
   default: return 0;
@@ -374,33 +364,6 @@ cudaError_t cluster_encode_maps(int l0, int l1, int csize, int layout, ClusterAr
   return cudaSuccess;
 }
 
-cudaError_t split_launch_f(int, int, const SplitArgs &, int, cudaStream_t);
-cudaError_t split_launch_b(int, int, const SplitArgs &, int, cudaStream_t);
-cudaError_t split_prepare_f(int, int *);
-cudaError_t split_prepare_b(int, int *);
-
-bool split_supported(int log2n) { return log2n == 15 || log2n == 16; }
-
-cudaError_t split_prepare(int log2n, int *max_clusters) {
-  int a = 0, b = 0;
-  cudaError_t e = split_prepare_f(log2n, &a);
-  if (e == cudaSuccess) e = split_prepare_b(log2n, &b);
-  *max_clusters = a < b ? a : b;
-  return e;
-}
-
-cudaError_t split_launch(int log2n, int layout, int dir, const SplitArgs &a, int max_clusters, cudaStream_t s) {
-  return dir < 0 ? split_launch_f(log2n, layout, a, max_clusters, s) : split_launch_b(log2n, layout, a, max_clusters, s);
-}
-
-void split_geom(int log2n, int64_t *threads, int64_t *smem, int64_t *csize) {
-  *threads = *smem = *csize = 0;
-  if (!split_supported(log2n)) return;
-  *threads = SplitGeom<2>::THREADS;
-  *smem = SplitGeom<2>::BYTES;
-  *csize = int64_t(1) << (log2n - 14);
-}
-
 cudaError_t cluster_prepare(int l0, int l1, int c, int *max_clusters) {
   int a = 0, b = 0;
   cudaError_t e = cluster_prepare_f(l0, l1, c, &a);
@@ -463,46 +426,3 @@ bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
 
 }  // namespace fftgen_b200
 
-// ---- K6 phased dispatch ------------------------------------------------------
-#include "phased_instances.cuh"
-
-namespace fftgen_b200 {
-
-cudaError_t phased_launch_f(int, int, int, const PhasedArgs &, int, cudaStream_t);
-cudaError_t phased_launch_b(int, int, int, const PhasedArgs &, int, cudaStream_t);
-cudaError_t phased_prepare_f(int, int, int *, int);
-cudaError_t phased_prepare_b(int, int, int *, int);
-
-void phased_geom(int l0, int l1, int variant, int64_t *threads, int64_t *smem, int64_t *tiles0, int64_t *tiles1) {
-  *threads = *smem = *tiles0 = *tiles1 = 0;
-  switch (l0 * 16 + l1) {
-#define FFTGEN_PG(A, B, NA, NB)                                                                    \
-  case A * 16 + B:                                                                                 \
-    *threads = PhasedGeom<NA, NB>::THREADS;                                                        \
-    *smem = variant == 2 ? StreamGeom<NA, NB>::SMEM : PhasedGeom<NA, NB>::SMEM;                    \
-    *tiles0 = PhasedGeom<NA, NB>::TILES0;                                                          \
-    *tiles1 = PhasedGeom<NA, NB>::TILES1;                                                          \
-    break;
-    FFTGEN_PHASED_SHAPES(FFTGEN_PG)
-#undef FFTGEN_PG
-  default: break;
-  }
-}
-
-bool phased_supported(int l0, int l1) {
-  int64_t t, m, a, b;
-  phased_geom(l0, l1, 1, &t, &m, &a, &b);
-  return t > 0;
-}
-
-cudaError_t phased_prepare(int l0, int l1, int variant, int *bps) {
-  *bps = 1 << 30;
-  cudaError_t e = phased_prepare_f(l0, l1, bps, variant);
-  return e != cudaSuccess ? e : phased_prepare_b(l0, l1, bps, variant);
-}
-
-cudaError_t phased_launch(int l0, int l1, int layout, int dir, const PhasedArgs &pa, int grid, cudaStream_t s) {
-  return dir < 0 ? phased_launch_f(l0, l1, layout, pa, grid, s) : phased_launch_b(l0, l1, layout, pa, grid, s);
-}
-
-}  // namespace fftgen_b200

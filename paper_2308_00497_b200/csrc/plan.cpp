@@ -1,8 +1,6 @@
 // plan.cpp -- host plan builder (see plan.hpp).
 #include "plan.hpp"
 
-#include <cstdlib>
-
 #include <cmath>
 #include <sstream>
 
@@ -158,7 +156,20 @@ void op_map(const RefOp &op, int64_t n, int64_t *map, int64_t *s_out) {
   }
 }
 
-ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
+void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_value) {
+  if (tile_kind < 0 || tile_kind > 2) throw LowerError("unknown tile policy " + std::to_string(tile_kind));
+  if (tile_kind != 0 && tile_value <= 0)  // tile_nest (transforms.cpp:85-95)
+    throw LowerError(std::string(tile_kind == 1 ? "tile size" : "cache volume") + " must be positive, got " +
+                     std::to_string(tile_value));
+  if (vec < 0 || vec > 2) throw LowerError("unknown vector mode " + std::to_string(vec));
+  if (vec != 0) {  // vectorize (transforms.cpp:349-354)
+    if (!is_pow2(vector_width))
+      throw LowerError("vector width must be a power of two, got " + std::to_string(vector_width));
+    if (vector_width > 64) throw LowerError("vector width capped at 64 lanes");
+  }
+}
+
+ExecPlan build_exec_plan(int64_t n) {
   if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
   ExecPlan p;
   p.n = n;
@@ -167,7 +178,7 @@ ExecPlan build_exec_plan(int64_t n, bool fourstep_14) {
     p.strategy = STRAT_IDENTITY;
     return p;
   }
-  if (p.log2n <= 14 && !(fourstep_14 && p.log2n == 14)) {
+  if (p.log2n <= 14) {
     p.strategy = STRAT_BLOCK;
     const int np = block_num_passes(p.log2n);
     for (int q = 0; q < np; ++q) {
@@ -228,19 +239,18 @@ std::vector<int> group_split(int log2n) {
   // 2^30; sizes as even as possible.  Measured on B200:
   // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
-  // 64-byte segments).  FFTGEN_GROUP_MAX_LOG2=L allows 3 groups up to 2^(3L).
-  int max3 = 28;
-  if (const char *env = std::getenv("FFTGEN_GROUP_MAX_LOG2")) max3 = 3 * std::atoi(env);
-  int g = log2n <= 20 ? 2 : (log2n <= max3 ? 3 : 4);
+  // 64-byte segments).
+  const int g = log2n <= 20 ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs
   // it (measured on B200: 2^17 0.45 / 0.47 vs 0.42 / 0.45, 2^25 0.29 / 0.30 vs
   // 0.27 / 0.28 split / interleaved); otherwise the larger groups go last
-  // (2^19 as 10+9: 0.36 vs 0.38).  FFTGEN_LARGE_FIRST=0 / 1 forces either.
-  bool large_first = log2n / g == 8 && log2n % g == 1;
-  if (const char *lf = std::getenv("FFTGEN_LARGE_FIRST")) large_first = lf[0] == '1';
+  // (2^19 as 10+9: 0.36 vs 0.38).
+  const bool large_first = log2n / g == 8 && log2n % g == 1;
   for (int i = 0; i < log2n % g; ++i) out[large_first ? i : g - 1 - i] += 1;
   return out;
 }
+
+bool group_prefers_tma(int log2ns, bool first, bool rows) { return !rows && first && log2ns >= 9; }
 
 }  // namespace fftgen_b200

@@ -23,6 +23,11 @@ struct PlanError : std::runtime_error { using std::runtime_error::runtime_error;
 struct DimensionError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct FuseError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ExecError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct LowerError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// The reference's CPU schedule options (PipelineConfig.vec / vector_width /
+// tile), validated like vectorize() / tile() (transforms.cpp:85-95, 351-354).
+void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_value);
 
 enum OpKind { OP_MKIV = 0, OP_IKMV = 1, OP_PKIV = 2, OP_TWIDDLE = 3, OP_PERMUTE = 4 };
 
@@ -77,13 +82,13 @@ struct ExecPlan {
 };
 
 // The group split of log2 N used by the four-step path (2..4 groups of
-// 2^6..2^10 points).
+// 2^7..2^12 points).
 std::vector<int> group_split(int log2n);
+// whether a group runs the persistent TMA-tile kernel by default (measured)
+bool group_prefers_tma(int log2ns, bool first, bool rows);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
-// fourstep_14: plan N = 2^14 as two 2^7-point groups (run by the K5 cluster
-// kernel) instead of the K2 block kernel.
-ExecPlan build_exec_plan(int64_t n, bool fourstep_14 = false);
+ExecPlan build_exec_plan(int64_t n);
 
 // K2 pass structure of an N-point block kernel (defined in kernels_common.cu
 // from the compile-time BlockPlan), and its [A][m] twiddle table in floats.

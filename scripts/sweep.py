@@ -2,13 +2,13 @@
 """Size / layout / variant sweep in one process (development tool, not the bench).
 
     python scripts/sweep.py --sizes 14,15,16 --layouts split,interleaved \
-        --variants default,FFTGEN_DISABLE_CLUSTER=1 [--bytes 1073741824] [--inverse]
+        --variants default,cluster_size=-1 [--bytes 1073741824] [--inverse]
 
 Per row: CUDA-event time of `steps` back-to-back executes on device-resident
 inputs of ~`bytes` per GPU (inputs + outputs far larger than L2), GFLOP/s of
 5 N log2 N and the fraction of the measured HBM peak for 16 N bytes per
-transform.  Variant = comma-free list of ENV=VAL pairs joined by '+', applied
-before plan creation (the plan reads its opt-in switches then).
+transform.  Variant = PipelineConfig field overrides KEY=INT joined by '+'
+(tuning=<FFTGEN_TUNE_* bits>, cluster_size=C).
 """
 import argparse
 import json
@@ -55,16 +55,12 @@ def main():
                 out0 = torch.empty_like(in0)
             ref = None
             for var in a.variants.split(","):
-                saved = dict(os.environ)
+                kw = {}
                 if var != "default":
                     for kv in var.split("+"):
                         k, v = kv.split("=", 1)
-                        os.environ[k] = v
-                try:
-                    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
-                finally:
-                    os.environ.clear()
-                    os.environ.update(saved)
+                        kw[k] = int(v, 0)
+                plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, **kw))
                 for _ in range(a.warmup):
                     plan.execute(in0, out0, in1, out1, direction=direction)
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -87,16 +87,16 @@ def test_cuda_graph_capture_and_replay(fg, orc, n):
 
 
 @pytest.mark.parametrize("n", [1 << 15, 1 << 16])
-def test_split_cluster_in_place_and_graph(fg, orc, n, monkeypatch):
-    """Opt-in K7: in-place is safe because every CTA of a cluster has read its
-    raw slices (cluster barrier) before any output of that transform is
-    written; the persistent launch also replays from a CUDA graph."""
-    monkeypatch.setenv("FFTGEN_SPLIT", "1")
+def test_cluster_in_place_and_graph(fg, orc, n):
+    """K5: in place is safe (each transform's tiles are read before any of its
+    outputs is written) and the persistent launch replays from a CUDA graph.
+    An unaligned execute inside a capture cannot allocate the two-launch
+    scratch: it fails with ExecError instead of breaking the capture."""
     batch = 200
     x = rand((batch, n, 2), 6)
     ref = x.clone()
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
-    assert "fft_split_kernel" in plan.describe()
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, cluster_size=8 if n == 1 << 15 else 16))
+    assert "fft_cluster_kernel" in plan.describe()
     plan.execute(x, x)
     torch.cuda.synchronize()
     check_rows(orc, ref, x, n, rows=(0, 99, batch - 1))
@@ -112,6 +112,14 @@ def test_split_cluster_in_place_and_graph(fg, orc, n, monkeypatch):
     g.replay()
     torch.cuda.synchronize()
     check_rows(orc, ref, y, n, rows=(1, batch - 2))
+    assert plan.scratch_bytes() == 0
+    buf = torch.zeros(batch * n * 2 + 2, device="cuda")
+    unaligned = buf[2:].view(batch, n, 2)
+    g2 = torch.cuda.CUDAGraph()
+    with pytest.raises(fg.ExecError):
+        with torch.cuda.graph(g2, stream=s):
+            plan.execute(unaligned, y, stream=s)
+    torch.cuda.synchronize()
 
 
 @pytest.mark.parametrize("n", [1 << 15, 1 << 17])
@@ -169,3 +177,30 @@ def test_many_plans_and_destroy(fg):
         p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 20, batch=16))
         p.close()
     assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)  # no leak of scratch/tables
+
+
+def test_partial_overlap_rejected_exact_in_place_accepted(fg, orc):
+    """validate_exec: an output plane sharing bytes with an input plane is an
+    ExecError unless it is exactly in place; the reference's [re n | im n]
+    storage (in1 = in0 + n, dist = 2n) in place is two disjoint strided sets."""
+    n, batch = 1024, 3
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
+    buf = rand((batch * n + 64, 2), 4)
+    with pytest.raises(fg.ExecError, match="overlaps"):
+        plan.execute(buf[:batch * n], buf[32:32 + batch * n])       # shifted by 32 elements
+    with pytest.raises(fg.ExecError, match="overlaps"):
+        plan.execute(buf[:batch * n], buf[n:n + batch * n])         # shifted by one transform
+    ref = buf[:batch * n].clone()
+    plan.execute(buf[:batch * n], buf[:batch * n])                  # exactly in place
+    torch.cuda.synchronize()
+    check_rows(orc, ref.view(batch, n, 2), buf[:batch * n].view(batch, n, 2), n, rows=(0, 2))
+    sp = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout="split"))
+    blk = rand((batch, 2 * n), 5)
+    want = blk.clone()
+    sp.execute(blk, blk, blk[:, n:], blk[:, n:], dist=2 * n)       # [re n | im n] in place
+    out = torch.empty_like(want)
+    sp.execute(want, out, want[:, n:], out[:, n:], dist=2 * n)
+    torch.cuda.synchronize()
+    assert torch.equal(blk, out)
+    with pytest.raises(fg.ExecError, match="overlap"):
+        sp.execute(want, out, want[:, n:], out[:, 1:], dist=2 * n)  # im plane over the re plane

@@ -159,46 +159,10 @@ def test_2p26_random_sampled_bins_and_roundtrip(fg, orc):
     assert np.abs(got - want).max() / scale < 1e-4
 
 
-@pytest.mark.parametrize("layout", ["interleaved", "split"])
-def test_l2_chunked_two_group_path(fg, orc, layout, monkeypatch):
-    """Batched 2-group plans run in L2-sized chunks on two internal streams;
-    the result is bitwise the unchunked one and matches the oracle."""
-    n, batch = 1 << 15, 700   # chunk = 32 MiB / 256 KiB = 128 transforms -> 6 chunks
-    g = torch.Generator(device="cuda").manual_seed(21)
-    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
-
-    def run_once():
-        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
-        if layout == "interleaved":
-            y = torch.full_like(x, float("nan"))
-            plan.execute(x, y)
-        else:
-            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
-            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
-            plan.execute(re, ore, im, oim)
-            y = torch.stack([ore, oim], dim=-1)
-        torch.cuda.synchronize()
-        return y
-
-    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
-    monkeypatch.setenv("FFTGEN_PHASED", "0")
-    monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", str(32 << 20))
-    chunked = run_once()
-    monkeypatch.setenv("FFTGEN_L2_CHUNK_BYTES", "0")
-    plain = run_once()
-    monkeypatch.delenv("FFTGEN_L2_CHUNK_BYTES")
-    assert torch.equal(chunked, plain)
-    for b in (0, 127, 128, 555, batch - 1):
-        xi = x[b].reshape(-1).double().cpu().numpy()
-        got = chunked[b].reshape(-1).double().cpu().numpy()
-        assert oracle.rel_l2(got, orc.forward(xi, "stockham", 4)) < 3e-6, b
-
-
-@pytest.mark.parametrize("l2,batch,csize", [(14, 301, 2), (14, 301, 4), (15, 301, 4), (15, 301, 8),
-                                            (16, 150, 8), (16, 150, 16)])
+@pytest.mark.parametrize("l2,batch,csize", [(15, 301, 4), (15, 301, 8), (16, 150, 8), (16, 150, 16)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 @pytest.mark.parametrize("direction", [-1, 1])
-def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layout, direction, monkeypatch):
+def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layout, direction):
     """K5 (persistent clusters, one transform per cluster, TMA tensor tiles in,
     the intermediate exchanged through distributed shared memory) performs
     exactly the arithmetic of the two-launch K3 path, so the results are
@@ -206,11 +170,9 @@ def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layou
     n = 1 << l2
     g = torch.Generator(device="cuda").manual_seed(100 + l2)
     x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
-    if l2 == 14:
-        monkeypatch.setenv("FFTGEN_CLUSTER14", "1")  # plan 2^14 as 2^7 x 2^7 groups
 
-    def run_once():
-        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+    def run_once(cluster_size):
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, cluster_size=cluster_size))
         if layout == "interleaved":
             y = torch.full_like(x, float("nan"))
             plan.execute(x, y, direction=direction)
@@ -222,12 +184,9 @@ def test_cluster_kernel_bitwise_two_launch_path(fg, orc, l2, batch, csize, layou
         torch.cuda.synchronize()
         return y, plan.describe()
 
-    monkeypatch.setenv("FFTGEN_CLUSTER_SIZE", str(csize))
-    cl, d1 = run_once()
+    cl, d1 = run_once(csize)
     assert f"fft_cluster_kernel<{1 << (l2 // 2)},{1 << (l2 - l2 // 2)},{csize}>" in d1
-    monkeypatch.delenv("FFTGEN_CLUSTER_SIZE")
-    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
-    two, d2 = run_once()
+    two, d2 = run_once(-1)
     assert "fft_cluster_kernel" not in d2
     assert torch.equal(cl, two)
     for b in (0, batch // 2, batch - 1):
@@ -259,7 +218,7 @@ def test_cluster_kernel_unaligned_rows_fall_back(fg, orc):
 
 @pytest.mark.parametrize("l2,batch", [(15, 40), (16, 20), (18, 6), (20, 3), (22, 1), (28, 1)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
-def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch):
+def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout):
     """The persistent TMA group kernels (tensor-tile prefetch) are bitwise the
     plain group kernels for every shape (first / middle columns, rows)."""
     if l2 == 28 and layout == "interleaved":
@@ -267,12 +226,11 @@ def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch
     n = 1 << l2
     g = torch.Generator(device="cuda").manual_seed(l2)
     x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
-    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
-    monkeypatch.setenv("FFTGEN_PHASED", "0")
 
     def run_once(tma):
-        monkeypatch.setenv("FFTGEN_GROUP_TMA", tma)
-        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
+        tuning = fg.TUNE_GROUP_TMA_ALL if tma == "1" else fg.TUNE_NO_TMA
+        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, cluster_size=-1,
+                                                     tuning=tuning))
         if layout == "interleaved":
             y = torch.full_like(x, float("nan"))
             plan.execute(x, y)
@@ -294,52 +252,6 @@ def test_group_tma_kernels_bitwise_plain(fg, orc, l2, batch, layout, monkeypatch
     if l2 <= 20:
         xi = x[0].reshape(-1).double().cpu().numpy()
         assert oracle.rel_l2(a[0].reshape(-1).double().cpu().numpy(), orc.forward(xi, "stockham", 4)) < 3e-6
-
-
-@pytest.mark.parametrize("l2,batch,slot_mb", [(15, 301, 24), (15, 37, 1), (16, 150, 24), (16, 9, 1),
-                                              (17, 77, 3), (18, 20, 24), (19, 7, 8), (20, 5, 8), (20, 2, 24)])
-@pytest.mark.parametrize("layout", ["interleaved", "split"])
-@pytest.mark.parametrize("direction", [-1, 1])
-@pytest.mark.parametrize("variant,lag", [("1", "1"), ("2", "1"), ("2", "3")])
-def test_phased_kernel_bitwise_two_launch_path(fg, orc, l2, batch, slot_mb, layout, direction, variant, lag,
-                                               monkeypatch):
-    """K6 (both groups in one cooperative launch, chunks alternating between two
-    L2-resident slots, grid barrier per chunk, intermediate discarded after use)
-    (opt-in) is bitwise the two-launch K3 path, for ragged last chunks, one-transform
-    chunks and batches smaller than a chunk; both match the oracle."""
-    n = 1 << l2
-    g = torch.Generator(device="cuda").manual_seed(200 + l2)
-    x = torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1
-    monkeypatch.setenv("FFTGEN_DISABLE_CLUSTER", "1")
-    monkeypatch.setenv("FFTGEN_PHASED", variant)
-    monkeypatch.setenv("FFTGEN_PHASE_LAG", lag)
-    monkeypatch.setenv("FFTGEN_PHASE_SLOT_MB", str(slot_mb))
-
-    def run_once():
-        plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
-        if layout == "interleaved":
-            y = torch.full_like(x, float("nan"))
-            plan.execute(x, y, direction=direction)
-        else:
-            re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
-            ore, oim = torch.full_like(re, float("nan")), torch.full_like(im, float("nan"))
-            plan.execute(re, ore, im, oim, direction=direction)
-            y = torch.stack([ore, oim], dim=-1)
-        torch.cuda.synchronize()
-        d = plan.describe()
-        plan.close()
-        return y, d
-
-    ph, d1 = run_once()
-    assert ("fft_phased_kernel" if variant == "1" else "fft_stream_kernel") in d1
-    monkeypatch.setenv("FFTGEN_PHASED", "0")
-    two, d2 = run_once()
-    assert "fft_phased_kernel" not in d2 and "fft_stream_kernel" not in d2
-    assert torch.equal(ph, two)
-    for b in (0, batch - 1):
-        xi = x[b].reshape(-1).double().cpu().numpy()
-        want = orc.forward(xi, "stockham", 4, inverse=direction > 0)
-        assert oracle.rel_l2(ph[b].reshape(-1).double().cpu().numpy(), want) < 3e-6, b
 
 
 @pytest.mark.parametrize("l2", [21, 22])
@@ -368,70 +280,4 @@ def test_huge_roundtrip_inverse(fg, l2):
     torch.cuda.synchronize()
     err = (torch.linalg.norm((y / n - x).double()) / torch.linalg.norm(x.double())).item()
     assert err < 1e-6, err
-    plan.close()
-
-
-@pytest.mark.parametrize("layout", ["interleaved", "split"])
-@pytest.mark.parametrize("direction", [-1, 1])
-@pytest.mark.parametrize("l2", [15, 16])
-def test_split_cluster_kernel_matches_oracle(fg, orc, l2, layout, direction, monkeypatch):
-    """K7 (fft_split.cuh): radix-C DIF step across a C-CTA cluster, one
-    2^14-point transform per CTA.  A batch above the co-resident cluster count
-    exercises the persistent loop (raw slice refills, z mbarrier phases)."""
-    monkeypatch.setenv("FFTGEN_SPLIT", "1")
-    n = 1 << l2
-    batch = 5
-    x = seeded_batch(orc, n, batch, seed0=11)
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch))
-    assert "fft_split_kernel" in plan.describe() and plan.launches() == 1
-    plan.close()
-    got = run(fg, n, layout, direction, x)
-    want = orc.forward(x, "stockham", 4, inverse=direction > 0, threads=4)
-    for b in range(batch):
-        err = oracle.rel_l2(got[b], want[b])
-        assert err <= tol(n) and err < 3e-6, (n, b, err)
-
-
-@pytest.mark.parametrize("l2", [15, 16])
-def test_split_cluster_kernel_long_batch(fg, orc, l2, monkeypatch):
-    """Many transforms per cluster: forward then inverse round trip on a batch
-    several times the co-resident cluster count, plus oracle spot checks."""
-    monkeypatch.setenv("FFTGEN_SPLIT", "1")
-    n = 1 << l2
-    batch = 300
-    g = torch.Generator(device="cuda").manual_seed(l2)
-    x = (torch.rand(batch, n, 2, device="cuda", generator=g) * 2 - 1).contiguous()
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="interleaved", batch=batch))
-    y = torch.empty_like(x)
-    z = torch.empty_like(x)
-    plan.execute(x, y, direction=-1)
-    plan.execute(y, z, direction=1)
-    torch.cuda.synchronize()
-    err = ((z / n - x).norm() / x.norm()).item()
-    assert err < 1e-6, err
-    for b in (0, 137, batch - 1):
-        xi = x[b].reshape(-1).double().cpu().numpy()
-        want = orc.forward(xi[None], "stockham", 4, threads=4)[0]
-        assert oracle.rel_l2(y[b].reshape(-1).double().cpu().numpy(), want) <= tol(n), b
-    plan.close()
-
-
-def test_split_cluster_unaligned_falls_back(fg, orc, monkeypatch):
-    monkeypatch.setenv("FFTGEN_SPLIT", "1")
-    n = 1 << 15
-    x = seeded_batch(orc, n, 2, seed0=3)
-    dist = n + 1
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout="split", batch=2))
-    xs = np.zeros((2, dist, 2))
-    xs[:, :n, 0], xs[:, :n, 1] = x[:, 0::2], x[:, 1::2]
-    re = torch.from_numpy(xs[..., 0].astype(np.float32)).cuda()
-    im = torch.from_numpy(xs[..., 1].astype(np.float32)).cuda()
-    ore, oim = torch.zeros_like(re), torch.zeros_like(im)
-    plan.execute(re, ore, im, oim, direction=-1, dist=dist)
-    torch.cuda.synchronize()
-    got = np.empty((2, 2 * n))
-    got[:, 0::2], got[:, 1::2] = ore[:, :n].double().cpu().numpy(), oim[:, :n].double().cpu().numpy()
-    want = orc.forward(x, "stockham", 4)
-    for b in range(2):
-        assert oracle.rel_l2(got[b], want[b]) <= tol(n)
     plan.close()

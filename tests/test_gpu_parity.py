@@ -62,10 +62,10 @@ def from_device(bufs, layout, n):
     return out
 
 
-def run(n, layout, direction, x, dist=None, radix=2):
+def run(n, layout, direction, x, dist=None, radix=2, tuning=0):
     batch = x.shape[0]
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, radix=radix,
-                                                 algorithm="stockham"))
+                                                 algorithm="stockham", tuning=tuning))
     src = to_device(x, layout, dist)
     dst = tuple(torch.full_like(t, float("nan")) if t is not None else None for t in src)
     plan.execute(src[0], dst[0], src[1], dst[1], direction=direction, dist=dist or n)
@@ -276,38 +276,28 @@ def test_introspection_matches_reference_goldens(golden, golden_meta):
 
 
 @pytest.mark.parametrize("n", [256, 512, 1024, 2048, 4096, 8192, 16384])
-def test_tma_and_direct_kernels_bitwise_equal(orc, n, monkeypatch):
-    """The persistent TMA variant and the direct variant run the same passes
-    (2^14: the opt-in single-stage plane-exchange variant)."""
-    monkeypatch.setenv("FFTGEN_TMA1", "1")
+def test_tma_and_direct_kernels_bitwise_equal(orc, n):
+    """The persistent TMA variants (bulk-store epilogue or register stores) and
+    the direct variant run the same passes: bitwise equal results."""
     x = seeded_batch(orc, n, 37)
     for layout in ("interleaved", "split"):
         a = run(n, layout, -1, x)
-        monkeypatch.setenv("FFTGEN_DISABLE_TMA", "1")
-        b = run(n, layout, -1, x)
-        monkeypatch.delenv("FFTGEN_DISABLE_TMA")
-        monkeypatch.setenv("FFTGEN_DISABLE_TMA_STORE", "1")
-        c = run(n, layout, -1, x)
-        monkeypatch.delenv("FFTGEN_DISABLE_TMA_STORE")
+        b = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA)
+        c = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA_STORE)
         assert np.array_equal(a, b) and np.array_equal(a, c), layout
         check(a, orc.forward(x, "stockham", 4), n)
 
 
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
-def test_tma1_exchange_variants_bitwise_equal(orc, layout, monkeypatch):
-    """2^14 single-stage kernel: float2 first exchange through the stage
-    (FFTGEN_TMA1_EX1=1, default) and both exchanges plane-wise run the same
-    arithmetic; with and without the bulk-store epilogue."""
+def test_tma1_store_variants_bitwise_equal(orc, layout):
+    """2^14 single-stage kernel with and without the bulk-store epilogue, both
+    directions, over a batch of several transforms per persistent CTA."""
     n = 16384
-    monkeypatch.setenv("FFTGEN_TMA1", "1")
     x = seeded_batch(orc, n, 301)
     outs = []
-    for ex1 in ("1", "0"):
-        monkeypatch.setenv("FFTGEN_TMA1_EX1", ex1)
-        for store in ("0", "1"):
-            monkeypatch.setenv("FFTGEN_DISABLE_TMA_STORE", store)
-            for d in (-1, 1):
-                outs.append(run(n, layout, d, x))
+    for tuning in (0, fg.TUNE_NO_TMA_STORE):
+        for d in (-1, 1):
+            outs.append(run(n, layout, d, x, tuning=tuning))
     for i in range(2, len(outs)):
         assert np.array_equal(outs[i], outs[i % 2]), i
     check(outs[0], orc.forward(x, "stockham", 4), n)

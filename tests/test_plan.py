@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, s), s
     import paper_2308_00497_b200 as fg
     assert set(fg.ABI_SYMBOLS) == set(syms)
-    assert lib.fftgen_abi_version() == 1
+    assert lib.fftgen_abi_version() == 2
 
 
 def test_error_strings_and_config_defaults():
@@ -54,6 +54,27 @@ def test_error_strings_and_config_defaults():
     lib.fftgen_config_init(ctypes.byref(c))
     # PipelineConfig defaults (driver.hpp:26-35): Cooley-Tukey, radix 2, interleaved
     assert (c.algorithm, c.radix, c.layout, c.batch, c.device) == (0, 2, 0, 1, 0)
+    # vec None, vector_width 8, interleaved_opt off, no tile; measured-default kernels
+    assert (c.vec, c.vector_width, c.interleaved_opt, c.tile_kind) == (0, 8, 0, 0)
+    assert (c.tuning, c.cluster_size, c.host_chunk_mb) == (0, 0, 0)
+    assert ctypes.sizeof(c) == 72
+    for code, name in ((8, b"LowerError"), (9, b"BoundsError"), (10, b"GpuMapError")):
+        assert lib.fftgen_error_string(code) == name
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(vec="inner", vector_width=6), "power of two"),
+    (dict(vec="outer", vector_width=128), "capped at 64"),
+    (dict(tile=("exact", 0)), "must be positive"),
+    (dict(tile=("cache", -5)), "must be positive"),
+])
+def test_schedule_options_rejected_like_vectorize_and_tile(kw, msg):
+    """PipelineConfig.vec / vector_width / tile are validated the way the
+    reference's vectorize() and tile() validate them (transforms.cpp:85-95,
+    349-354): LowerError, raised before any device is touched."""
+    import paper_2308_00497_b200 as fg
+    with pytest.raises(fg.LowerError, match=msg):
+        fg.compile_pipeline(fg.PipelineConfig(n=64, **kw))
 
 
 @pytest.fixture(scope="module")
