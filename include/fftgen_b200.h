@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define FFTGEN_B200_ABI_VERSION 2
+#define FFTGEN_B200_ABI_VERSION 3
 
 typedef struct fftgen_plan fftgen_plan;
 
@@ -161,6 +161,43 @@ fftgen_status fftgen_interpret_f64(const fftgen_plan *plan, int direction,
  * computed in fp64 on the device, exact at quadrant multiples. */
 fftgen_status fftgen_twiddle_multiply(int direction, void *data, int64_t rows, int64_t cols, int64_t ld,
                                       int64_t row_offset, int64_t col_offset, int64_t n, void *stream);
+
+/* ---- distributed four-step: ONE n-point transform over `world` ranks ----
+ * (config C5; the reference's two-factor split formula.cpp:160-165
+ * with K = world, M = n/world).  Interleaved fp32 complex only.  Rank r holds
+ * x[r M : (r+1) M] and ends with X[r M : (r+1) M] (natural order).  Every
+ * exchange is an all-to-all of `world` CONTIGUOUS chunks of n/world^2
+ * elements (chunk q of the send buffer goes to rank q and lands as chunk r of
+ * its receive buffer: ncclSend/ncclRecv in a group, all_to_all_single):
+ *
+ *   exchange(in -> w0); butterfly(w0 -> w1); exchange(w1 -> w0);
+ *   local(w0 -> w1);    exchange(w1 -> w0);  unpack(w0 -> out)
+ *
+ * The P-point butterfly applies the twiddle diagonal D^N and stores in the
+ * per-peer chunk order (no pack copy); the local stage is the single-GPU
+ * plan of size n/world; unpack is the final stride-`world` interleave.
+ * Buffers are n/world elements, 16-byte aligned, pairwise disjoint. */
+typedef struct fftgen_dist_plan fftgen_dist_plan;
+/* PlanError: n not a power of two or n/world > 2^30; DimensionError: world not
+ * 1/2/4/8/16, rank outside [0, world), or n < 2*world^2. */
+fftgen_status fftgen_dist_plan_create(fftgen_dist_plan **out, int64_t n, int world, int rank, int device);
+fftgen_status fftgen_dist_plan_destroy(fftgen_dist_plan *plan);
+fftgen_status fftgen_dist_butterfly(const fftgen_dist_plan *plan, int direction, const void *recv, void *send,
+                                    void *stream);
+fftgen_status fftgen_dist_local(const fftgen_dist_plan *plan, int direction, const void *in, void *out,
+                                void *stream);
+fftgen_status fftgen_dist_unpack(const fftgen_dist_plan *plan, const void *recv, void *out, void *stream);
+/* All-to-all callback: `world` chunks of chunk_bytes, send -> recv, enqueued
+ * on (or ordered after) `stream`; returns 0 on success. */
+typedef int (*fftgen_exchange_fn)(void *ctx, const void *send, void *recv, size_t chunk_bytes, void *stream);
+/* The whole pipeline above on one rank with the caller's exchange. */
+fftgen_status fftgen_dist_execute(const fftgen_dist_plan *plan, int direction, const void *in, void *out,
+                                  void *work0, void *work1, fftgen_exchange_fn exchange, void *ctx, void *stream);
+/* Elements per exchange chunk (n/world^2) and the rank's block (n/world). */
+int64_t fftgen_dist_chunk_elems(const fftgen_dist_plan *plan);
+int64_t fftgen_dist_block_elems(const fftgen_dist_plan *plan);
+/* The local n/world-point plan (for describe / launch accounting). */
+const fftgen_plan *fftgen_dist_local_plan(const fftgen_dist_plan *plan);
 
 const char *fftgen_error_string(fftgen_status status);
 /* Detail message of the most recent failure on the calling thread. */

@@ -43,7 +43,9 @@ ABI_SYMBOLS = (
     "fftgen_abi_version", "fftgen_plan_radices", "fftgen_plan_num_ops", "fftgen_plan_op",
     "fftgen_plan_op_map", "fftgen_plan_pipeline_text", "fftgen_plan_num_passes", "fftgen_plan_pass",
     "fftgen_plan_describe", "fftgen_plan_launches", "fftgen_plan_scratch_bytes",
-    "fftgen_twiddle_multiply",
+    "fftgen_twiddle_multiply", "fftgen_dist_plan_create", "fftgen_dist_plan_destroy", "fftgen_dist_butterfly",
+    "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
+    "fftgen_dist_block_elems", "fftgen_dist_local_plan",
 )
 
 
@@ -111,8 +113,8 @@ def _load() -> C.CDLL:
                           "(or __graft_entry__.build()); there is no CPU fallback")
     L = C.CDLL(LIB_PATH)
     L.fftgen_abi_version.restype = C.c_int
-    if L.fftgen_abi_version() != 2:
-        raise ImportError(f"{LIB_PATH} has ABI {L.fftgen_abi_version()}, this binding needs 2: rebuild it")
+    if L.fftgen_abi_version() != 3:
+        raise ImportError(f"{LIB_PATH} has ABI {L.fftgen_abi_version()}, this binding needs 3: rebuild it")
     vp, i64, i64p = C.c_void_p, C.c_int64, C.POINTER(C.c_int64)
     L.fftgen_config_init.argtypes = [C.POINTER(_Config)]
     L.fftgen_config_init.restype = None
@@ -136,6 +138,18 @@ def _load() -> C.CDLL:
     L.fftgen_plan_scratch_bytes.argtypes = [vp]
     L.fftgen_plan_scratch_bytes.restype = C.c_size_t
     L.fftgen_twiddle_multiply.argtypes = [C.c_int, vp, i64, i64, i64, i64, i64, i64, vp]
+    L.fftgen_dist_plan_create.argtypes = [C.POINTER(vp), i64, C.c_int, C.c_int, C.c_int]
+    L.fftgen_dist_plan_destroy.argtypes = [vp]
+    L.fftgen_dist_butterfly.argtypes = [vp, C.c_int, vp, vp, vp]
+    L.fftgen_dist_local.argtypes = [vp, C.c_int, vp, vp, vp]
+    L.fftgen_dist_unpack.argtypes = [vp, vp, vp, vp]
+    L.fftgen_dist_execute.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp]
+    L.fftgen_dist_chunk_elems.argtypes = [vp]
+    L.fftgen_dist_chunk_elems.restype = i64
+    L.fftgen_dist_block_elems.argtypes = [vp]
+    L.fftgen_dist_block_elems.restype = i64
+    L.fftgen_dist_local_plan.argtypes = [vp]
+    L.fftgen_dist_local_plan.restype = vp
     return L
 
 
@@ -397,6 +411,72 @@ def twiddle_multiply(block, row_offset: int, col_offset: int, n: int, direction:
         stream = stream.cuda_stream
     _check(lib.fftgen_twiddle_multiply(direction, _ptr(block), rows, cols, ld, row_offset, col_offset, n,
                                        int(stream)))
+
+
+class DistPlan:
+    """One rank's share of a distributed n-point transform (fftgen_dist_plan):
+    the P-point butterfly + D^N twiddle, the local n/world-point plan and the
+    stride-world unpack (include/fftgen_b200.h, "distributed four-step").
+    Buffers are CUDA complex64 (or float32 (..., 2)) blocks of n/world
+    elements; the exchanges between the stages are the caller's
+    (distributed.DistributedFFT)."""
+
+    def __init__(self, n: int, world: int, rank: int, device: int = 0):
+        h = C.c_void_p()
+        _check(lib.fftgen_dist_plan_create(C.byref(h), int(n), int(world), int(rank), int(device)))
+        self._h = h
+        self.n, self.world, self.rank, self.device = int(n), int(world), int(rank), int(device)
+        self.block = int(lib.fftgen_dist_block_elems(h))
+        self.chunk = int(lib.fftgen_dist_chunk_elems(h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib.fftgen_dist_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _buf(self, name, a):
+        import torch
+        if not hasattr(a, "data_ptr") or a.device.type != "cuda" or a.device.index != self.device:
+            raise ExecError(f"{name} must be a CUDA tensor on cuda:{self.device}")
+        if a.dtype not in (torch.complex64, torch.float32) or not a.is_contiguous():
+            raise ExecError(f"{name} must be a contiguous complex64 / float32 tensor")
+        elems = a.numel() if a.dtype == torch.complex64 else a.numel() // 2
+        if elems != self.block:
+            raise DimensionError(f"{name} holds {elems} elements, the rank's block is {self.block}")
+        return _ptr(a)
+
+    @staticmethod
+    def _stream(stream, dev):
+        import torch
+        if stream is None:
+            return torch.cuda.current_stream(dev).cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def butterfly(self, recv, send, direction: int = FORWARD, stream=None) -> None:
+        _check(lib.fftgen_dist_butterfly(self._h, direction, self._buf("recv", recv), self._buf("send", send),
+                                         self._stream(stream, self.device)))
+
+    def local(self, inp, out, direction: int = FORWARD, stream=None) -> None:
+        _check(lib.fftgen_dist_local(self._h, direction, self._buf("in", inp), self._buf("out", out),
+                                     self._stream(stream, self.device)))
+
+    def unpack(self, recv, out, stream=None) -> None:
+        _check(lib.fftgen_dist_unpack(self._h, self._buf("recv", recv), self._buf("out", out),
+                                      self._stream(stream, self.device)))
+
+    def describe_local(self) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        _check(lib.fftgen_plan_describe(lib.fftgen_dist_local_plan(self._h), buf, len(buf)))
+        return buf.value.decode()
+
+    def local_launches(self) -> int:
+        return int(lib.fftgen_plan_launches(lib.fftgen_dist_local_plan(self._h)))
 
 
 def flops(n: int, batch: int = 1) -> float:

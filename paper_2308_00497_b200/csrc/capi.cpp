@@ -78,6 +78,8 @@ template <class F> fftgen_status guarded(F &&f) {
 }
 }  // namespace
 
+void fftgen_b200::set_last_error(const std::string &msg) { g_last_error = msg; }
+
 struct fftgen_plan {
   fftgen_config cfg{};
   ExecPlan ex;

@@ -109,6 +109,14 @@ cudaError_t gen_twiddles(float2 *out, int64_t rows, int64_t cols, int64_t row_sc
 cudaError_t twiddle_block(float2 *data, int64_t rows, int64_t cols, int64_t ld, int64_t row_offset,
                           int64_t col_offset, int64_t n, int dir, cudaStream_t s);
 
+// distributed four-step stages (dist.cu): P-point butterfly + D^N twiddle over
+// P chunks of l1 elements (a0 = rank * l1), and the stride-P output interleave
+bool dist_world_supported(int p);
+cudaError_t dist_gen_tables(float2 *tlo, float2 *thi, int log2n, int h, cudaStream_t s);
+cudaError_t dist_butterfly(int p, int dir, const float2 *in, float2 *out, int64_t l1, int64_t a0, const float2 *tlo,
+                           const float2 *thi, int h, int log2n, cudaStream_t s);
+cudaError_t dist_unpack(int p, const float2 *in, float2 *out, int64_t l1, cudaStream_t s);
+
 cudaError_t convert_f64_to_f32(const double *in, float *out, int64_t count, cudaStream_t s);
 cudaError_t convert_f32_to_f64(const float *in, double *out, int64_t count, cudaStream_t s);
 cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, int64_t istride,

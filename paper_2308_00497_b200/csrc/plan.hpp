@@ -25,6 +25,9 @@ struct FuseError : std::runtime_error { using std::runtime_error::runtime_error;
 struct ExecError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct LowerError : std::runtime_error { using std::runtime_error::runtime_error; };
 
+// Sets the calling thread's fftgen_last_error() text (capi.cpp).
+void set_last_error(const std::string &msg);
+
 // The reference's CPU schedule options (PipelineConfig.vec / vector_width /
 // tile), validated like vectorize() / tile() (transforms.cpp:85-95, 351-354).
 void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_value);

@@ -4,32 +4,37 @@
   batch ranges; every rank owns its own plan and twiddle tables and there is
   NO data-path collective (weak scaling).
 * DistributedFFT  -- one very large transform (config C5, N = 2^30) block
-  distributed over P ranks: the reference's Eq. 1 split
-  DFT_N = (DFT_N1 (x) I) D^N (I (x) DFT_N2) Pi^N_N1 (formula.hpp:102-106) run
-  as a distributed four-step with three all-to-all exchanges (NCCL over
-  NVLink on GPUs; any torch.distributed backend works):
+  distributed over P ranks (rank r holds x[r M : (r+1) M], M = N/P).  The
+  reference's two-factor split (formula.cpp:160-165, Eq. 1) with K = P:
 
-    rank r holds x[r M : (r+1) M], M = N/P, viewed as rows a of X[a][c] (N1 x N2)
-    1. all-to-all: rank r gets columns c in [r N2/P, (r+1) N2/P) of every row
-    2. N1-point FFTs down those columns            (local batched plan)
-    3. twiddle D^N: F[c][k1] *= w_N^{c k1}          (fftgen_twiddle_multiply)
-    4. all-to-all: rank r gets k1 in [r N1/P, (r+1) N1/P) for every c
-    5. N2-point FFTs along c                        (local batched plan)
-    6. all-to-all back to natural order: rank r ends with X^[r M : (r+1) M]
+    X[k_b + P k_a] = sum_a w_M^{a k_a} (w_N^{a k_b} sum_r x[a + M r] w_P^{r k_b})
 
-  Packing into per-peer contiguous chunks and the local transposes are
-  strided tensor copies; the FFT passes are the sm_100a kernels.  The local
-  FFT and the twiddle are injectable so the exchange logic is testable on
-  CPU with the gloo backend (tests/test_distributed.py) against the oracle.
+  runs as three all-to-alls of CONTIGUOUS equal chunks (NCCL grouped
+  send/recv through torch.distributed.all_to_all_single; no pack or
+  transpose copy on either side) around three sm_100a stages of the C ABI
+  (fftgen_dist_*, csrc/dist.cu):
+
+    1. exchange   the input block as-is            -> R1[r][j] = x[r M + q L1 + j]
+    2. butterfly  P-point DFT over r + D^N twiddle, stored per destination rank
+    3. exchange                                    -> R2 = the natural M-point input
+    4. local      the single-GPU M-point plan (K2 / K5 / K3)
+    5. exchange   contiguous output chunks         -> R3[q'][j] = X[s M + P j + q']
+    6. unpack     out[P j + q'] = R3[q'][j]  (the stride-P interleave of Pi^N_P)
+
+  L1 = N/P^2.  The stages are injectable so the exchange logic is testable on
+  CPU with gloo (tests/test_distributed.py, a numpy restatement of the three
+  stages) and `EmulatedDistributedFFT` runs P ranks in lockstep on ONE GPU
+  with the real kernels, the exchanges being device copies of the same
+  chunks (tests/test_gpu_distributed.py).
 """
 from __future__ import annotations
 
-from typing import Callable, Optional
+from typing import Optional, Sequence
 
 import torch
 import torch.distributed as dist
 
-from . import FORWARD, PipelineConfig, compile_pipeline, twiddle_multiply
+from . import FORWARD, DistPlan, PipelineConfig, compile_pipeline
 
 
 def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -66,78 +71,112 @@ class BatchShardedFFT:
             self.plan.execute(in0, out0, in1, out1, direction=direction, stream=stream)
 
 
+def check_geometry(n: int, world: int) -> None:
+    if n < 4 or n & (n - 1):
+        raise ValueError(f"n must be a power of two >= 4, got {n}")
+    if world not in (1, 2, 4, 8, 16):
+        raise ValueError(f"world size must be 1, 2, 4, 8 or 16, got {world}")
+    if n < 2 * world * world:
+        raise ValueError(f"n = {n} is below 2 * world^2 = {2 * world * world}")
+
+
 class DistributedFFT:
-    """One N-point transform block-distributed over the process group."""
+    """One N-point transform block-distributed over the process group.
 
-    def __init__(self, n: int, group=None, n1: Optional[int] = None, device: Optional[int] = None,
-                 local_fft: Optional[Callable] = None, twiddle: Optional[Callable] = None):
+    `stages` supplies butterfly(recv, send, direction), local(inp, out,
+    direction) and unpack(recv, out) on this rank's blocks; the default is the
+    sm_100a DistPlan.  `exchange(send, recv)` defaults to
+    all_to_all_single over the group (a copy when the world is 1)."""
+
+    def __init__(self, n: int, group=None, device: Optional[int] = None, rank: Optional[int] = None,
+                 world: Optional[int] = None, stages=None):
+        r, w = _rank_world(group)
         self.group = group
-        self.rank, self.world = _rank_world(group)
-        if n < 4 or n & (n - 1):
-            raise ValueError(f"n must be a power of two >= 4, got {n}")
-        log2 = n.bit_length() - 1
+        self.rank = r if rank is None else rank
+        self.world = w if world is None else world
+        check_geometry(n, self.world)
         self.n = n
-        self.n1 = n1 or 1 << ((log2 + 1) // 2)
-        self.n2 = n // self.n1
-        P = self.world
-        if self.n1 * self.n2 != n or self.n1 % P or self.n2 % P:
-            raise ValueError(f"world size {P} must divide both factors {self.n1} x {self.n2}")
-        self.m = n // P
-        self._plans: dict = {}
-        self.device = device
-        self.local_fft = local_fft or self._gpu_fft
-        self.twiddle = twiddle or (lambda blk, ro, co, nn, d: twiddle_multiply(blk, ro, co, nn, d))
+        self.m = n // self.world
+        self.l1 = self.m // self.world
+        if stages is None:
+            if device is None:
+                device = torch.cuda.current_device()
+            stages = DistPlan(n, self.world, self.rank, device)
+        self.stages = stages
+        self._work: dict = {}
 
-    # ---- default GPU building blocks --------------------------------------
-    def _gpu_fft(self, x: torch.Tensor, size: int, direction: int) -> torch.Tensor:
-        """Batched contiguous complex64 FFTs of `size` along the last axis."""
-        batch = x.shape[0]
-        key = (size, batch)
-        if key not in self._plans:
-            dev = x.device.index if self.device is None else self.device
-            self._plans[key] = compile_pipeline(PipelineConfig(n=size, batch=batch, layout="interleaved",
-                                                               device=dev, algorithm="stockham"))
-        out = torch.empty_like(x)
-        self._plans[key].execute(x, out, direction=direction)
-        return out
-
-    def _a2a(self, send: torch.Tensor) -> torch.Tensor:
-        recv = torch.empty_like(send)
-        if self.world == 1:
+    def exchange(self, send: torch.Tensor, recv: torch.Tensor) -> None:
+        """All-to-all of `world` contiguous chunks: send chunk q -> rank q, recv chunk r <- rank r."""
+        if self.world == 1 and not (dist.is_available() and dist.is_initialized()):
             recv.copy_(send)
         else:
             dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send), group=self.group)
-        return recv
 
-    # ---- the distributed four-step ----------------------------------------
-    def execute(self, x_local: torch.Tensor, direction: int = FORWARD) -> torch.Tensor:
+    def workspace(self, like: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+        key = (like.device, like.dtype)
+        if key not in self._work:
+            self._work[key] = (torch.empty(self.m, dtype=like.dtype, device=like.device),
+                               torch.empty(self.m, dtype=like.dtype, device=like.device))
+        return self._work[key]
+
+    def execute(self, x_local: torch.Tensor, direction: int = FORWARD,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """x_local: complex64 (M,) = x[rank*M : (rank+1)*M]; returns X^ of the same block."""
-        P, r, N1, N2 = self.world, self.rank, self.n1, self.n2
         if x_local.numel() != self.m or x_local.dtype != torch.complex64:
-            raise ValueError(f"expected complex64 block of {self.m} elements")
-        if P == 1 and self.local_fft == self._gpu_fft:
-            # nothing to exchange: the single-GPU K3 plan is the whole transform
-            return self.local_fft(x_local.reshape(1, -1), self.n, direction).reshape(-1)
-        X = x_local.reshape(N1 // P, N2)
-        # 1. columns to their owners: chunk q = rows(r) x cols(q)
-        R1 = self._a2a(X.reshape(N1 // P, P, N2 // P).transpose(0, 1).contiguous())
-        del X
-        Z = R1.reshape(N1, N2 // P).t().contiguous()          # (N2/P, N1): column c_loc contiguous
-        del R1
-        # 2. N1-point FFTs along a
-        F = self.local_fft(Z, N1, direction)                   # F[c_loc][k1]
-        del Z
-        # 3. twiddle diagonal: c = r N2/P + c_loc, k1
-        self.twiddle(F, r * (N2 // P), 0, self.n, direction)
-        # 4. k1 ranges to their owners
-        R2 = self._a2a(F.reshape(N2 // P, P, N1 // P).transpose(0, 1).contiguous())
-        del F
-        H = R2.reshape(N2, N1 // P).t().contiguous()          # (N1/P, N2): row k1_loc contiguous
-        del R2
-        # 5. N2-point FFTs along c
-        O = self.local_fft(H, N2, direction)                   # O[k1_loc][k2]
-        del H
-        # 6. natural order: k = k1 + N1 k2, rank s owns k2 in [s N2/P, (s+1) N2/P)
-        R3 = self._a2a(O.reshape(N1 // P, P, N2 // P).transpose(0, 1).contiguous())
-        del O
-        return R3.reshape(N1, N2 // P).t().contiguous().reshape(-1)
+            raise ValueError(f"expected a complex64 block of {self.m} elements")
+        x_local = x_local.reshape(-1)
+        w0, w1 = self.workspace(x_local)
+        if out is None:
+            out = torch.empty_like(x_local)
+        self.exchange(x_local, w0)
+        self.stages.butterfly(w0, w1, direction)
+        self.exchange(w1, w0)
+        self.stages.local(w0, w1, direction)
+        self.exchange(w1, w0)
+        self.stages.unpack(w0, out)
+        return out
+
+
+def emulated_exchange(sends: Sequence[torch.Tensor], recvs: Sequence[torch.Tensor], chunk: int) -> None:
+    """The all-to-all of P ranks held by one process: chunk q of rank r's send
+    buffer lands as chunk r of rank q's receive buffer (what NCCL moves)."""
+    P = len(sends)
+    for r in range(P):
+        for q in range(P):
+            recvs[q][r * chunk:(r + 1) * chunk].copy_(sends[r][q * chunk:(q + 1) * chunk])
+
+
+class EmulatedDistributedFFT:
+    """P ranks of the distributed four-step in lockstep on one device: the
+    real per-rank stages (kernels, twiddle offsets, chunk layouts), with the
+    three all-to-alls as device copies.  Tests the composition the NCCL path
+    runs, on one GPU."""
+
+    def __init__(self, n: int, world: int, device: Optional[int] = None, stages_factory=None):
+        check_geometry(n, world)
+        self.n, self.world = n, world
+        self.m = n // world
+        self.l1 = self.m // world
+        if stages_factory is None:
+            dev = torch.cuda.current_device() if device is None else device
+            stages_factory = lambda r: DistPlan(n, world, r, dev)  # noqa: E731
+        self.stages = [stages_factory(r) for r in range(world)]
+
+    def execute(self, blocks: Sequence[torch.Tensor], direction: int = FORWARD) -> list[torch.Tensor]:
+        P = self.world
+        if len(blocks) != P or any(b.numel() != self.m or b.dtype != torch.complex64 for b in blocks):
+            raise ValueError(f"expected {P} complex64 blocks of {self.m} elements")
+        blocks = [b.reshape(-1) for b in blocks]
+        w0 = [torch.empty_like(b) for b in blocks]
+        w1 = [torch.empty_like(b) for b in blocks]
+        out = [torch.empty_like(b) for b in blocks]
+        emulated_exchange(blocks, w0, self.l1)
+        for r in range(P):
+            self.stages[r].butterfly(w0[r], w1[r], direction)
+        emulated_exchange(w1, w0, self.l1)
+        for r in range(P):
+            self.stages[r].local(w0[r], w1[r], direction)
+        emulated_exchange(w1, w0, self.l1)
+        for r in range(P):
+            self.stages[r].unpack(w0[r], out[r])
+        return out

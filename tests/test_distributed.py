@@ -1,10 +1,12 @@
-"""Multi-process paths on CPU (gloo, world size 2 and 4) and on one GPU (NCCL,
-world size 1).
+"""Multi-process paths on CPU: gloo at world size 2 and 4, plus an in-process
+emulation of P = 1..16 ranks.
 
-The CPU tests exercise the host logic of paper_2308_00497_b200.distributed --
-batch shard ranges and the three all-to-all exchanges of the distributed
-four-step -- with the pinned CPU oracle injected as the local FFT (product
-code never imports the oracle), against the oracle's full transform.
+They exercise the host logic of paper_2308_00497_b200.distributed -- batch
+shard ranges and the three contiguous-chunk all-to-alls of the distributed
+four-step -- with a numpy restatement of the three per-rank stages (the local
+transform by the pinned oracle; product code never imports the oracle),
+against the oracle's full transform.  The same composition with the sm_100a
+stages runs on one GPU in tests/test_gpu_distributed.py.
 """
 import os
 import socket
@@ -42,34 +44,71 @@ def test_shard_range_partitions_exactly():
         shard_range(10, 2, 2)
 
 
-# ---------------------------------------------------------------- gloo workers
-def _oracle_fft(x: torch.Tensor, size: int, direction: int) -> torch.Tensor:
-    """Test-side local FFT: the pinned oracle on a batch of complex rows."""
+# ------------------------------------------------- numpy restatement of the stages
+class NumpyStages:
+    """Test-side restatement of the three per-rank stages of csrc/dist.cu on
+    CPU complex64 tensors (the butterfly's P-point DFT and w_N twiddle in fp64,
+    the local M-point transform by the pinned oracle)."""
+
+    def __init__(self, n, world, rank):
+        self.n, self.P, self.q = n, world, rank
+        self.m = n // world
+        self.l1 = self.m // world
+
+    def butterfly(self, recv, send, direction):
+        P, l1, n = self.P, self.l1, self.n
+        r1 = recv.numpy().astype(np.complex128).reshape(P, l1)
+        sgn = 1.0 if direction > 0 else -1.0
+        kb = np.arange(P)
+        dftP = np.exp(sgn * 2j * np.pi * np.outer(kb, kb) / P)          # [k_b][r]
+        y = dftP @ r1                                                     # [k_b][j]
+        a = self.q * l1 + np.arange(l1)
+        y *= np.exp(sgn * 2j * np.pi * ((np.outer(kb, a)) % n) / n)
+        send.copy_(torch.from_numpy(y.reshape(-1).astype(np.complex64)))
+
+    def local(self, inp, out, direction):
+        orc = oracle.Oracle()
+        inter = oracle.as_interleaved(inp.numpy().astype(np.complex128)[None, :])
+        y = orc.forward(inter, "stockham", 4, inverse=direction > 0)
+        out.copy_(torch.from_numpy(oracle.as_complex(y)[0].astype(np.complex64)))
+
+    def unpack(self, recv, out):
+        out.copy_(recv.reshape(self.P, self.l1).t().reshape(-1))
+
+
+def _want(n, direction):
     orc = oracle.Oracle()
-    inter = oracle.as_interleaved(x.numpy().astype(np.complex128))
-    y = orc.forward(inter, "stockham", 4, inverse=direction > 0)
-    return torch.from_numpy(oracle.as_complex(y).astype(np.complex64))
+    x = orc.seeded_input(n, 1).astype(np.float32).astype(np.float64)
+    z = oracle.as_complex(x).astype(np.complex64)
+    want = oracle.as_complex(orc.forward(x, "stockham", 4, inverse=direction > 0))
+    return z, want
 
 
-def _np_twiddle(blk: torch.Tensor, ro: int, co: int, n: int, direction: int) -> None:
-    r = np.arange(blk.shape[0], dtype=np.int64)[:, None] + ro
-    c = np.arange(blk.shape[1], dtype=np.int64)[None, :] + co
-    e = (r * c) % n
-    w = np.exp(direction * 2j * np.pi * e / n)
-    blk.copy_(torch.from_numpy((blk.numpy().astype(np.complex128) * w).astype(np.complex64)))
+@pytest.mark.parametrize("world,n", [(1, 1 << 8), (2, 1 << 10), (4, 1 << 12), (8, 1 << 12), (16, 1 << 12)])
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_emulated_composition_numpy_stages(world, n, direction):
+    """The exchange pattern + stage algebra of the distributed four-step, all
+    P ranks in one process (emulated_exchange), against the oracle."""
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    z, want = _want(n, direction)
+    e = EmulatedDistributedFFT(n, world, stages_factory=lambda r: NumpyStages(n, world, r))
+    m = n // world
+    outs = e.execute([torch.from_numpy(z[r * m:(r + 1) * m].copy()) for r in range(world)], direction)
+    got = torch.cat(outs).numpy()
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 1e-5 * np.log2(n), err
 
 
+# ---------------------------------------------------------------- gloo workers
 def _dist_worker(rank, world, port, n, direction, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2308_00497_b200.distributed import DistributedFFT
-        orc = oracle.Oracle()
-        x = orc.seeded_input(n, 1).astype(np.float32).astype(np.float64)
-        z = oracle.as_complex(x).astype(np.complex64)
+        z, _ = _want(n, direction)
         m = n // world
-        d = DistributedFFT(n, local_fft=_oracle_fft, twiddle=_np_twiddle)
+        d = DistributedFFT(n, stages=NumpyStages(n, world, rank))
         local = torch.from_numpy(z[rank * m:(rank + 1) * m].copy())
         out = d.execute(local, direction=direction)
         gathered = [torch.empty_like(out) for _ in range(world)]
@@ -83,6 +122,7 @@ def _dist_worker(rank, world, port, n, direction, q):
 @pytest.mark.parametrize("world,n", [(2, 1 << 10), (4, 1 << 12), (2, 1 << 13)])
 @pytest.mark.parametrize("direction", [-1, 1])
 def test_distributed_four_step_gloo(world, n, direction):
+    """Real process group (gloo all_to_all_single), world 2 / 4."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
@@ -93,50 +133,16 @@ def test_distributed_four_step_gloo(world, n, direction):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    orc = oracle.Oracle()
-    x = orc.seeded_input(n, 1).astype(np.float32).astype(np.float64)
-    want = oracle.as_complex(orc.forward(x, "stockham", 4, inverse=direction > 0))
+    _, want = _want(n, direction)
     err = np.linalg.norm(got - want) / np.linalg.norm(want)
     assert err < 1e-5 * np.log2(n), err
 
 
 def test_distributed_rejects_bad_geometry():
-    from paper_2308_00497_b200.distributed import DistributedFFT
+    from paper_2308_00497_b200.distributed import DistributedFFT, EmulatedDistributedFFT
     with pytest.raises(ValueError):
-        DistributedFFT(1000)
+        DistributedFFT(1000, world=1, rank=0, stages=object())
     with pytest.raises(ValueError):
-        DistributedFFT(1 << 10, n1=3)
-
-
-# ---------------------------------------------------------------- one GPU, NCCL
-def _nccl_single(n):
-    from paper_2308_00497_b200.distributed import BatchShardedFFT, DistributedFFT
-    import paper_2308_00497_b200 as fg
-    g = torch.Generator(device="cuda").manual_seed(5)
-    x = torch.complex(torch.rand(n, device="cuda", generator=g) * 2 - 1,
-                      torch.rand(n, device="cuda", generator=g) * 2 - 1)
-    d = DistributedFFT(n)
-    y = d.execute(x)
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=1))
-    ref = torch.empty_like(x)
-    plan.execute(torch.view_as_real(x), torch.view_as_real(ref))
-    torch.cuda.synchronize()
-    rel = (torch.linalg.norm(y - ref) / torch.linalg.norm(ref)).item()
-    back = d.execute(y, direction=fg.INVERSE) / n
-    rt = (torch.linalg.norm(back - x) / torch.linalg.norm(x)).item()
-    s = BatchShardedFFT(1024, 10, layout="interleaved")
-    assert (s.start, s.count) == (0, 10)
-    return rel, rt
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("l2", [20, 24])
-def test_distributed_four_step_nccl_world1(l2):
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ["MASTER_PORT"] = str(free_port())
-    dist.init_process_group("nccl", rank=0, world_size=1)
-    try:
-        rel, rt = _nccl_single(1 << l2)
-        assert rel < 5e-6 and rt < 1e-6, (rel, rt)
-    finally:
-        dist.destroy_process_group()
+        EmulatedDistributedFFT(1 << 10, 3, stages_factory=lambda r: None)
+    with pytest.raises(ValueError):
+        EmulatedDistributedFFT(64, 8, stages_factory=lambda r: None)   # n < 2 world^2

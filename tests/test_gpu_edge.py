@@ -185,7 +185,7 @@ def test_partial_overlap_rejected_exact_in_place_accepted(fg, orc):
     storage (in1 = in0 + n, dist = 2n) in place is two disjoint strided sets."""
     n, batch = 1024, 3
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch))
-    buf = rand((batch * n + 64, 2), 4)
+    buf = rand(((batch + 1) * n + 64, 2), 4)
     with pytest.raises(fg.ExecError, match="overlaps"):
         plan.execute(buf[:batch * n], buf[32:32 + batch * n])       # shifted by 32 elements
     with pytest.raises(fg.ExecError, match="overlaps"):

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, s), s
     import paper_2308_00497_b200 as fg
     assert set(fg.ABI_SYMBOLS) == set(syms)
-    assert lib.fftgen_abi_version() == 2
+    assert lib.fftgen_abi_version() == 3
 
 
 def test_error_strings_and_config_defaults():
