@@ -4,8 +4,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
+`--gpus N` without a torchrun environment re-executes itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU); under
+torchrun WORLD_SIZE must equal N.
+
 Workload (BASELINE.json configs[1]): N=4096, batch=65536 per GPU, split
-re/im layout, forward.  A step is one execute of the whole batch.  Inputs
+re/im layout, forward, on the reference's own inputs (seeded_input,
+verify.cpp:55-78, transform b of rank r seeded 1 + r*batch + b) generated on
+the device.  A step is one execute of the whole batch.  Inputs
 (2 GiB) and outputs (2 GiB) per GPU are far larger than the 126 MB L2, so no
 flush is needed between steps.  Multi-GPU: the batch shards with no
 communication (weak scaling, per-GPU batch fixed), timed per rank with CUDA
@@ -50,19 +56,68 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON)")
     ap.add_argument("--workload", choices=["batched", "distributed"], default="batched",
                     help="distributed: one N-point transform over all ranks (config C5, e.g. --n 1073741824)")
+    ap.add_argument("--launch-selftest", action="store_true",
+                    help="CPU check of the rank launcher: gloo ranks all-reduce MAX of their rank")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(a) -> bool:
+    """`--gpus N` outside torchrun: re-exec this command as N torchrun ranks
+    (the driver's own launch line).  Returns True when this process only
+    launched the ranks."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != a.gpus:
+            sys.exit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={env_world}")
+        return False
+    if a.gpus <= 1:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        sys.exit(rc)
+    return True
+
+
+def launch_selftest(a):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank), 1.0])
+    if world > 1:
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+    if rank == 0:
+        print(json.dumps({"selftest": "launch", "n_gpus": world, "max_rank": int(t[0]), "ranks": int(t[1]),
+                          "gpus_flag": a.gpus}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def gflop(n: int, batch: int) -> float:
     return 5.0 * n * math.log2(n) * batch / 1e9
 
 
-def workload(a) -> dict:
+def workload(a, world: int = 1) -> dict:
     return {"workload": f"c2c fp32 FFT N={a.n} batch={a.batch}/GPU {a.layout} {a.direction}",
-            "n": a.n, "batch_per_gpu": a.batch, "layout": a.layout, "direction": a.direction,
+            "n": a.n, "batch_per_gpu": a.batch, "global_batch": a.batch * world, "layout": a.layout,
+            "direction": a.direction,
             "l2": "inputs+outputs (16N*batch = %.1f GiB/GPU) exceed the 126 MB L2; no flush"
                   % (16 * a.n * a.batch / 2 ** 30),
-            "parallelism": f"batch-sharded x{a.gpus}, no collective"}
+            "parallelism": f"batch-sharded over {world} rank(s), no collective"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -225,13 +280,13 @@ def run_ours(a):
     direction = fg.FORWARD if a.direction == "forward" else fg.INVERSE
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=a.layout, batch=batch, device=local,
                                                  algorithm="stockham"))
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # the reference's inputs (seeded_input, verify.cpp:55-78), generated on the device
+    seed0 = 1 + rank * batch
     if a.layout == "split":
-        in0 = torch.rand(batch, n, device=dev, generator=g) * 2 - 1
-        in1 = torch.rand(batch, n, device=dev, generator=g) * 2 - 1
+        in0, in1 = fg.seeded_input(n, batch, "split", seed0=seed0, device=local)
         out0, out1 = torch.empty_like(in0), torch.empty_like(in1)
     else:
-        in0 = torch.rand(batch, n, 2, device=dev, generator=g) * 2 - 1
+        in0 = fg.seeded_input(n, batch, "interleaved", seed0=seed0, device=local)
         in1 = out1 = None
         out0 = torch.empty_like(in0)
     stream = torch.cuda.current_stream(dev)
@@ -335,8 +390,10 @@ def run_ours(a):
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic: uniform [-1,1) re/im generated on device (torch.rand), resident in HBM",
-        "config": workload(a),
+        "data": "synthetic: the reference's seeded_input (verify.cpp:55-78, splitmix64 uniform [-1,1) re/im), "
+                "transform b of rank r seeded 1 + r*batch + b, generated on the device "
+                "(fftgen_seeded_input), resident in HBM",
+        "config": workload(a, world),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "kernel": next((w for w in plan.describe().split() if "kernel<" in w), "?"),
@@ -357,6 +414,12 @@ def run_ours(a):
 
 
 def run_reference(a):
+    """The reference arm: the unmodified reference (oracle/_ref, compiled from
+    /root/reference's own sources) through its execute API
+    (compile_pipeline + interpret, fp64), batch-parallel on all host cores.
+    Each step is a MEASURED pass over a fixed sample of the workload's
+    transforms (sample_transforms, sized from a calibration pass so a step
+    takes ~2 s and the whole --steps/--warmup run a few minutes)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
@@ -365,96 +428,219 @@ def run_reference(a):
     if not os.path.exists(oracle.REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfftgen_ref.so not built"}))
         return None
-    # each step = a bounded sample of the workload (the full 65536-transform
-    # batch would take ~1 min per step on the interpreter)
-    per_step = max(1.0, a.cpu_seconds / max(1, a.steps + a.warmup))
+    if a.n > 65536:
+        print(json.dumps({"impl": "reference", "unavailable": f"N={a.n}: the reference interpreter needs ~46 s "
+                                                              "and 13 GB per 2^24 transform (SURVEY 6)"}))
+        return None
+    ref = oracle.Ref()
+    alg, radix, lay = "stockham", 4, a.layout  # the reference's best interpreter config at N=4096
+    ref.compile(a.n, alg, radix, lay)
+    chunk = max(threads * 4, 8)
+    x = np.stack([ref.seeded_input(a.n, 1 + b) for b in range(chunk)])
+    if lay == "split":
+        x = oracle.relayout_to_split(x)
+    x = x.astype(np.float32).astype(np.float64)
+    # calibration: transforms per step for ~step_s seconds
+    step_s = max(0.5, min(2.5, 120.0 / max(1, a.steps + a.warmup)))
+    t0 = time.perf_counter()
+    ref.forward(x, alg, radix, lay, threads=threads)
+    rate = chunk / (time.perf_counter() - t0)
+    calls = max(1, int(round(rate * step_s / chunk)))
+    sample = calls * chunk
+
+    def step():
+        for _ in range(calls):
+            ref.forward(x, alg, radix, lay, threads=threads)
+
     for _ in range(a.warmup):
-        cpu_reference_rate(a, per_step / 2, threads, with_aot=False)
-    vals, samples = [], []
+        step()
+    times = []
     for _ in range(a.steps):
-        r = cpu_reference_rate(a, per_step, threads, with_aot=False)
-        vals.append(r["value"])
-        samples.append(r["sample"])
-    v = float(np.mean(vals))
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = float(np.mean(times)) * 1e3
+    v = gflop(a.n, sample) / (ms / 1e3)
     # the reference's ahead-of-time C path on the same workload, reported beside it once
     aot = None
-    if a.layout == "split":
-        ref_x = None
-        try:
-            ref = oracle.Ref()
-            ref_x = oracle.relayout_to_split(np.stack([ref.seeded_input(a.n, 1 + b) for b in range(64)]))
-            ref_x = ref_x.astype(np.float32).astype(np.float64)
-        except Exception:
-            pass
-        aot = cpu_aot_rate(a, ref_x, 4.0, threads)
+    if lay == "split":
+        aot = cpu_aot_rate(a, x, 4.0, threads)
+    cfg = workload(a, 1)
+    cfg["sample_transforms"] = sample
+    cfg["parallelism"] = f"host CPU, {threads} threads, one transform per thread"
     line = {
-        "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": a.gpus, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": round(gflop(a.n, a.batch) / v * 1e3, 1),
+        "metric": METRIC, "value": round(v, 4), "unit": "GFLOP/s", "n_gpus": 0, "launched_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: fp32-rounded seeded_input (verify.cpp:69-78)", "config": workload(a),
+        "data": "synthetic: fp32-rounded seeded_input (verify.cpp:55-78)", "config": cfg,
         "impl": "reference",
         "cpu_baseline": {"value": round(v, 4), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-                         "sample": samples[-1], "aot_emit_c": aot},
+                         "sample": f"{sample} transforms of N={a.n} {lay} per step (seeds 1..{chunk}, repeated), "
+                                   f"compile_pipeline(stockham, radix 4)+interpret fp64, measured per step",
+                         "aot_emit_c": aot},
         "e2e": {"value": round(v, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference = unmodified fftgen compile_pipeline+interpret (oracle/_ref), batch-parallel "
-                "one transform per thread; ms_per_step extrapolated to the full batch",
+        "note": "reference = unmodified fftgen compile_pipeline+interpret (oracle/_ref) on the host cores, "
+                "batch-parallel one transform per thread; each step is a measured pass over "
+                "config.sample_transforms transforms of the workload (n_gpus 0: no GPU on this path)",
     }
     print(json.dumps(line), flush=True)
     return line
 
 
-def run_distributed(a):
-    """Config C5: one N-point transform block-distributed over all ranks,
-    three NCCL all-to-alls (paper_2308_00497_b200.distributed)."""
+def a2a_probe(m: int, dev, world: int, reps: int = 10) -> dict:
+    """all_to_all_single (NCCL grouped send/recv) of an m-element complex64
+    block per rank: the exchange roofline of the distributed four-step."""
     import torch
     import torch.distributed as dist
+    send = torch.empty(m, dtype=torch.complex64, device=dev).uniform_()
+    recv = torch.empty_like(send)
+
+    def xchg():
+        if world == 1:
+            recv.copy_(send)
+        else:
+            dist.all_to_all_single(torch.view_as_real(recv), torch.view_as_real(send))
+
+    for _ in range(3):
+        xchg()
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        xchg()
+    e.record()
+    torch.cuda.synchronize(dev)
+    t = torch.tensor([s.elapsed_time(e) / reps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    wire = 8 * m * (world - 1) / world if world > 1 else 16 * m  # bytes leaving each GPU / HBM bytes of the copy
+    return {"ms": ms, "gbs": wire / (ms / 1e3) / 1e9,
+            "what": ("all_to_all_single over NCCL, bytes sent per GPU / time" if world > 1
+                     else "world 1: the exchange is a device copy (HBM read + write bytes / time)")}
+
+
+def run_distributed(a):
+    """Config C5: one N-point transform block-distributed over all ranks:
+    exchange -> butterfly -> exchange -> local -> exchange -> unpack
+    (paper_2308_00497_b200.distributed.DistributedFFT)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2308_00497_b200 as fg
     from paper_2308_00497_b200.distributed import DistributedFFT
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("nccl", rank=rank, world_size=world)
-    dev = torch.device("cuda", local)
+        os.environ.setdefault("MASTER_PORT", str(free_port()))
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     n = a.n
     m = n // world
-    g = torch.Generator(device=dev).manual_seed(7 + rank)
-    x = torch.complex(torch.rand(m, device=dev, generator=g) * 2 - 1, torch.rand(m, device=dev, generator=g) * 2 - 1)
+    # rank r's block of the reference input x = seeded_input(n, 1), generated on the device
+    x = torch.view_as_complex(fg.seeded_input(n, 1, "interleaved", seed0=1, device=local)[0][rank * m:(rank + 1) * m])
+    x = x.contiguous()
     d = DistributedFFT(n, device=local)
+    out = torch.empty_like(x)
+    direction = fg.FORWARD if a.direction == "forward" else fg.INVERSE
     for _ in range(a.warmup):
-        y = d.execute(x)
+        d.execute(x, direction, out=out)
     torch.cuda.synchronize(dev)
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         s.record()
         for _ in range(a.steps):
-            y = d.execute(x)
+            d.execute(x, direction, out=out)
         e.record()
         torch.cuda.synchronize(dev)
     dist.barrier()
     t = torch.tensor([s.elapsed_time(e) / a.steps], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
-    del y
+    # per-stage device times of one execute (events between the stages)
+    w0, w1 = d.workspace(x)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    ev[0].record()
+    d.exchange(x, w0); ev[1].record()
+    d.stages.butterfly(w0, w1, direction); ev[2].record()
+    d.exchange(w1, w0); ev[3].record()
+    d.stages.local(w0, w1, direction); ev[4].record()
+    d.exchange(w1, w0); ev[5].record()
+    d.stages.unpack(w0, out); ev[6].record()
+    torch.cuda.synchronize(dev)
+    names = ["exchange1", "butterfly", "exchange2", "local", "exchange3", "unpack"]
+    stages = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(6)], device=dev, dtype=torch.float64)
+    dist.all_reduce(stages, op=dist.ReduceOp.MAX)
+    probe = a2a_probe(m, dev, world)
+    # e2e: the rank's block from pinned host memory in, the result back out, every step
+    h_in = x.cpu().pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    d_in = torch.empty_like(x)
+    e2e_steps = max(1, a.e2e_steps)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d_in.copy_(h_in, non_blocking=True)
+        d.execute(d_in, direction, out=out)
+        h_out.copy_(out, non_blocking=True)
+        torch.cuda.synchronize(dev)
+    el = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
     if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except Exception:
+            pass
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        st = {k: round(float(v), 4) for k, v in zip(names, stages)}
+        xms = st["exchange1"] + st["exchange2"] + st["exchange3"]
+        wire = 3 * 8 * m * (world - 1) / world
+        local_plan = d.stages.describe_local().splitlines()
         print(json.dumps({
             "metric": METRIC, "value": round(gflop(n, 1) / (ms / 1e3), 2), "unit": "GFLOP/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: uniform [-1,1) re/im on device", "impl": "ours",
-            "config": {"workload": f"single c2c fp32 FFT N={n} distributed over {world} GPU(s), "
-                                   f"{d.n1}x{d.n2} four-step, 3 all-to-alls", "n": n, "n1": d.n1, "n2": d.n2},
+            "data": "synthetic: the reference's seeded_input(N, 1) (verify.cpp:55-78) generated on the device, "
+                    "block-distributed", "impl": "ours",
+            "config": {"workload": f"single c2c fp32 FFT N={n} block-distributed over {world} GPU(s): "
+                                   f"P-point butterfly + local N/P plan + unpack, 3 contiguous all-to-alls",
+                       "n": n, "block_per_gpu": m, "chunk": m // world, "direction": a.direction,
+                       "l2": "blocks of 8N/P bytes exceed the 126 MB L2 for N >= 2^25; no flush"},
+            "stages_ms": st,
+            "roofline": ({"bound": "nvlink", "achieved": round(wire / (xms / 1e3) / 1e9, 1) if xms else None,
+                          "peak": round(probe["gbs"], 1), "unit": "GB/s",
+                          "frac": round(wire / (xms / 1e3) / 1e9 / probe["gbs"], 4) if xms else None,
+                          "peak_source": "measured all_to_all_single probe in this run", "traffic": None}
+                         if world > 1 else
+                         {"bound": "hbm", "achieved": round(16.0 * n / (ms / 1e3) / 1e9, 1), "peak": hbm,
+                          "unit": "GB/s", "frac": round(16.0 * n / (ms / 1e3) / 1e9 / hbm, 4), "traffic": None,
+                          "note": "single-pass 16N fraction; one rank does butterfly + local passes + unpack + "
+                                  "3 device-copy exchanges"}),
+            "a2a_probe": probe,
+            "local_plan": local_plan[2:] if len(local_plan) > 2 else local_plan,
+            "e2e": {"value": round(gflop(n, 1) / float(el[0]), 2), "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": 8 * m,
+                    "ms_per_step": round(float(el[0]) * 1e3, 3), "path": "DistributedFFT.execute with pinned "
+                    "host block copies in and out per rank"},
+            "gpu_launches": a.steps * (2 + d.stages.local_launches()),
             "clocks": clk.summary()}), flush=True)
+    dist.barrier()
     dist.destroy_process_group()
 
 
 def main():
     a = parse()
-    if a.impl == "reference":
+    if relaunch_if_needed(a):
+        return
+    if a.launch_selftest:
+        launch_selftest(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.workload == "distributed":
         run_distributed(a)

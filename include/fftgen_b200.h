@@ -199,6 +199,14 @@ int64_t fftgen_dist_block_elems(const fftgen_dist_plan *plan);
 /* The local n/world-point plan (for describe / launch accounting). */
 const fftgen_plan *fftgen_dist_local_plan(const fftgen_dist_plan *plan);
 
+/* The reference's synthetic input seeded_input(n, seed) (verify.cpp:55-78:
+ * splitmix64, re/im uniform in [-1, 1)) generated on `device` for `batch`
+ * transforms, transform b with seed seed0 + b, rounded once to fp32 (bitwise
+ * the host generator's values cast to float), written in `layout` with the
+ * fftgen_execute addressing (out1 = im plane for split). */
+fftgen_status fftgen_seeded_input(int layout, int64_t n, int64_t batch, uint64_t seed0, void *out0, void *out1,
+                                  int64_t dist, int device, void *stream);
+
 const char *fftgen_error_string(fftgen_status status);
 /* Detail message of the most recent failure on the calling thread. */
 const char *fftgen_last_error(void);

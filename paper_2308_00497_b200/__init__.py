@@ -45,7 +45,7 @@ ABI_SYMBOLS = (
     "fftgen_plan_describe", "fftgen_plan_launches", "fftgen_plan_scratch_bytes",
     "fftgen_twiddle_multiply", "fftgen_dist_plan_create", "fftgen_dist_plan_destroy", "fftgen_dist_butterfly",
     "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
-    "fftgen_dist_block_elems", "fftgen_dist_local_plan",
+    "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input",
 )
 
 
@@ -150,6 +150,7 @@ def _load() -> C.CDLL:
     L.fftgen_dist_block_elems.restype = i64
     L.fftgen_dist_local_plan.argtypes = [vp]
     L.fftgen_dist_local_plan.restype = vp
+    L.fftgen_seeded_input.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, i64, C.c_int, vp]
     return L
 
 
@@ -411,6 +412,29 @@ def twiddle_multiply(block, row_offset: int, col_offset: int, n: int, direction:
         stream = stream.cuda_stream
     _check(lib.fftgen_twiddle_multiply(direction, _ptr(block), rows, cols, ld, row_offset, col_offset, n,
                                        int(stream)))
+
+
+def seeded_input(n: int, batch: int, layout: str = "interleaved", seed0: int = 1, device: int = 0,
+                 dist: Optional[int] = None, stream=None):
+    """The reference's seeded_input (verify.cpp:55-78) for `batch` transforms
+    (seeds seed0 .. seed0+batch-1), generated on the device in fp32: a
+    (batch, dist, 2) float32 tensor (interleaved) or a pair of (batch, dist)
+    planes (split)."""
+    import torch
+    dist = n if dist is None else dist
+    dev = torch.device("cuda", device)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev).cuda_stream
+    elif hasattr(stream, "cuda_stream"):
+        stream = stream.cuda_stream
+    if layout == "split":
+        re = torch.empty(batch, dist, dtype=torch.float32, device=dev)
+        im = torch.empty_like(re)
+        _check(lib.fftgen_seeded_input(1, n, batch, seed0, _ptr(re), _ptr(im), dist, device, int(stream)))
+        return re, im
+    x = torch.empty(batch, dist, 2, dtype=torch.float32, device=dev)
+    _check(lib.fftgen_seeded_input(0, n, batch, seed0, _ptr(x), None, dist, device, int(stream)))
+    return x
 
 
 class DistPlan:

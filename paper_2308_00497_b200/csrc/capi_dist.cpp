@@ -1,5 +1,6 @@
 // capi_dist.cpp -- C ABI of the distributed four-step (include/fftgen_b200.h,
-// "distributed four-step"; device stages in dist.cu).
+// "distributed four-step"; device stages in dist.cu) and of the device-side
+// seeded_input generator.
 //
 // A fftgen_dist_plan is one rank's share of an n-point transform over `world`
 // ranks: the P-point butterfly's twiddle tables (rank-independent), the
@@ -180,6 +181,19 @@ fftgen_status fftgen_dist_execute(const fftgen_dist_plan *p, int direction, cons
   if ((st = fftgen_dist_local(p, direction, w0, w1, stream)) != FFTGEN_OK) return st;
   if ((st = xchg(w1, w0)) != FFTGEN_OK) return st;
   return fftgen_dist_unpack(p, w0, out, stream);
+}
+
+fftgen_status fftgen_seeded_input(int layout, int64_t n, int64_t batch, uint64_t seed0, void *out0, void *out1,
+                                  int64_t dist, int device, void *stream) {
+  const bool split = layout == FFTGEN_LAYOUT_SPLIT;
+  if (layout != FFTGEN_LAYOUT_INTERLEAVED && !split)
+    return dfail(FFTGEN_ERR_EXEC, "unknown complex layout " + std::to_string(layout));
+  if (n < 1 || batch < 0 || dist < n) return dfail(FFTGEN_ERR_DIMENSION, "bad seeded_input geometry");
+  if (!out0 || (split && !out1)) return dfail(FFTGEN_ERR_EXEC, "NULL data pointer");
+  Guard g(device);
+  if (g.err != cudaSuccess) return dcuda(g.err, "cudaSetDevice");
+  cudaError_t e = seeded_input(split, out0, out1, n, batch, seed0, dist, (cudaStream_t)stream);
+  return e == cudaSuccess ? FFTGEN_OK : dcuda(e, "seeded_input kernel");
 }
 
 int64_t fftgen_dist_chunk_elems(const fftgen_dist_plan *p) { return p ? p->l1 : -1; }

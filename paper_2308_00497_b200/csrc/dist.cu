@@ -169,4 +169,53 @@ cudaError_t dist_unpack(int p, const float2 *in, float2 *out, int64_t l1, cudaSt
   return cudaGetLastError();
 }
 
+// ---- seeded_input (verify.cpp:55-78) on the device ------------------------
+// The reference draws splitmix64 sequentially from state = seed; draw k
+// (1-based) sees state seed + k*gamma, so element j of transform b is
+//   re = 2 u(mix(s + (2j+1) gamma)) - 1,  im = 2 u(mix(s + (2j+2) gamma)) - 1,
+// s = seed0 + b, u(bits) = (bits >> 11) 2^-53 -- computed in fp64 like the
+// reference and rounded once to fp32 (bit-identical to the host generator's
+// values cast to float).
+namespace {
+__device__ __forceinline__ uint64_t splitmix_finalize(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ float seeded_value(uint64_t state) {
+  return (float)(2.0 * ((double)(splitmix_finalize(state) >> 11) * 0x1.0p-53) - 1.0);
+}
+
+template <bool SPLIT>
+__global__ void __launch_bounds__(256) seeded_input_kernel(void *out0, void *out1, int64_t n, int64_t batch,
+                                                           uint64_t seed0, int64_t dist) {
+  constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+  const int64_t total = n * batch;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / n, j = i - b * n;
+    const uint64_t s = seed0 + (uint64_t)b;
+    const float re = seeded_value(s + (uint64_t)(2 * j + 1) * kGamma);
+    const float im = seeded_value(s + (uint64_t)(2 * j + 2) * kGamma);
+    if constexpr (SPLIT) {
+      reinterpret_cast<float *>(out0)[b * dist + j] = re;
+      reinterpret_cast<float *>(out1)[b * dist + j] = im;
+    } else {
+      reinterpret_cast<float2 *>(out0)[b * dist + j] = make_float2(re, im);
+    }
+  }
+}
+}  // namespace
+
+cudaError_t seeded_input(bool split, void *out0, void *out1, int64_t n, int64_t batch, uint64_t seed0, int64_t dist,
+                         cudaStream_t s) {
+  const int64_t total = n * batch;
+  if (total <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (split)
+    seeded_input_kernel<true><<<g, 256, 0, s>>>(out0, out1, n, batch, seed0, dist);
+  else
+    seeded_input_kernel<false><<<g, 256, 0, s>>>(out0, out1, n, batch, seed0, dist);
+  return cudaGetLastError();
+}
+
 }  // namespace fftgen_b200

@@ -117,6 +117,10 @@ cudaError_t dist_butterfly(int p, int dir, const float2 *in, float2 *out, int64_
                            const float2 *thi, int h, int log2n, cudaStream_t s);
 cudaError_t dist_unpack(int p, const float2 *in, float2 *out, int64_t l1, cudaStream_t s);
 
+// seeded_input (verify.cpp:55-78) for transforms b < batch, seed seed0 + b, fp32
+cudaError_t seeded_input(bool split, void *out0, void *out1, int64_t n, int64_t batch, uint64_t seed0, int64_t dist,
+                         cudaStream_t s);
+
 cudaError_t convert_f64_to_f32(const double *in, float *out, int64_t count, cudaStream_t s);
 cudaError_t convert_f32_to_f64(const float *in, double *out, int64_t count, cudaStream_t s);
 cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, int64_t istride,
