@@ -125,9 +125,14 @@ class DistributedFFT:
         if x_local.numel() != self.m or x_local.dtype != torch.complex64:
             raise ValueError(f"expected a complex64 block of {self.m} elements")
         x_local = x_local.reshape(-1)
-        w0, w1 = self.workspace(x_local)
         if out is None:
             out = torch.empty_like(x_local)
+        if self.world == 1:
+            # P = 1: both exchanges, the 1-point butterfly (w^0 = 1) and the
+            # stride-1 unpack are identities; the local plan is the transform
+            self.stages.local(x_local, out, direction)
+            return out
+        w0, w1 = self.workspace(x_local)
         self.exchange(x_local, w0)
         self.stages.butterfly(w0, w1, direction)
         self.exchange(w1, w0)
