@@ -85,7 +85,9 @@ enum { FFTGEN_TILE_NONE = 0, FFTGEN_TILE_EXACT = 1, FFTGEN_TILE_CACHE = 2 }; /* 
 enum {
   FFTGEN_TUNE_NO_TMA = 1,        /* N <= 2^14: the direct block kernel; four-step groups: plain tiles */
   FFTGEN_TUNE_NO_TMA_STORE = 2,  /* block kernels: register stores instead of bulk stores */
-  FFTGEN_TUNE_GROUP_TMA_ALL = 4  /* every four-step group as the persistent TMA-tile kernel */
+  FFTGEN_TUNE_GROUP_TMA_ALL = 4, /* every four-step group as the persistent TMA-tile kernel */
+  FFTGEN_TUNE_GROUPS_1024 = 8,   /* four-step groups of at most 2^10 points (three passes from 2^21) */
+  FFTGEN_TUNE_TWO_PASS = 16      /* two four-step groups up to 2^24 (NS = 2^11 / 2^12 tiles) */
 };
 
 typedef struct {

@@ -260,10 +260,17 @@ template <int N> struct Tma1Geom {
 #ifndef FFTGEN_GROUP_TILE_LARGE
 #define FFTGEN_GROUP_TILE_LARGE 65536
 #endif
+// NS = 2^11 / 2^12 groups (the 2-pass plans of 2^21 .. 2^24) keep 128 KB
+// tiles -- 8 / 4 columns of 64 / 32 bytes -- one CTA of 256 threads per SM
+// with the full register file for the 64-point codelets.
+#ifndef FFTGEN_GROUP_TILE_HUGE
+#define FFTGEN_GROUP_TILE_HUGE 131072
+#endif
 template <int NS, int MAXT = 512> struct GroupGeom {
   using PL = GroupPlan<NS>;
   static constexpr int T = BlockGeom<NS, 0, PL>::T;
-  static constexpr int TILE_BYTES = NS <= 256 ? FFTGEN_GROUP_TILE_SMALL : FFTGEN_GROUP_TILE_LARGE;
+  static constexpr int TILE_BYTES =
+      NS <= 256 ? FFTGEN_GROUP_TILE_SMALL : (NS <= 1024 ? FFTGEN_GROUP_TILE_LARGE : FFTGEN_GROUP_TILE_HUGE);
   static constexpr int TC_BYTES = TILE_BYTES / (8 * NS);                // transforms per tile
   static constexpr int TC = TC_BYTES * T > MAXT ? MAXT / T : TC_BYTES;  // <= MAXT threads
   using G = BlockGeom<NS, TC, PL>;
@@ -274,7 +281,7 @@ template <int NS, int MAXT = 512> struct GroupGeom {
   // resident CTAs the register budget must allow: 16-point codelets fit 64
   // registers, 32-point ones (NS >= 512) need 128
   static constexpr int MIN_BLOCKS =
-      G::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3));
+      NS >= 2048 ? 1 : (G::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3)));
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };

@@ -431,7 +431,9 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);
     auto radices = stockham_radices(cfg->n, cfg->radix);
     check_schedule(cfg->vec, cfg->vector_width, cfg->tile_kind, cfg->tile_value);
-    ExecPlan ex = build_exec_plan(cfg->n);
+    ExecPlan ex = build_exec_plan(cfg->n, (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
+                                              ? SPLIT_GROUPS_1024
+                                              : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT));
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);

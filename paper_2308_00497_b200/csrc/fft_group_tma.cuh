@@ -32,10 +32,11 @@ constexpr int kGroupTmaStages = FFTGEN_GROUP_TMA_STAGES;
 // STAGES = 1: two CTAs per SM, each refilling its stage after pass 1.
 template <int NS, int STAGES_ = kGroupTmaStages> struct GroupTmaGeom {
   using GG = GroupGeom<NS>;
-  static constexpr int STAGES = STAGES_;
   static constexpr int TC = GG::TC, REG = GG::REG, THREADS = GG::THREADS;
   static constexpr int RAW = TC * NS * 8;  // raw tile bytes
   static constexpr int STAGE = ((TC * REG * 8 > RAW ? TC * REG * 8 : RAW) + 127) / 128 * 128;
+  // 128 KB tiles (NS >= 2048) fit one stage: the refill overlaps the stores
+  static constexpr int STAGES = STAGES_ * STAGE + 64 > 227 * 1024 ? 1 : STAGES_;
   static constexpr int BYTES = STAGES * STAGE + 64;
   static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 0 ? (228 * 1024) / (BYTES + 1024) : 1;
 };

@@ -104,6 +104,8 @@ std::vector<float> group_twiddles(int log2ns) {
   case 8: emit(BlockGeom<256, 0, GroupPlan<256>>{}); break;
   case 9: emit(BlockGeom<512, 0, GroupPlan<512>>{}); break;
   case 10: emit(BlockGeom<1024, 0, GroupPlan<1024>>{}); break;
+  case 11: emit(BlockGeom<2048, 0, GroupPlan<2048>>{}); break;
+  case 12: emit(BlockGeom<4096, 0, GroupPlan<4096>>{}); break;
   default: throw PlanError("no group kernel for 2^" + std::to_string(log2ns));
   }
   return out;
@@ -118,7 +120,8 @@ void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_
     *smem = GroupGeom<NN>::BYTES;      \
     *r0 = GroupGeom<NN>::R0;           \
     return;
-    FFTGEN_GG(7, 128) FFTGEN_GG(8, 256) FFTGEN_GG(9, 512) FFTGEN_GG(10, 1024)
+    FFTGEN_GG(7, 128) FFTGEN_GG(8, 256) FFTGEN_GG(9, 512) FFTGEN_GG(10, 1024) FFTGEN_GG(11, 2048)
+    FFTGEN_GG(12, 4096)
 #undef FFTGEN_GG
   default:
     *threads = *tc = *smem = *r0 = 0;

@@ -1,5 +1,5 @@
 // group_instances.cuh -- instantiates the K3 group kernel (fft_group.cuh)
-// for NS = 2^6 .. 2^10 and the (input layout, output layout, rows) shapes a
+// for NS = 2^7 .. 2^12 and the (input layout, output layout, rows) shapes a
 // multi-group plan uses: first group (user -> interleaved scratch, columns),
 // middle groups (scratch -> scratch, columns), last group (scratch -> user,
 // rows with the transposed store).
@@ -96,6 +96,8 @@ template <int NS, int DIR> cudaError_t group_tma_prepare_ns(int *bps) {
     case 8: return group_launch_ns<256, DIR>(shape, a, grid, s);                                    \
     case 9: return group_launch_ns<512, DIR>(shape, a, grid, s);                                    \
     case 10: return group_launch_ns<1024, DIR>(shape, a, grid, s);                                  \
+    case 11: return group_launch_ns<2048, DIR>(shape, a, grid, s);                                  \
+    case 12: return group_launch_ns<4096, DIR>(shape, a, grid, s);                                  \
     default: return cudaErrorInvalidValue;                                                          \
     }                                                                                               \
   }                                                                                                 \
@@ -105,6 +107,8 @@ template <int NS, int DIR> cudaError_t group_tma_prepare_ns(int *bps) {
     case 8: return group_prepare_ns<256, DIR>();                                                    \
     case 9: return group_prepare_ns<512, DIR>();                                                    \
     case 10: return group_prepare_ns<1024, DIR>();                                                  \
+    case 11: return group_prepare_ns<2048, DIR>();                                                  \
+    case 12: return group_prepare_ns<4096, DIR>();                                                  \
     default: return cudaErrorInvalidValue;                                                          \
     }                                                                                               \
   }                                                                                                 \
@@ -115,6 +119,8 @@ template <int NS, int DIR> cudaError_t group_tma_prepare_ns(int *bps) {
     case 8: return group_tma_launch_ns<256, DIR>(shape, ta, grid, s);                               \
     case 9: return group_tma_launch_ns<512, DIR>(shape, ta, grid, s);                               \
     case 10: return group_tma_launch_ns<1024, DIR>(shape, ta, grid, s);                             \
+    case 11: return group_tma_launch_ns<2048, DIR>(shape, ta, grid, s);                             \
+    case 12: return group_tma_launch_ns<4096, DIR>(shape, ta, grid, s);                             \
     default: return cudaErrorInvalidValue;                                                          \
     }                                                                                               \
   }                                                                                                 \
@@ -124,6 +130,8 @@ template <int NS, int DIR> cudaError_t group_tma_prepare_ns(int *bps) {
     case 8: return group_tma_prepare_ns<256, DIR>(bps);                                             \
     case 9: return group_tma_prepare_ns<512, DIR>(bps);                                             \
     case 10: return group_tma_prepare_ns<1024, DIR>(bps);                                           \
+    case 11: return group_tma_prepare_ns<2048, DIR>(bps);                                           \
+    case 12: return group_tma_prepare_ns<4096, DIR>(bps);                                           \
     default: return cudaErrorInvalidValue;                                                          \
     }                                                                                               \
   }

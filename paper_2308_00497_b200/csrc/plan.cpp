@@ -169,7 +169,7 @@ void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_v
   }
 }
 
-ExecPlan build_exec_plan(int64_t n) {
+ExecPlan build_exec_plan(int64_t n, int split_mode) {
   if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
   ExecPlan p;
   p.n = n;
@@ -194,7 +194,7 @@ ExecPlan build_exec_plan(int64_t n) {
     throw PlanError("size 2^" + std::to_string(p.log2n) + " exceeds the single-GPU limit 2^30");
   // K3 four-step: groups of consecutive Stockham stages, each one kernel
   p.strategy = STRAT_FOURSTEP;
-  const std::vector<int> split = group_split(p.log2n);
+  const std::vector<int> split = group_split(p.log2n, split_mode);
   int64_t s = 1;
   std::vector<int> seen_local;
   for (size_t g = 0; g < split.size(); ++g) {
@@ -234,13 +234,20 @@ ExecPlan build_exec_plan(int64_t n) {
   return p;
 }
 
-std::vector<int> group_split(int log2n) {
-  // 2 groups up to 2^20 (NS <= 2^10), 3 groups up to 2^28, 4 groups up to
-  // 2^30; sizes as even as possible.  Measured on B200:
+std::vector<int> group_split(int log2n, int mode) {
+  // 2 groups up to 2^21 (NS <= 2^11), 3 groups up to 2^28, 4 groups up to
+  // 2^30; sizes as even as possible.  mode SPLIT_GROUPS_1024: NS <= 2^10 (2
+  // groups up to 2^20); SPLIT_TWO_PASS: 2 groups up to 2^24 (NS <= 2^12, 32 N
+  // bytes of HBM traffic instead of 48 N).  Measured on B200 (1 GiB batches,
+  // split / interleaved ms): 2^21 10+11 1.05 / 1.00 vs 7+7+7 1.17 / 1.14;
+  // 2^22 11+11 1.23 / 1.16 vs 7+7+8 1.15 / 1.08; 2^24 12+12 1.95 / 1.54 vs
+  // 8+8+8 1.15 / 1.07 (the 128 KB NS = 4096 tiles leave one CTA per SM).
+  // Earlier:
   // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
   // 64-byte segments).
-  const int g = log2n <= 20 ? 2 : (log2n <= 28 ? 3 : 4);
+  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : 21);
+  const int g = log2n <= two ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs
   // it (measured on B200: 2^17 0.45 / 0.47 vs 0.42 / 0.45, 2^25 0.29 / 0.30 vs

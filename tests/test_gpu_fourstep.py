@@ -34,9 +34,10 @@ def seeded_batch(orc, n, batch, seed0=1):
     return x.astype(np.float32).astype(np.float64)
 
 
-def run(fg, n, layout, direction, x):
+def run(fg, n, layout, direction, x, tuning=0):
     batch = x.shape[0]
-    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, algorithm="stockham"))
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, algorithm="stockham",
+                                                 tuning=tuning))
     if layout == "interleaved":
         src = torch.from_numpy(x.astype(np.float32)).cuda()
         dst = torch.full_like(src, float("nan"))
@@ -72,10 +73,25 @@ def test_fourstep_matches_oracle(fg, orc, l2, layout, direction):
 def test_three_group_sizes_vs_oracle(fg, orc, l2):
     n = 1 << l2
     x = seeded_batch(orc, n, 1, seed0=5)
-    got = run(fg, n, "split", -1, x)
+    got = run(fg, n, "split", -1, x, tuning=8)
     want = orc.forward(x, "stockham", 4)
     err = oracle.rel_l2(got[0], want[0])
     assert err <= tol(n) and err < 4e-6, err
+
+
+@pytest.mark.parametrize("l2", [21, 22, 23, 24])
+@pytest.mark.parametrize("layout,direction", [("split", -1), ("interleaved", 1)])
+@pytest.mark.parametrize("tuning", [16, 16 | 1, 16 | 4])
+def test_two_pass_plans_vs_oracle(fg, orc, l2, layout, direction, tuning):
+    """2^21..2^24 as two groups of 2^11 / 2^12 points (plain / TMA tiles)."""
+    n = 1 << l2
+    batch = 2 if l2 <= 22 else 1
+    x = seeded_batch(orc, n, batch, seed0=11)
+    got = run(fg, n, layout, direction, x, tuning=tuning)
+    want = orc.forward(x, "stockham", 4, inverse=direction > 0, threads=8)
+    for b in range(batch):
+        err = oracle.rel_l2(got[b], want[b])
+        assert err <= tol(n) and err < 4e-6, (b, err)
 
 
 def test_fourstep_plan_shape(fg):
@@ -84,6 +100,14 @@ def test_fourstep_plan_shape(fg):
     assert p.launches() == 3
     assert p.scratch_bytes() == 2 * (1 << 24) * 8
     assert "transposed store" in p.describe()
+    # two-pass plans: NS = 2^11 / 2^12 groups, one scratch buffer
+    p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 24, layout="split", batch=1, tuning=16))
+    assert [d[0] for d in p.passes()] == [4096, 4096] and p.launches() == 2
+    assert p.scratch_bytes() == (1 << 24) * 8
+    p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 21, layout="split", batch=1))
+    assert [d[0] for d in p.passes()] == [1024, 2048] and p.launches() == 2
+    p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 21, layout="split", batch=1, tuning=8))
+    assert [d[0] for d in p.passes()] == [128, 128, 128]
     q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 15, layout="split", batch=4))
     # 2^15 runs as one cluster per transform: one launch, no HBM scratch
     assert [d[0] for d in q.passes()] == [128, 256] and q.scratch_bytes() == 0 and q.launches() == 1
