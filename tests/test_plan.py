@@ -30,7 +30,8 @@ PLAN_TOOL = os.path.join(ROOT, "paper_2308_00497_b200", "build", "plan_tool")
 def declared_symbols():
     text = open(HDR).read()
     return sorted(set(re.findall(
-        r"^(?:fftgen_status|int|void|size_t|const char \*)\s*\*?(fftgen_[a-z0-9_]+)\(", text, re.M)))
+        r"^(?:fftgen_status|int|int64_t|void|size_t|const char \*|const fftgen_plan \*)\s*\*?(fftgen_[a-z0-9_]+)\(",
+        text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -159,7 +160,7 @@ def test_fourstep_groups_cover_large_sizes(plan_tool):
         assert 2 <= len(groups) <= 4
         prod = 1
         for R, cols, k, s in groups:
-            assert 64 <= R <= 1024 and cols == prod and s == R * cols and k * s == 1 << l2
+            assert 64 <= R <= 4096 and cols == prod and s == R * cols and k * s == 1 << l2
             prod *= R
         assert prod == 1 << l2 and groups[-1][2] == 1
     assert plan_tool("passes", 1 << 31)[0] == 1  # PlanError above 2^30
