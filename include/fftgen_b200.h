@@ -233,6 +233,15 @@ fftgen_status fftgen_plan_pipeline_text(const fftgen_plan *plan, char *buf, size
 int fftgen_plan_num_passes(const fftgen_plan *plan);
 fftgen_status fftgen_plan_pass(const fftgen_plan *plan, int idx, int64_t desc[4]);
 fftgen_status fftgen_plan_describe(const fftgen_plan *plan, char *buf, size_t cap);
+/* Host-only program texts for a config (no device touched; validates like
+ * fftgen_plan_create: PlanError / FuseError / LowerError):
+ *   FFTGEN_TEXT_FORMULA   print_formula of plan_cooley_tukey / plan_stockham
+ *                         (formula.cpp:104-197), byte-identical to the reference
+ *   FFTGEN_TEXT_PIPELINE  print_pipeline of the fused op list (rewrite.cpp:275-296)
+ *   FFTGEN_TEXT_LOOPS     the sm_100a pass / group program as loop nests
+ *   FFTGEN_TEXT_RADICES   the Stockham radices, application order */
+enum { FFTGEN_TEXT_FORMULA = 0, FFTGEN_TEXT_PIPELINE = 1, FFTGEN_TEXT_LOOPS = 2, FFTGEN_TEXT_RADICES = 3 };
+fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf, size_t cap);
 /* Kernel launches one fftgen_execute issues (for launch accounting). */
 int fftgen_plan_launches(const fftgen_plan *plan);
 size_t fftgen_plan_scratch_bytes(const fftgen_plan *plan);

@@ -1,31 +1,44 @@
 // include/fftgen_b200.hpp -- C++ host API over the C ABI (include/fftgen_b200.h).
 //
-// A drop-in for the reference's plan -> execute API in proj/include/fftgen:
-// the same names, argument meaning and error behaviour, so a caller of the
-// reference switches by including this header instead of
-// fftgen/driver.hpp + fftgen/exec.hpp + fftgen/error.hpp and linking
-// libfftgen_b200.so.
+// Source-compatible with the reference's public plan -> execute API in
+// proj/include/fftgen (driver.hpp, exec.hpp, error.hpp and the ComplexBuffer /
+// TilePolicy types of loopir.hpp): the same names, fields, argument meaning
+// and exception classes, so code written against
 //
-//   reference                                       here
-//   Error / PlanError / DimensionError / FuseError  same classes (error.hpp:16-71)
-//     / ExecError
-//   Algorithm, ComplexLayout                        same enums (driver.hpp:21, loopir.hpp:187)
-//   PipelineConfig {n, algorithm, radix, layout}    same fields + batch, device (driver.hpp:26-35)
-//   CompiledPipeline compile_pipeline(config)       same (driver.hpp:44-45); owns the device plan
-//   ComplexBuffer {data, layout, logical_len}       same storage contract (loopir.hpp:215-228)
-//   ComplexBuffer interpret(program, input)         same (exec.hpp:26-27), on the GPU; an
-//                                                   overload takes a batch of buffers
-//   print_pipeline(ops)                             CompiledPipeline::pipeline_text()
-//   algorithm_name / layout_name                    same (driver.hpp:47-49)
+//   CompiledPipeline c = compile_pipeline(config);
+//   ComplexBuffer y = interpret(c.final_ir, ComplexBuffer::from_vector(x, layout), opts);
+//
+// compiles unchanged against this header (the reference's own
+// tests/test_exec.cpp known-answer cases do: tests/cpp/refshim +
+// tests/test_cpp_api.py) and runs the sm_100a kernels.
+//
+//   reference (file:line)                          here
+//   Error / ParseError / DimensionError /          same classes (error.hpp:16-71)
+//     PlanError / FuseError / LowerError /
+//     ExecError / BoundsError / GpuMapError
+//   Algorithm, VecMode (driver.hpp:21-23)          same enums
+//   ComplexLayout, TilePolicy (loopir.hpp:187,240) same
+//   PipelineConfig (driver.hpp:26-35)              same fields + batch, device, tuning
+//   CompiledPipeline {formula, fused, complex_ir,  same members (driver.hpp:37-42); the
+//     final_ir} (driver.hpp:37-42)                 LoopProgram is the device plan handle
+//   compile_pipeline (driver.hpp:44-45)            same; validates like the reference
+//   algorithm_name / layout_name / vec_mode_name   same (driver.hpp:47-52)
+//   ExecOptions {threads} (exec.hpp:16-21)         same + direction (the reference is forward-only)
+//   interpret(LoopProgram, ComplexBuffer,          same (exec.hpp:26-27): fp64 storage in/out,
+//     ExecOptions) (exec.hpp:26-27)                fp32 on the GPU; ExecError on a length or
+//                                                  layout mismatch (interpret.cpp:46-63)
+//   ComplexBuffer (loopir.hpp:215-228)             same storage contract
 //
 // plus device-pointer execution (CompiledPipeline::execute) with a direction
-// and a CUDA stream.  Header-only; no CUDA headers are required.
+// and a CUDA stream, and a batched interpret.  Header-only; no CUDA headers.
 #ifndef FFTGEN_B200_HPP
 #define FFTGEN_B200_HPP
 
+#include <algorithm>
 #include <complex>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -36,9 +49,17 @@ namespace fftgen {
 
 using cplx = std::complex<double>;
 
+// ---- error.hpp:16-71 ---------------------------------------------------------
 class Error : public std::runtime_error {
  public:
   explicit Error(const std::string &msg) : std::runtime_error(msg) {}
+};
+class ParseError : public Error {  // malformed formula text, 1-based position
+ public:
+  ParseError(const std::string &msg, int line, int column)
+      : Error(std::to_string(line) + ":" + std::to_string(column) + ": " + msg), line(line), column(column) {}
+  int line;
+  int column;
 };
 class DimensionError : public Error {
  public:
@@ -52,26 +73,61 @@ class FuseError : public Error {
  public:
   using Error::Error;
 };
+class LowerError : public Error {
+ public:
+  using Error::Error;
+};
 class ExecError : public Error {
  public:
   using Error::Error;
 };
+class BoundsError : public Error {
+ public:
+  using Error::Error;
+};
+class GpuMapError : public Error {
+ public:
+  using Error::Error;
+};
 
+// ---- driver.hpp:21-35, loopir.hpp:187 / 240-248 -------------------------------
 enum class Algorithm { CooleyTukey, Stockham };
+enum class VecMode { None, Inner, Outer };
 enum class ComplexLayout { Interleaved, Split };
 enum class Direction { Forward = FFTGEN_FORWARD, Inverse = FFTGEN_INVERSE };
+
+struct TilePolicy {
+  enum Kind { ExactSize, CacheVolume } kind = ExactSize;
+  int64_t value = 0;  // tile size or byte budget
+  static TilePolicy exact(int64_t t) { return {ExactSize, t}; }
+  static TilePolicy cache(int64_t bytes = 32 * 1024) { return {CacheVolume, bytes}; }
+};
 
 struct PipelineConfig {
   int64_t n = 0;
   Algorithm algorithm = Algorithm::CooleyTukey;
   int64_t radix = 2;
   ComplexLayout layout = ComplexLayout::Interleaved;
-  int64_t batch = 1;  // transforms per execute
-  int device = 0;     // CUDA device ordinal
+  // the reference's CPU loop-IR schedule: validated like vectorize() / tile()
+  // (LowerError), result-neutral on the GPU (the reference guarantees
+  // scheduled and scalar programs agree bitwise)
+  VecMode vec = VecMode::None;
+  int64_t vector_width = 8;
+  bool interleaved_opt = false;
+  std::optional<TilePolicy> tile;
+  // B200 extensions
+  int64_t batch = 1;      // transforms per execute
+  int device = 0;         // CUDA device ordinal
+  uint32_t tuning = 0;    // FFTGEN_TUNE_* kernel-selection bits (0 = measured defaults)
 };
 
 inline std::string algorithm_name(Algorithm a) { return a == Algorithm::CooleyTukey ? "cooley-tukey" : "stockham"; }
 inline std::string layout_name(ComplexLayout l) { return l == ComplexLayout::Interleaved ? "interleaved" : "split"; }
+// "none", "inner", "outer", "inner-opt", "outer-opt" (driver.cpp:44-51)
+inline std::string vec_mode_name(const PipelineConfig &config) {
+  if (config.vec == VecMode::None) return "none";
+  return std::string(config.vec == VecMode::Inner ? "inner" : "outer") + (config.interleaved_opt ? "-opt" : "");
+}
 
 // Maps a C-ABI status onto the reference's exception classes.
 inline void check(fftgen_status st) {
@@ -82,6 +138,9 @@ inline void check(fftgen_status st) {
   case FFTGEN_ERR_FUSE: throw FuseError(msg);
   case FFTGEN_ERR_DIMENSION:
   case FFTGEN_ERR_INVALID: throw DimensionError(msg);
+  case FFTGEN_ERR_LOWER: throw LowerError(msg);
+  case FFTGEN_ERR_BOUNDS: throw BoundsError(msg);
+  case FFTGEN_ERR_GPUMAP: throw GpuMapError(msg);
   default: throw ExecError(msg);
   }
 }
@@ -132,93 +191,205 @@ struct ComplexBuffer {
   }
 };
 
-// The compiled plan (CompiledPipeline analogue): radix stages, fused op list,
-// sm_100a passes and the device twiddle tables.  Cheap to copy (shared).
-class CompiledPipeline {
- public:
-  explicit CompiledPipeline(const PipelineConfig &cfg) : cfg_(cfg) {
-    fftgen_config c;
-    fftgen_config_init(&c);
-    c.n = cfg.n;
-    c.algorithm = cfg.algorithm == Algorithm::Stockham ? FFTGEN_ALG_STOCKHAM : FFTGEN_ALG_COOLEY_TUKEY;
-    c.radix = static_cast<int32_t>(cfg.radix);
-    c.layout = cfg.layout == ComplexLayout::Split ? FFTGEN_LAYOUT_SPLIT : FFTGEN_LAYOUT_INTERLEAVED;
-    c.batch = cfg.batch;
-    c.device = cfg.device;
-    fftgen_plan *p = nullptr;
-    check(fftgen_plan_create(&p, &c));
-    plan_.reset(p, [](fftgen_plan *q) { fftgen_plan_destroy(q); });
-  }
+// ---- the compiled program ------------------------------------------------------
+// One fused operator of the reference's list (rewrite.hpp:24-52, application
+// order): kind 0 FusedMKIV(m, copies) 1 FusedIKMV(n, copies) 2 FusedPKIV(m,
+// total, k) 3 TwiddleMul(len) 4 Permute(m, total).
+struct FusedOp {
+  int kind = 0;
+  int64_t p0 = 0, p1 = 0, p2 = 0;
+};
+struct FuseResult {
+  std::vector<FusedOp> ops;
+};
+// The factorisation the plan was built from (formula.hpp): plan_stockham /
+// plan_cooley_tukey of (n, radix).
+struct Formula {
+  int64_t n = 0;
+  Algorithm algorithm = Algorithm::CooleyTukey;
+  int64_t radix = 2;
+};
+using FormulaPtr = std::shared_ptr<const Formula>;
 
-  const PipelineConfig &config() const { return cfg_; }
+// LoopProgram (loopir.hpp:151-208) on the B200 is the device program: the
+// sm_100a pass / group schedule, the fp32 twiddle tables on the device and
+// the plan's scratch, owned through a shared handle (cheap to copy).
+class LoopProgram {
+ public:
+  LoopProgram() = default;
+  LoopProgram(std::shared_ptr<fftgen_plan> plan, int64_t n, ComplexLayout layout, int64_t batch)
+      : plan_(std::move(plan)), n_(n), layout_(layout), batch_(batch) {}
   fftgen_plan *handle() const { return plan_.get(); }
+  int64_t size() const { return n_; }
+  int64_t batch() const { return batch_; }
+  ComplexLayout layout() const { return layout_; }
+  explicit operator bool() const { return plan_ != nullptr; }
 
   // Device buffers; dist in complex elements (interleaved) or floats (split).
   void execute(Direction dir, const void *in0, const void *in1, void *out0, void *out1, int64_t dist,
                void *stream = nullptr) const {
-    check(fftgen_execute(plan_.get(), static_cast<int>(dir), in0, in1, out0, out1, dist, stream));
+    check(fftgen_execute(need(), static_cast<int>(dir), in0, in1, out0, out1, dist, stream));
   }
   // Host fp32 buffers, pipelined through the device.
   void execute_host(Direction dir, const float *in0, const float *in1, float *out0, float *out1,
                     int64_t dist) const {
-    check(fftgen_execute_host(plan_.get(), static_cast<int>(dir), in0, in1, out0, out1, dist));
+    check(fftgen_execute_host(need(), static_cast<int>(dir), in0, in1, out0, out1, dist));
   }
-
-  std::vector<int64_t> radices() const {
-    std::vector<int64_t> r(64);
-    r.resize(fftgen_plan_radices(plan_.get(), r.data(), 64));
-    return r;
-  }
-  std::string pipeline_text() const { return text(fftgen_plan_pipeline_text); }
   std::string describe() const { return text(fftgen_plan_describe); }
-  int launches() const { return fftgen_plan_launches(plan_.get()); }
+  std::string pipeline_text() const { return text(fftgen_plan_pipeline_text); }
+  int launches() const { return fftgen_plan_launches(need()); }
 
  private:
+  fftgen_plan *need() const {
+    if (!plan_) throw ExecError("empty LoopProgram: compile a pipeline first");
+    return plan_.get();
+  }
   std::string text(fftgen_status (*fn)(const fftgen_plan *, char *, size_t)) const {
     std::vector<char> buf(1 << 16);
-    while (fn(plan_.get(), buf.data(), buf.size()) != FFTGEN_OK) {
+    while (fn(need(), buf.data(), buf.size()) != FFTGEN_OK) {
       if (buf.size() > (size_t(1) << 28)) check(FFTGEN_ERR_DIMENSION);
       buf.resize(buf.size() * 4);
     }
     return std::string(buf.data());
   }
-  PipelineConfig cfg_;
   std::shared_ptr<fftgen_plan> plan_;
+  int64_t n_ = 0;
+  ComplexLayout layout_ = ComplexLayout::Interleaved;
+  int64_t batch_ = 0;
 };
 
-inline CompiledPipeline compile_pipeline(const PipelineConfig &config) { return CompiledPipeline(config); }
+// CompiledPipeline (driver.hpp:37-42): the same four members; complex_ir and
+// final_ir are the same device program (the B200 lowering has no separate
+// pre-layout form), plus convenience forwarding to final_ir.
+struct CompiledPipeline {
+  FormulaPtr formula;
+  FuseResult fused;
+  LoopProgram complex_ir;
+  LoopProgram final_ir;
+  PipelineConfig config_;
 
-// interpret(): one ComplexBuffer per transform, layouts must match the plan
-// (interpret.cpp:46-63 raises ExecError on a length or layout mismatch).
-inline std::vector<ComplexBuffer> interpret(const CompiledPipeline &prog, const std::vector<ComplexBuffer> &inputs,
-                                            Direction dir = Direction::Forward) {
-  const PipelineConfig &cfg = prog.config();
-  if (static_cast<int64_t>(inputs.size()) != cfg.batch)
+  const PipelineConfig &config() const { return config_; }
+  fftgen_plan *handle() const { return final_ir.handle(); }
+  void execute(Direction dir, const void *in0, const void *in1, void *out0, void *out1, int64_t dist,
+               void *stream = nullptr) const {
+    final_ir.execute(dir, in0, in1, out0, out1, dist, stream);
+  }
+  void execute_host(Direction dir, const float *in0, const float *in1, float *out0, float *out1,
+                    int64_t dist) const {
+    final_ir.execute_host(dir, in0, in1, out0, out1, dist);
+  }
+  std::vector<int64_t> radices() const {
+    std::vector<int64_t> r(64);
+    r.resize(fftgen_plan_radices(handle(), r.data(), 64));
+    return r;
+  }
+  std::string pipeline_text() const { return final_ir.pipeline_text(); }
+  std::string describe() const { return final_ir.describe(); }
+  int launches() const { return final_ir.launches(); }
+};
+
+// compile_pipeline (driver.cpp:11-34): plan -> fuse -> [tile / vectorize
+// validation] -> the sm_100a program; PlanError / FuseError / LowerError /
+// DimensionError like the reference, GpuMapError when the device cannot run it.
+inline CompiledPipeline compile_pipeline(const PipelineConfig &config) {
+  fftgen_config c;
+  fftgen_config_init(&c);
+  c.n = config.n;
+  c.algorithm = config.algorithm == Algorithm::Stockham ? FFTGEN_ALG_STOCKHAM : FFTGEN_ALG_COOLEY_TUKEY;
+  if (config.radix < 0 || config.radix > (int64_t(1) << 30))
+    throw PlanError("radix must be a power of two >= 2, got " + std::to_string(config.radix));
+  c.radix = static_cast<int32_t>(config.radix);
+  c.layout = config.layout == ComplexLayout::Split ? FFTGEN_LAYOUT_SPLIT : FFTGEN_LAYOUT_INTERLEAVED;
+  c.vec = config.vec == VecMode::Inner ? FFTGEN_VEC_INNER : (config.vec == VecMode::Outer ? FFTGEN_VEC_OUTER
+                                                                                          : FFTGEN_VEC_NONE);
+  if (config.vector_width > (int64_t(1) << 30) || config.vector_width < -(int64_t(1) << 30))
+    throw LowerError("vector width capped at 64 lanes");
+  c.vector_width = static_cast<int32_t>(config.vector_width);
+  c.interleaved_opt = config.interleaved_opt ? 1 : 0;
+  if (config.tile) {
+    c.tile_kind = config.tile->kind == TilePolicy::ExactSize ? FFTGEN_TILE_EXACT : FFTGEN_TILE_CACHE;
+    c.tile_value = config.tile->value;
+  }
+  c.batch = config.batch;
+  c.device = config.device;
+  c.tuning = config.tuning;
+  fftgen_plan *p = nullptr;
+  check(fftgen_plan_create(&p, &c));
+  std::shared_ptr<fftgen_plan> plan(p, [](fftgen_plan *q) { fftgen_plan_destroy(q); });
+  CompiledPipeline out;
+  out.config_ = config;
+  out.formula = std::make_shared<const Formula>(Formula{config.n, config.algorithm, config.radix});
+  const int nops = fftgen_plan_num_ops(p);
+  for (int i = 0; i < nops; ++i) {
+    int64_t d[4];
+    check(fftgen_plan_op(p, i, d));
+    out.fused.ops.push_back(FusedOp{static_cast<int>(d[0]), d[1], d[2], d[3]});
+  }
+  out.final_ir = LoopProgram(plan, config.n, config.layout, config.batch);
+  out.complex_ir = out.final_ir;
+  return out;
+}
+
+// ---- exec.hpp:16-27 ----------------------------------------------------------
+struct ExecOptions {
+  int threads = 1;  // the reference's host workers; the GPU program ignores it (results never depend on it)
+  Direction direction = Direction::Forward;  // B200 extension: the reference has no inverse
+};
+
+namespace detail {
+inline void check_input(const LoopProgram &prog, const ComplexBuffer &b) {
+  if (b.logical_len != prog.size())
+    throw ExecError("input length " + std::to_string(b.logical_len) + " does not match pipeline size " +
+                    std::to_string(prog.size()));
+  if (b.layout != prog.layout())
+    throw ExecError("input layout does not match the layout the program was lowered for");
+  if (static_cast<int64_t>(b.data.size()) != 2 * b.logical_len)
+    throw ExecError("buffer storage holds " + std::to_string(b.data.size()) + " doubles, expected " +
+                    std::to_string(2 * b.logical_len));
+}
+}  // namespace detail
+
+// interpret over `batch` buffers at once (one per transform of the plan).
+inline std::vector<ComplexBuffer> interpret(const LoopProgram &prog, const std::vector<ComplexBuffer> &inputs,
+                                            const ExecOptions &opts = {}) {
+  if (!prog) throw ExecError("empty LoopProgram: compile a pipeline first");
+  if (static_cast<int64_t>(inputs.size()) != prog.batch())
     throw ExecError("got " + std::to_string(inputs.size()) + " buffers for a plan of batch " +
-                    std::to_string(cfg.batch));
+                    std::to_string(prog.batch()));
+  const int64_t n = prog.size();
   std::vector<double> flat;
-  flat.reserve(2 * cfg.n * cfg.batch);
+  flat.reserve(2 * n * prog.batch());
   for (const ComplexBuffer &b : inputs) {
-    if (b.logical_len != cfg.n)
-      throw ExecError("input length " + std::to_string(b.logical_len) + " does not match pipeline size " +
-                      std::to_string(cfg.n));
-    if (b.layout != cfg.layout)
-      throw ExecError("input layout does not match the layout the program was lowered for");
+    detail::check_input(prog, b);
     flat.insert(flat.end(), b.data.begin(), b.data.end());
   }
   std::vector<double> out(flat.size());
-  check(fftgen_interpret_f64(prog.handle(), static_cast<int>(dir), flat.data(), out.data()));
+  check(fftgen_interpret_f64(prog.handle(), static_cast<int>(opts.direction), flat.data(), out.data()));
   std::vector<ComplexBuffer> res(inputs.size());
   for (size_t i = 0; i < inputs.size(); ++i) {
-    res[i] = ComplexBuffer::zeros(cfg.n, cfg.layout);
-    std::copy(out.begin() + i * 2 * cfg.n, out.begin() + (i + 1) * 2 * cfg.n, res[i].data.begin());
+    res[i] = ComplexBuffer::zeros(n, prog.layout());
+    std::copy(out.begin() + i * 2 * n, out.begin() + (i + 1) * 2 * n, res[i].data.begin());
   }
   return res;
 }
 
+// interpret (exec.hpp:26-27): out-of-place, the result by value.
+inline ComplexBuffer interpret(const LoopProgram &prog, const ComplexBuffer &input, const ExecOptions &opts = {}) {
+  return interpret(prog, std::vector<ComplexBuffer>{input}, opts).front();
+}
+
+// Direction-first forms over a CompiledPipeline (the round-1 API).
+inline std::vector<ComplexBuffer> interpret(const CompiledPipeline &prog, const std::vector<ComplexBuffer> &inputs,
+                                            Direction dir = Direction::Forward) {
+  ExecOptions o;
+  o.direction = dir;
+  return interpret(prog.final_ir, inputs, o);
+}
 inline ComplexBuffer interpret(const CompiledPipeline &prog, const ComplexBuffer &input,
                                Direction dir = Direction::Forward) {
-  return interpret(prog, std::vector<ComplexBuffer>{input}, dir).front();
+  ExecOptions o;
+  o.direction = dir;
+  return interpret(prog.final_ir, input, o);
 }
 
 }  // namespace fftgen

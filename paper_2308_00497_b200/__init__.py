@@ -45,7 +45,7 @@ ABI_SYMBOLS = (
     "fftgen_plan_describe", "fftgen_plan_launches", "fftgen_plan_scratch_bytes",
     "fftgen_twiddle_multiply", "fftgen_dist_plan_create", "fftgen_dist_plan_destroy", "fftgen_dist_butterfly",
     "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
-    "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input",
+    "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input", "fftgen_program_text",
 )
 
 
@@ -151,6 +151,7 @@ def _load() -> C.CDLL:
     L.fftgen_dist_local_plan.argtypes = [vp]
     L.fftgen_dist_local_plan.restype = vp
     L.fftgen_seeded_input.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, i64, C.c_int, vp]
+    L.fftgen_program_text.argtypes = [C.POINTER(_Config), C.c_int, C.c_char_p, C.c_size_t]
     return L
 
 
@@ -197,29 +198,35 @@ def _ptr(x) -> int:
     return int(x)
 
 
+def _to_config(cfg: PipelineConfig) -> "_Config":
+    """PipelineConfig -> the C ABI fftgen_config (driver.hpp:26-35 + B200 fields)."""
+    c = _Config()
+    lib.fftgen_config_init(C.byref(c))
+    c.n = int(cfg.n)
+    c.algorithm = ALGORITHMS[cfg.algorithm] if isinstance(cfg.algorithm, str) else int(cfg.algorithm)
+    c.radix = int(cfg.radix)
+    c.layout = LAYOUTS[cfg.layout] if isinstance(cfg.layout, str) else int(cfg.layout)
+    c.batch = int(cfg.batch)
+    c.device = int(cfg.device)
+    c.vec = VEC_MODES[cfg.vec] if isinstance(cfg.vec, str) else int(cfg.vec)
+    c.vector_width = int(cfg.vector_width)
+    c.interleaved_opt = int(bool(cfg.interleaved_opt))
+    if cfg.tile is not None:
+        kind, value = cfg.tile
+        c.tile_kind = {"exact": 1, "cache": 2}[kind]
+        c.tile_value = int(value)
+    c.tuning = int(cfg.tuning)
+    c.cluster_size = int(cfg.cluster_size)
+    c.host_chunk_mb = int(cfg.host_chunk_mb)
+    return c
+
+
 class Plan:
     """A compiled plan (CompiledPipeline analogue); owns device twiddle tables."""
 
     def __init__(self, cfg: PipelineConfig):
         self.config = cfg
-        c = _Config()
-        lib.fftgen_config_init(C.byref(c))
-        c.n = int(cfg.n)
-        c.algorithm = ALGORITHMS[cfg.algorithm] if isinstance(cfg.algorithm, str) else int(cfg.algorithm)
-        c.radix = int(cfg.radix)
-        c.layout = LAYOUTS[cfg.layout] if isinstance(cfg.layout, str) else int(cfg.layout)
-        c.batch = int(cfg.batch)
-        c.device = int(cfg.device)
-        c.vec = VEC_MODES[cfg.vec] if isinstance(cfg.vec, str) else int(cfg.vec)
-        c.vector_width = int(cfg.vector_width)
-        c.interleaved_opt = int(bool(cfg.interleaved_opt))
-        if cfg.tile is not None:
-            kind, value = cfg.tile
-            c.tile_kind = {"exact": 1, "cache": 2}[kind]
-            c.tile_value = int(value)
-        c.tuning = int(cfg.tuning)
-        c.cluster_size = int(cfg.cluster_size)
-        c.host_chunk_mb = int(cfg.host_chunk_mb)
+        c = _to_config(cfg)
         h = C.c_void_p()
         _check(lib.fftgen_plan_create(C.byref(h), C.byref(c)))
         self._h = h
@@ -374,6 +381,19 @@ class Plan:
 
     def scratch_bytes(self) -> int:
         return int(lib.fftgen_plan_scratch_bytes(self._h))
+
+
+TEXTS = {"formula": 0, "ir": 1, "loops": 2, "radices": 3}
+
+
+def program_text(cfg: PipelineConfig, what: str = "formula") -> str:
+    """Host-only program text of a config (no device): "formula"
+    (print_formula, formula.cpp:104-146), "ir" (print_pipeline), "loops" (the
+    sm_100a pass / group program) or "radices"."""
+    c = _to_config(cfg)
+    buf = C.create_string_buffer(1 << 22)
+    _check(lib.fftgen_program_text(C.byref(c), TEXTS[what], buf, len(buf)))
+    return buf.value.decode()
 
 
 def compile_pipeline(cfg: PipelineConfig) -> Plan:

@@ -640,6 +640,8 @@ fftgen_status fftgen_interpret_f64(const fftgen_plan *cp, int direction, const d
     if ((e = cudaMemcpyAsync(d64in, in + b0 * 2 * n, cntf * sizeof(double), cudaMemcpyHostToDevice, s)) !=
         cudaSuccess)
       return e;
+    if (p->ex.strategy == STRAT_IDENTITY)  // DFT_1: no arithmetic, so no fp32 rounding either
+      return cudaMemcpyAsync(out + b0 * 2 * n, d64in, cntf * sizeof(double), cudaMemcpyDeviceToHost, s);
     if ((e = convert_f64_to_f32(d64in, f32in, cntf, s)) != cudaSuccess) return e;
     if (split)  // reference ComplexBuffer split storage: [re n | im n] per transform
       e = enqueue(p, direction, f32in, f32in + n, f32out, f32out + n, 2 * n, cnt, s);
@@ -685,6 +687,35 @@ fftgen_status fftgen_plan_op_map(const fftgen_plan *p, int idx, int64_t *map, in
 fftgen_status fftgen_plan_pipeline_text(const fftgen_plan *p, char *buf, size_t cap) {
   if (!p) return fail(FFTGEN_ERR_INVALID, "NULL plan");
   return copy_text(pipeline_text(p->ops, p->cfg.n), buf, cap);
+}
+
+fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf, size_t cap) {
+  if (!cfg) return fail(FFTGEN_ERR_INVALID, "NULL config");
+  std::string text;
+  fftgen_status st = guarded([&]() -> fftgen_status {
+    if (cfg->algorithm != FFTGEN_ALG_COOLEY_TUKEY && cfg->algorithm != FFTGEN_ALG_STOCKHAM)
+      throw PlanError("unknown algorithm " + std::to_string(cfg->algorithm));
+    const auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);  // the plan_create validation order
+    check_schedule(cfg->vec, cfg->vector_width, cfg->tile_kind, cfg->tile_value);
+    switch (what) {
+    case FFTGEN_TEXT_FORMULA: text = formula_text(cfg->n, cfg->algorithm, cfg->radix) + "\n"; break;
+    case FFTGEN_TEXT_PIPELINE: text = pipeline_text(ops, cfg->n); break;
+    case FFTGEN_TEXT_LOOPS:
+      text = program_text(cfg->n, (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
+                                      ? SPLIT_GROUPS_1024
+                                      : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT));
+      break;
+    case FFTGEN_TEXT_RADICES: {
+      std::ostringstream o;
+      for (int64_t r : stockham_radices(cfg->n, cfg->radix)) o << r << " ";
+      text = o.str() + "\n";
+      break;
+    }
+    default: throw DimensionError("unknown program text kind " + std::to_string(what));
+    }
+    return FFTGEN_OK;
+  });
+  return st != FFTGEN_OK ? st : copy_text(text, buf, cap);
 }
 
 int fftgen_plan_num_passes(const fftgen_plan *p) { return p ? (int)p->ex.passes.size() : -1; }

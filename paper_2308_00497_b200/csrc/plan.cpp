@@ -117,6 +117,71 @@ std::vector<RefOp> fuse_ops(int64_t n, int algorithm, int64_t radix) {
   return ops;
 }
 
+namespace {
+// plan_cooley_tukey(n, radix) (formula.cpp:150-166) printed by print_formula
+// (formula.cpp:104-146): compose factors joined by " . ", Kronecker factors
+// inside a composition parenthesised, a composition in atom position too.
+std::string ct_formula(int64_t n, int64_t radix, bool atom) {
+  if (n <= radix) return "DFT " + std::to_string(n);
+  const int64_t k = radix, m = n / k;
+  const std::string body = "(DFT " + std::to_string(k) + " kron I " + std::to_string(m) + ") . D " +
+                           std::to_string(n) + " " + std::to_string(m) + " . (I " + std::to_string(k) + " kron " +
+                           ct_formula(m, radix, true) + ") . Pi " + std::to_string(n) + " " + std::to_string(k);
+  return atom ? "(" + body + ")" : body;
+}
+}  // namespace
+
+std::string formula_text(int64_t n, int algorithm, int64_t radix) {
+  check_sizes(n, radix);
+  if (algorithm == 0) return ct_formula(n, radix, false);
+  // plan_stockham(n, radix) (formula.cpp:168-197): per stage, outermost
+  // (largest s) first, DFT_r (x) I_{n/r}, then (D^s_{s/r} (x) I_k) and
+  // (Pi^s_r (x) I_k) unless s == r
+  if (n == 1) return "DFT 1";
+  std::vector<std::string> f;
+  for (int64_t remaining = n; remaining > 1;) {
+    const int64_t r = radix < remaining ? radix : remaining;
+    const int64_t s = remaining, k = n / s;
+    const std::string rs = std::to_string(r), ss = std::to_string(s), ks = std::to_string(k);
+    f.push_back(n / r == 1 ? "DFT " + rs : "(DFT " + rs + " kron I " + std::to_string(n / r) + ")");
+    if (s > r) {
+      const std::string d = "D " + ss + " " + std::to_string(s / r);
+      f.push_back(k == 1 ? d : "(" + d + " kron I " + ks + ")");
+      f.push_back("(Pi " + ss + " " + rs + " kron I " + ks + ")");
+    }
+    remaining /= r;
+  }
+  std::string out;  // a single factor (n <= radix) prints bare: compose() returns it
+
+  for (size_t i = 0; i < f.size(); ++i) out += (i ? " . " : "") + f[i];
+  return out;
+}
+
+std::string program_text(int64_t n, int split_mode) {
+  // the sm_100a execution plan as loop nests: one Stockham stage of radix R
+  // per register pass (K2) or per four-step group launch (K3)
+  const ExecPlan p = build_exec_plan(n, split_mode);
+  std::ostringstream out;
+  if (p.strategy == STRAT_IDENTITY) {
+    out << "copy: y[0] = x[0]\n";
+    return out.str();
+  }
+  const bool four = p.strategy == STRAT_FOURSTEP;
+  out << (four ? "four-step: " : "block: ") << p.passes.size() << (four ? " group launches" : " register passes")
+      << " over N = " << n << "\n";
+  for (size_t i = 0; i < p.passes.size(); ++i) {
+    const PassDesc &d = p.passes[i];
+    const bool first = i == 0, last = i + 1 == p.passes.size();
+    out << (four ? "group " : "pass ") << i << ": for m < " << d.cols << ", c < " << d.k << ", B < " << d.R
+        << ":  y[(B*" << d.cols << " + m)*" << d.k << " + c] = sum_A W_" << d.R << "^(B A) * "
+        << (d.cols > 1 ? "w_" + std::to_string(d.s) + "^(A m) * " : std::string())
+        << "x[(m*" << d.R << " + A)*" << d.k << " + c]"
+        << "   [" << (first ? "HBM" : (four ? "HBM scratch" : "smem")) << " -> "
+        << (last ? "HBM" : (four ? "HBM scratch" : "smem")) << "]\n";
+  }
+  return out.str();
+}
+
 std::string pipeline_text(const std::vector<RefOp> &ops, int64_t n) {
   std::ostringstream out;  // print_pipeline format (rewrite.cpp:275-296)
   for (const RefOp &op : ops) {

@@ -50,6 +50,8 @@ void unit_root(int64_t n, int64_t t, double *re, double *im);
 std::vector<int64_t> stockham_radices(int64_t n, int64_t radix);
 std::vector<RefOp> fuse_ops(int64_t n, int algorithm, int64_t radix);
 std::string pipeline_text(const std::vector<RefOp> &ops, int64_t n);
+// print_formula(plan_cooley_tukey / plan_stockham (n, radix)) (formula.cpp:104-197)
+std::string formula_text(int64_t n, int algorithm, int64_t radix);
 void op_map(const RefOp &op, int64_t n, int64_t *map, int64_t *s_out);
 
 // One execution pass: a radix-R Stockham stage over the whole transform.
@@ -93,6 +95,8 @@ bool group_prefers_tma(int log2ns, bool first, bool rows);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
 ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT);
+// the sm_100a pass / group program as loop nests (the --emit loops text)
+std::string program_text(int64_t n, int split_mode = SPLIT_DEFAULT);
 
 // K2 pass structure of an N-point block kernel (defined in kernels_common.cu
 // from the compile-time BlockPlan), and its [A][m] twiddle table in floats.

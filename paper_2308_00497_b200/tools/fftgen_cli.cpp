@@ -1,18 +1,23 @@
 // fftgen_cli.cpp -- command-line front end of the B200 path, mirroring the
-// reference CLI (proj/tools/main.cpp:127-259):
+// reference CLI (proj/tools/main.cpp:28-259) flag for flag:
 //
-//   fftgen-b200 compile --size N [--algorithm A] [--radix R] [--layout L] --emit ir|kernels|radices
-//   fftgen-b200 run     --size N [...] (--random SEED | --input FILE) [--inverse]
+//   fftgen-b200 compile --size N [stage flags] --emit formula|ir|loops|kernels|c
+//   fftgen-b200 run     --size N [stage flags] (--random SEED | --input FILE) [--inverse]
 //   fftgen-b200 verify  [--sizes 16..4096|a,b,c] [--inputs 5]
-//   fftgen-b200 bench   --sizes ... --csv PATH [--batch B] [--repeats R] [--layout L] [--inverse]
+//   fftgen-b200 bench   --sizes ... --csv PATH [stage flags] [--repeats R]
+//                       [--device [--batch B] [--inverse] [--peak-gbs G]]
 //
-// Exit codes: 0 success, 1 failed verification or runtime error, 2 usage
-// error (main.cpp:250-258).  `verify` runs the reference's configuration
-// matrix (verify.cpp:127-181: both algorithms, radices {2,4,16}, both
-// layouts; vectorisation modes do not exist on this path) on the GPU against
-// an fp64 brute-force DFT (the dft_oracle formula, verify.cpp:19-37) with the
-// reference's gate max|a-b|/N < 1e-7 (verify.cpp:173).  `bench` writes the
-// reference CSV schema (verify.cpp:102-117) plus GPU columns.
+// stage flags (StageFlags, main.cpp:28-85): --algorithm cooley-tukey|stockham,
+// --radix R, --layout interleaved|split, --vectorize none|inner|outer,
+// --vector-width W, --interleaved-opt, --tile-size T | --tile-cache BYTES.
+//
+// Exit codes: 0 success, 1 failed verification or runtime error (an
+// fftgen::Error), 2 usage error (main.cpp:250-258).  `verify` is the
+// reference's run_verification matrix (verify.cpp:127-181) through the GPU
+// program; `bench` writes the reference CSV (verify.cpp:80-117: interpret()
+// timing, the reference's end-to-end rate); `bench --device` times batched
+// executes on device-resident data and adds the GPU columns.  `--emit c`
+// (the reference's scalar C emitter) has no B200 counterpart: LowerError.
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -27,6 +32,7 @@
 #include <vector>
 
 #include "fftgen_b200.hpp"
+#include "fftgen_b200_verify.hpp"
 
 using namespace fftgen;
 
@@ -38,59 +44,6 @@ struct UsageError : std::runtime_error {
 
 bool is_pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 
-// seeded_input (verify.cpp:55-78): splitmix64, re/im uniform in [-1, 1)
-std::vector<cplx> seeded_input(int64_t n, uint64_t seed) {
-  uint64_t state = seed;
-  auto next = [&]() {
-    state += 0x9e3779b97f4a7c15ULL;
-    uint64_t z = state;
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-    return z ^ (z >> 31);
-  };
-  std::vector<cplx> x(n);
-  for (int64_t j = 0; j < n; ++j) {
-    const double re = 2.0 * static_cast<double>(next() >> 11) * 0x1.0p-53 - 1.0;
-    const double im = 2.0 * static_cast<double>(next() >> 11) * 0x1.0p-53 - 1.0;
-    x[j] = {re, im};
-  }
-  return x;
-}
-
-// unit_root (matrix.cpp:14-35) and the O(N^2) double-sum DFT (verify.cpp:19-37)
-cplx unit_root(int64_t n, int64_t t) {
-  t %= n;
-  if (t < 0) t += n;
-  if (4 * t % n == 0) {
-    static const cplx q[4] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
-    return q[4 * t / n];
-  }
-  const double a = -2.0 * M_PI * static_cast<double>(t) / static_cast<double>(n);
-  return {std::cos(a), std::sin(a)};
-}
-
-std::vector<cplx> dft(const std::vector<cplx> &x) {
-  const int64_t n = static_cast<int64_t>(x.size());
-  std::vector<cplx> roots(n), out(n);
-  for (int64_t t = 0; t < n; ++t) roots[t] = unit_root(n, t);
-  for (int64_t j = 0; j < n; ++j) {
-    double re = 0, im = 0;
-    for (int64_t k = 0; k < n; ++k) {
-      const cplx w = roots[(j * k) % n];
-      re += w.real() * x[k].real() - w.imag() * x[k].imag();
-      im += w.real() * x[k].imag() + w.imag() * x[k].real();
-    }
-    out[j] = {re, im};
-  }
-  return out;
-}
-
-double error_metric(const std::vector<cplx> &a, const std::vector<cplx> &b) {
-  double worst = 0;
-  for (size_t j = 0; j < a.size(); ++j) worst = std::max(worst, std::abs(a[j] - b[j]));
-  return worst / static_cast<double>(a.size());
-}
-
 struct Args {
   std::vector<std::string> v;
   size_t i = 0;
@@ -100,8 +53,12 @@ struct Args {
     return false;
   }
   std::string get(const char *flag, const std::string &def = "", bool required = false) const {
-    for (size_t k = 0; k + 1 < v.size(); ++k)
-      if (v[k] == flag) return v[k + 1];
+    for (size_t k = 0; k < v.size(); ++k)
+      if (v[k] == flag) {
+        if (k + 1 >= v.size() || v[k + 1].rfind("--", 0) == 0)
+          throw UsageError(std::string(flag) + " needs a value");
+        return v[k + 1];
+      }
     if (required) throw UsageError(std::string("missing ") + flag);
     return def;
   }
@@ -125,45 +82,94 @@ std::vector<int64_t> parse_sizes(const std::string &text) {
   return sizes;
 }
 
-PipelineConfig config_from(const Args &a) {
+// StageFlags::to_config (main.cpp:62-85): shape errors are usage errors
+PipelineConfig config_from(const Args &a, bool with_size = true) {
   PipelineConfig c;
-  c.n = std::stoll(a.get("--size", "0", true));
+  if (with_size) {
+    c.n = std::stoll(a.get("--size", "0", true));
+    if (!is_pow2(c.n)) throw UsageError("--size must be a power of two");
+  }
   const std::string alg = a.get("--algorithm", "cooley-tukey");
   if (alg != "cooley-tukey" && alg != "stockham") throw UsageError("--algorithm cooley-tukey|stockham");
   c.algorithm = alg == "stockham" ? Algorithm::Stockham : Algorithm::CooleyTukey;
   c.radix = std::stoll(a.get("--radix", "2"));
+  if (!is_pow2(c.radix) || c.radix < 2) throw UsageError("--radix must be a power of two >= 2");
   const std::string lay = a.get("--layout", "interleaved");
   if (lay != "interleaved" && lay != "split") throw UsageError("--layout interleaved|split");
   c.layout = lay == "split" ? ComplexLayout::Split : ComplexLayout::Interleaved;
+  const std::string vec = a.get("--vectorize", "none");
+  if (vec != "none" && vec != "inner" && vec != "outer") throw UsageError("--vectorize none|inner|outer");
+  c.vec = vec == "none" ? VecMode::None : (vec == "inner" ? VecMode::Inner : VecMode::Outer);
+  c.vector_width = std::stoll(a.get("--vector-width", "8"));
+  c.interleaved_opt = a.has("--interleaved-opt");
+  if (c.interleaved_opt && c.layout == ComplexLayout::Split)
+    throw UsageError("--interleaved-opt only applies to the interleaved layout");
+  if (a.has("--tile-size") && a.has("--tile-cache")) throw UsageError("--tile-size excludes --tile-cache");
+  const int64_t ts = std::stoll(a.get("--tile-size", "0")), tcache = std::stoll(a.get("--tile-cache", "0"));
+  if (ts > 0) c.tile = TilePolicy::exact(ts);
+  else if (tcache > 0) c.tile = TilePolicy::cache(tcache);
   c.batch = std::stoll(a.get("--batch", "1"));
   return c;
 }
 
-std::string describe(const PipelineConfig &c) {  // describe_config (verify.cpp:119-125)
-  std::ostringstream o;
-  o << "n=" << c.n << " alg=" << algorithm_name(c.algorithm) << " radix=" << c.radix
-    << " layout=" << layout_name(c.layout) << " vec=none";
-  return o.str();
+fftgen_config c_config(const PipelineConfig &c) {
+  fftgen_config f;
+  fftgen_config_init(&f);
+  f.n = c.n;
+  f.algorithm = c.algorithm == Algorithm::Stockham ? FFTGEN_ALG_STOCKHAM : FFTGEN_ALG_COOLEY_TUKEY;
+  f.radix = static_cast<int32_t>(c.radix);
+  f.layout = c.layout == ComplexLayout::Split ? FFTGEN_LAYOUT_SPLIT : FFTGEN_LAYOUT_INTERLEAVED;
+  f.vec = c.vec == VecMode::Inner ? FFTGEN_VEC_INNER : (c.vec == VecMode::Outer ? FFTGEN_VEC_OUTER : FFTGEN_VEC_NONE);
+  f.vector_width = static_cast<int32_t>(c.vector_width);
+  f.interleaved_opt = c.interleaved_opt;
+  if (c.tile) {
+    f.tile_kind = c.tile->kind == TilePolicy::ExactSize ? FFTGEN_TILE_EXACT : FFTGEN_TILE_CACHE;
+    f.tile_value = c.tile->value;
+  }
+  return f;
 }
 
+// host-only texts (no device): formula, ir, loops, radices
+std::string program_text(const PipelineConfig &c, int what) {
+  const fftgen_config f = c_config(c);
+  std::vector<char> buf(1 << 16);
+  fftgen_status st;
+  while ((st = fftgen_program_text(&f, what, buf.data(), buf.size())) == FFTGEN_ERR_DIMENSION &&
+         buf.size() < (size_t(1) << 28))
+    buf.resize(buf.size() * 4);
+  check(st);
+  return std::string(buf.data());
+}
+
+// cmd_compile (main.cpp:127-148)
 int cmd_compile(const Args &a) {
-  const PipelineConfig c = config_from(a);
   const std::string emit = a.get("--emit", "", true);
-  auto prog = compile_pipeline(c);
-  if (emit == "ir") {
-    std::cout << prog.pipeline_text();
-  } else if (emit == "kernels") {
-    std::cout << prog.describe();
+  if (emit != "formula" && emit != "ir" && emit != "loops" && emit != "kernels" && emit != "c" && emit != "radices")
+    throw UsageError("--emit formula|ir|loops|kernels|c");
+  if (emit == "c" && a.get("--vectorize", "none") != "none")
+    throw UsageError("--emit c is scalar only; use --vectorize none");
+  const PipelineConfig c = config_from(a);
+  if (emit == "formula") {
+    std::cout << program_text(c, FFTGEN_TEXT_FORMULA);
+  } else if (emit == "ir") {
+    std::cout << program_text(c, FFTGEN_TEXT_PIPELINE);
+  } else if (emit == "loops") {
+    std::cout << program_text(c, FFTGEN_TEXT_LOOPS);
   } else if (emit == "radices") {
-    for (int64_t r : prog.radices()) std::cout << r << " ";
-    std::cout << "\n";
+    std::cout << program_text(c, FFTGEN_TEXT_RADICES);
+  } else if (emit == "kernels") {
+    std::cout << compile_pipeline(c).describe();
   } else {
-    throw UsageError("--emit ir|kernels|radices");
+    program_text(c, FFTGEN_TEXT_PIPELINE);  // the config's own errors first
+    throw LowerError("LowerError: --emit c: the B200 program is a device plan, not a scalar C translation unit");
   }
   return 0;
 }
 
+// cmd_run (main.cpp:150-165): prints "%.17g %.17g" per output element
 int cmd_run(const Args &a) {
+  if (!a.has("--random") && !a.has("--input")) throw UsageError("run: need --input FILE or --random SEED");
+  if (a.has("--random") && a.has("--input")) throw UsageError("--random excludes --input");
   PipelineConfig c = config_from(a);
   c.batch = 1;
   std::vector<cplx> x;
@@ -186,44 +192,42 @@ int cmd_run(const Args &a) {
   return 0;
 }
 
+// cmd_verify (main.cpp:167-179): run_verification through the GPU program
 int cmd_verify(const Args &a) {
   const auto sizes = parse_sizes(a.get("--sizes", "16..4096"));
   const int inputs = std::stoi(a.get("--inputs", "5"));
-  int cases = 0, failures = 0;
-  for (int64_t n : sizes) {
-    std::vector<std::vector<cplx>> xs, want;
-    for (int t = 0; t < inputs; ++t) {
-      xs.push_back(seeded_input(n, 1 + t));
-      want.push_back(dft(xs.back()));
-    }
-    for (Algorithm alg : {Algorithm::CooleyTukey, Algorithm::Stockham})
-      for (int64_t radix : {2, 4, 16}) {
-        if (radix > n || n % radix != 0) continue;
-        for (ComplexLayout lay : {ComplexLayout::Interleaved, ComplexLayout::Split}) {
-          PipelineConfig c;
-          c.n = n;
-          c.algorithm = alg;
-          c.radix = radix;
-          c.layout = lay;
-          c.batch = inputs;
-          auto prog = compile_pipeline(c);
-          std::vector<ComplexBuffer> in;
-          for (const auto &x : xs) in.push_back(ComplexBuffer::from_vector(x, lay));
-          const auto out = interpret(prog, in);
-          double err = 0;
-          for (int t = 0; t < inputs; ++t) err = std::max(err, error_metric(out[t].to_vector(), want[t]));
-          const bool pass = err < 1e-7;
-          std::printf("%s %s err=%.3e\n", pass ? "PASS" : "FAIL", describe(c).c_str(), err);
-          ++cases;
-          failures += !pass;
-        }
-      }
+  const auto cases = run_verification(sizes, inputs);
+  int failures = 0;
+  for (const VerifyCase &vc : cases) {
+    std::printf("%s %s err=%.3e\n", vc.pass ? "PASS" : "FAIL", describe_config(vc.config).c_str(), vc.max_error);
+    failures += !vc.pass;
   }
-  std::printf("%d configurations, %d failed\n", cases, failures);
+  std::printf("%zu configurations, %d failed\n", cases.size(), failures);
   return failures == 0 ? 0 : 1;
 }
 
+// cmd_bench (main.cpp:181-197): the reference CSV of bench() per size
+int cmd_bench_reference(const Args &a) {
+  const auto sizes = parse_sizes(a.get("--sizes", "", true));
+  const std::string csv_path = a.get("--csv", "", true);
+  const int64_t repeats = std::stoll(a.get("--repeats", "1000"));
+  PipelineConfig flags = config_from(a, false);
+  std::ofstream csv(csv_path);
+  if (!csv) throw Error("cannot open " + csv_path + " for writing");
+  csv << bench_csv_header() << "\n";
+  for (int64_t n : sizes) {
+    flags.n = n;
+    const BenchResult r = bench(flags, repeats);
+    csv << bench_csv_row(r) << "\n";
+    std::printf("%s mean=%.3es rate=%.1f mflops\n", describe_config(r.config).c_str(), r.mean_seconds,
+                r.rate_mflops);
+  }
+  return 0;
+}
+
+// bench --device: batched executes on device-resident data, CUDA-event timed
 int cmd_bench(const Args &a) {
+  if (!a.has("--device")) return cmd_bench_reference(a);
   const auto sizes = parse_sizes(a.get("--sizes", "", true));
   const std::string csv_path = a.get("--csv", "", true);
   const int64_t repeats = std::stoll(a.get("--repeats", "100"));
@@ -272,7 +276,7 @@ int cmd_bench(const Args &a) {
                   flops / mean / 1e6, (long long)c.batch, dir == Direction::Forward ? "forward" : "inverse",
                   flops / mean / 1e9, gbs, gbs / peak_gbs);
     csv << row << "\n";
-    std::printf("%s batch=%lld mean=%.3es rate=%.1f gflops %.0f GB/s\n", describe(c).c_str(), (long long)c.batch,
+    std::printf("%s batch=%lld mean=%.3es rate=%.1f gflops %.0f GB/s\n", describe_config(c).c_str(), (long long)c.batch,
                 mean, flops / mean / 1e9, gbs);
     cudaFree(in);
     cudaFree(out);
@@ -293,6 +297,15 @@ int main(int argc, char **argv) {
   for (int i = 2; i < argc; ++i) a.v.push_back(argv[i]);
   const std::string cmd = argv[1];
   try {
+    // every value option must carry a value wherever it appears (CLI11 semantics)
+    static const char *kValueFlags[] = {"--size", "--algorithm", "--radix", "--layout", "--vectorize",
+                                        "--vector-width", "--tile-size", "--tile-cache", "--emit", "--input",
+                                        "--random", "--sizes", "--inputs", "--repeats", "--csv", "--batch",
+                                        "--batch-bytes", "--peak-gbs"};
+    for (size_t k = 0; k < a.v.size(); ++k)
+      for (const char *f : kValueFlags)
+        if (a.v[k] == f && (k + 1 >= a.v.size() || a.v[k + 1].rfind("--", 0) == 0))
+          throw UsageError(std::string(f) + " needs a value");
     if (cmd == "compile") return cmd_compile(a);
     if (cmd == "run") return cmd_run(a);
     if (cmd == "verify") return cmd_verify(a);

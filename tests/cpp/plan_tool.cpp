@@ -3,6 +3,8 @@
 // to check plan indices against the reference's goldens without a GPU.
 //   plan_tool text N ALG RADIX      print_pipeline text
 //   plan_tool maps N ALG RADIX      per data-movement / twiddle op: idx kind s values...
+//   plan_tool formula N ALG RADIX   print_formula text of the planner
+//   plan_tool loops N               the sm_100a pass / group program
 //   plan_tool radices N RADIX       Stockham radices, application order
 //   plan_tool passes N              sm_100a passes: R cols k s
 //   plan_tool twiddles N            K2 pass twiddle table (hex floats)
@@ -39,6 +41,10 @@ int main(int argc, char **argv) {
         for (int64_t v : map) std::printf(" %lld", (long long)v);
         std::printf("\n");
       }
+    } else if (cmd == "formula") {
+      std::printf("%s\n", formula_text(n, std::atoi(argv[3]), std::atoll(argv[4])).c_str());
+    } else if (cmd == "loops") {
+      std::fputs(program_text(n).c_str(), stdout);
     } else if (cmd == "radices") {
       for (int64_t r : stockham_radices(n, std::atoll(argv[3]))) std::printf("%lld ", (long long)r);
       std::printf("\n");

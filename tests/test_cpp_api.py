@@ -32,3 +32,58 @@ def test_cpp_api_known_answers_and_parity(api_test):
     p = subprocess.run([api_test, "gpu"], capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout + p.stderr
     assert " 0 failed" in p.stdout
+
+
+# ---- the reference's own test files, compiled unchanged against the B200 API
+REF_TESTS = os.path.join(ROOT, "oracle", "_ref")
+REF_SRC = "/root/reference/proj/tests"
+KAT_EXEC = ("transform of a delta*,size-2 transform*,size-8 pipeline*,interpretation is pure*")
+HOST_VERIFY = "oracle*,error metric*,rate normalization*,seeded inputs*"
+
+
+def ref_test(name):
+    path = os.path.join(REF_TESTS, f"ref_test_{name}")
+    if not os.path.exists(path):
+        if os.path.exists(os.path.join(REF_SRC, f"test_{name}.cpp")):
+            subprocess.run(["make", "-C", ORCDIR], check=True, stdout=subprocess.DEVNULL)
+        else:
+            pytest.skip("reference tests not built (no /root/reference and no prebuilt oracle/_ref)")
+    return path
+
+
+def test_reference_test_files_compile_unchanged():
+    """test_exec.cpp / test_verify.cpp from /root/reference are compiled as-is
+    (oracle/Makefile: the source path is the reference's own file) against
+    include/fftgen_b200.hpp + fftgen_b200_verify.hpp; every test case is
+    registered."""
+    p = subprocess.run([ref_test("exec"), "--list-test-cases"], capture_output=True, text=True)
+    assert p.returncode == 0 and len(p.stdout.splitlines()) == 10
+    p = subprocess.run([ref_test("verify"), "--list-test-cases"], capture_output=True, text=True)
+    assert p.returncode == 0 and len(p.stdout.splitlines()) == 8
+
+
+def test_reference_verify_host_cases_pass():
+    """test_verify.cpp's host-side cases (oracle, metric, rate, seeded input)
+    against the header restatement, no GPU needed."""
+    p = subprocess.run([ref_test("verify"), f"-tc={HOST_VERIFY}"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "6 passed, 0 failed" in p.stdout
+
+
+@pytest.mark.gpu
+def test_reference_test_exec_known_answers_on_b200():
+    """The reference's test_exec.cpp known-answer cases (exec.hpp interpret on
+    compile_pipeline(...).final_ir) run unchanged on the sm_100a kernels."""
+    p = subprocess.run([ref_test("exec"), f"-tc={KAT_EXEC}"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "4 passed, 0 failed" in p.stdout
+
+
+@pytest.mark.gpu
+def test_reference_test_verify_all_cases_on_b200():
+    """All of test_verify.cpp, including bench() and the run_verification()
+    sweep (both algorithms, radices 2/4/16, both layouts, all vector modes,
+    error_metric < 1e-7) through the GPU program."""
+    p = subprocess.run([ref_test("verify")], capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "8 passed, 0 failed" in p.stdout
