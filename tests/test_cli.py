@@ -86,7 +86,8 @@ def test_verify_matrix_passes():
     lines = p.stdout.splitlines()
     assert lines[-1].endswith(", 0 failed")
     assert all(l.startswith("PASS ") for l in lines[:-1])
-    assert len(lines) - 1 == sum(2 * len([r for r in (2, 4, 16) if r <= n]) * 2 for n in [16 << i for i in range(9)])
+    # both algorithms x radices {2,4,16} x (5 vector modes interleaved + 3 split), verify.cpp:136-155
+    assert len(lines) - 1 == sum(2 * len([r for r in (2, 4, 16) if r <= n]) * 8 for n in [16 << i for i in range(9)])
 
 
 @pytest.mark.gpu
@@ -125,8 +126,8 @@ def test_reference_test_cli_host_cases():
 
 @pytest.mark.gpu
 def test_reference_test_cli_all_cases():
-    """Every case of the reference's test_cli.cpp against fftgen-b200: formula
+    """All seven cases of the reference's test_cli.cpp against fftgen-b200: formula
     text, run --size 1 identity, input files, byte-stable emits, usage exit
     codes, the verify sweep and the bench CSV schema."""
     p = subprocess.run([ref_cli_test()], capture_output=True, text=True, timeout=900)
-    assert p.returncode == 0 and "6 passed, 0 failed" in p.stdout, p.stdout + p.stderr
+    assert p.returncode == 0 and "7 passed, 0 failed" in p.stdout, p.stdout + p.stderr
