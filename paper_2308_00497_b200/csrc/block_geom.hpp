@@ -266,6 +266,68 @@ template <int N> struct Tma1Geom {
 #ifndef FFTGEN_GROUP_TILE_HUGE
 #define FFTGEN_GROUP_TILE_HUGE 131072
 #endif
+// Transform stride REG of a group tile's exchange (float2 between the TC
+// transforms): lanes walk the tile index f fastest on the column-mapped
+// sides (f = l % TC, t = l / TC), and the first-pass writer of the rows group
+// walks t (f = l / T).  With TC >= 16 any odd stride puts a half-warp's 16
+// transforms on distinct bank pairs; with TC = 4 / 8 (the NS = 2^11 / 2^12
+// tiles) a half-warp mixes f and t, so the stride is searched here by
+// simulating every pass boundary's accesses like PadSearch (ideal: 2
+// wavefronts per warp access).
+template <int NS, int TC, class PL> struct GroupRegSearch {
+  using G = BlockGeom<NS, 0, PL>;
+  static constexpr Pad PAD0 = BoundaryPad<NS, 0, 8, PL>::value;
+  static constexpr Pad PAD1 = G::P > 2 ? BoundaryPad<NS, 1, 8, PL>::value : Pad{16, 0};
+  static constexpr int side_cost(int p, int side, bool rows_map, int reg) {
+    const int T = G::T, q = p + side;
+    const int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / G::R(q);
+    const Pad pd = p == 0 ? PAD0 : PAD1;
+    const int xs[4] = {0, 1, R / 2, R - 1};
+    const int js[2] = {0, J - 1};
+    int worst = 0;
+    for (int jj = 0; jj < 2; ++jj)
+      for (int xx = 0; xx < 4; ++xx) {
+        int wavefronts = 0;
+        for (int half = 0; half < 2; ++half) {
+          int cnt[16] = {};
+          int deg = 0;
+          for (int l = 16 * half; l < 16 * half + 16; ++l) {
+            const int f = rows_map ? l / T : l % TC, t = rows_map ? l % T : l / TC;
+            if (f >= TC || t >= T) continue;
+            const int u = t + js[jj] * T, m = u / k, c = u % k, x = xs[xx];
+            const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
+            const int b = (padded(idx, pd) + f * reg) % 16;
+            cnt[b]++;
+            deg = cnt[b] > deg ? cnt[b] : deg;
+          }
+          wavefronts += deg;
+        }
+        worst = wavefronts > worst ? wavefronts : worst;
+      }
+    return worst;
+  }
+  static constexpr int cost(int reg) {
+    int worst = 0;
+    for (int p = 0; p + 1 < G::P; ++p) {
+      int w = side_cost(p, 0, false, reg);
+      if (p == 0) {
+        const int wr = side_cost(p, 0, true, reg);
+        w = wr > w ? wr : w;
+      }
+      const int r = side_cost(p, 1, false, reg);
+      w = r > w ? r : w;
+      worst = w > worst ? w : worst;
+    }
+    return worst;
+  }
+  static constexpr int best(int base) {  // base: the odd default; move only when strictly better
+    int br = base, bc = cost(base);
+    for (int r = base + 1; r < base + 32; ++r)
+      if (cost(r) < bc) bc = cost(r), br = r;
+    return br;
+  }
+};
+
 template <int NS, int MAXT = 512> struct GroupGeom {
   using PL = GroupPlan<NS>;
   static constexpr int T = BlockGeom<NS, 0, PL>::T;
@@ -276,7 +338,11 @@ template <int NS, int MAXT = 512> struct GroupGeom {
   using G = BlockGeom<NS, TC, PL>;
   static constexpr int THREADS = G::THREADS;
   static constexpr int EX = SmemGeom<NS, PL>::BASE > NS ? SmemGeom<NS, PL>::BASE : NS;
-  static constexpr int REG = EX | 1;  // odd float2 stride: lanes over f hit distinct banks
+  // float2 stride between the tile's transforms: odd (lanes over f hit
+  // distinct bank pairs) unless the simulated accesses find a better one
+  static constexpr int REG = GroupRegSearch<NS, TC, PL>::best(EX | 1);
+  static constexpr int REG_WAVEFRONTS = GroupRegSearch<NS, TC, PL>::cost(REG);
+  static constexpr int REG_WAVEFRONTS_ODD = GroupRegSearch<NS, TC, PL>::cost(EX | 1);
   static constexpr int BYTES = TC * REG * 8;
   // resident CTAs the register budget must allow: 16-point codelets fit 64
   // registers, 32-point ones (NS >= 512) need 128
