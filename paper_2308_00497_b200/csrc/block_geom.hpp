@@ -347,7 +347,7 @@ template <int NS, int MAXT = 512> struct GroupGeom {
   // resident CTAs the register budget must allow: 16-point codelets fit 64
   // registers, 32-point ones (NS >= 512) need 128
   static constexpr int MIN_BLOCKS =
-      NS >= 2048 ? 1 : (G::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3)));
+      NS >= 2048 ? (TILE_BYTES > 65536 ? 1 : 2) : (G::RMAX > 16 ? 2 : (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 3)));
   static constexpr int R0 = G::R(0);
   static constexpr int K0 = NS / R0;
 };
