@@ -242,6 +242,13 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *plan, char *buf, size_t ca
  *   FFTGEN_TEXT_RADICES   the Stockham radices, application order */
 enum { FFTGEN_TEXT_FORMULA = 0, FFTGEN_TEXT_PIPELINE = 1, FFTGEN_TEXT_LOOPS = 2, FFTGEN_TEXT_RADICES = 3 };
 fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf, size_t cap);
+/* The device-generated twiddle tables of four-step group `group` (K4; parity
+ * introspection): which 0 = Q[A0][m] = w_s^{A0 (NS/R0) m} (R0 x cols), which 1
+ * = P = w_s^{c m} ([c][m] for column groups, [m][c] for the rows group),
+ * copied to `out` as (re, im) float pairs, at most `cap` elements.  Returns the
+ * table's element count, 0 for a group without a table (cols == 1), -1 on a
+ * bad argument. */
+int64_t fftgen_plan_group_twiddles(const fftgen_plan *plan, int group, int which, float *out, int64_t cap);
 /* Kernel launches one fftgen_execute issues (for launch accounting). */
 int fftgen_plan_launches(const fftgen_plan *plan);
 size_t fftgen_plan_scratch_bytes(const fftgen_plan *plan);

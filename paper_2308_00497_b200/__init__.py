@@ -46,6 +46,7 @@ ABI_SYMBOLS = (
     "fftgen_twiddle_multiply", "fftgen_dist_plan_create", "fftgen_dist_plan_destroy", "fftgen_dist_butterfly",
     "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
     "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input", "fftgen_program_text",
+    "fftgen_plan_group_twiddles",
 )
 
 
@@ -152,6 +153,8 @@ def _load() -> C.CDLL:
     L.fftgen_dist_local_plan.restype = vp
     L.fftgen_seeded_input.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, i64, C.c_int, vp]
     L.fftgen_program_text.argtypes = [C.POINTER(_Config), C.c_int, C.c_char_p, C.c_size_t]
+    L.fftgen_plan_group_twiddles.argtypes = [vp, C.c_int, C.c_int, vp, i64]
+    L.fftgen_plan_group_twiddles.restype = i64
     return L
 
 
@@ -378,6 +381,16 @@ class Plan:
 
     def launches(self) -> int:
         return int(lib.fftgen_plan_launches(self._h))
+
+    def group_twiddles(self, group: int, which: int) -> np.ndarray:
+        """Device twiddle table of a four-step group (0: Q, 1: P) as complex64."""
+        cnt = int(lib.fftgen_plan_group_twiddles(self._h, group, which, None, 0))
+        if cnt < 0:
+            _check(5)
+        out = np.empty(max(cnt, 0), dtype=np.complex64)
+        if cnt:
+            lib.fftgen_plan_group_twiddles(self._h, group, which, out.ctypes.data, cnt)
+        return out
 
     def scratch_bytes(self) -> int:
         return int(lib.fftgen_plan_scratch_bytes(self._h))

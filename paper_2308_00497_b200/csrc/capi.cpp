@@ -718,6 +718,27 @@ fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf,
   return st != FFTGEN_OK ? st : copy_text(text, buf, cap);
 }
 
+int64_t fftgen_plan_group_twiddles(const fftgen_plan *p, int group, int which, float *out, int64_t cap) {
+  if (!p || p->ex.strategy != STRAT_FOURSTEP || group < 0 || group >= (int)p->ex.groups.size() ||
+      (which != 0 && which != 1) || cap < 0 || (cap > 0 && !out)) {
+    fail(FFTGEN_ERR_INVALID, "bad plan, group or table");
+    return -1;
+  }
+  const GroupDesc &d = p->ex.groups[group];
+  if (d.cols <= 1) return 0;
+  const int64_t count = which == 0 ? d.r0 * d.cols : (d.ns / d.r0) * d.cols;
+  const int64_t m = std::min(count, cap);
+  if (m > 0) {
+    DeviceGuard g(p->cfg.device);
+    const float2 *src = p->d_twg + (which == 0 ? d.q_off : d.p_off);
+    if (cudaMemcpy(out, src, (size_t)m * sizeof(float2), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      fail(FFTGEN_ERR_CUDA, "twiddle table copy");
+      return -1;
+    }
+  }
+  return count;
+}
+
 int fftgen_plan_num_passes(const fftgen_plan *p) { return p ? (int)p->ex.passes.size() : -1; }
 
 fftgen_status fftgen_plan_pass(const fftgen_plan *p, int idx, int64_t desc[4]) {
