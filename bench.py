@@ -386,6 +386,13 @@ def run_ours(a):
         except Exception as e:  # reported, never silently replaced
             cpu = {"value": None, "error": str(e)}
 
+    if e2e and cpu and cpu.get("value"):
+        # the end-to-end speed-up against both of the reference's CPU paths on
+        # this host: its execute API (interpret, the reference arm) and its
+        # ahead-of-time emitted C for the same plan (the faster, honest one)
+        aot = (cpu.get("aot_emit_c") or {}).get("value")
+        e2e["vs_cpu"] = {"reference_interpret": round(e2e["value"] / cpu["value"], 1),
+                         "reference_emit_c": round(e2e["value"] / aot, 2) if aot else None}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_per_step, 4),
