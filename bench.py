@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON)")
     ap.add_argument("--workload", choices=["batched", "distributed"], default="batched",
                     help="distributed: one N-point transform over all ranks (config C5, e.g. --n 1073741824)")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="distributed: NCCL all-to-alls, or the exchanges fused into the kernels over symmetric memory")
     ap.add_argument("--launch-selftest", action="store_true",
                     help="CPU check of the rank launcher: gloo ranks all-reduce MAX of their rank")
     return ap.parse_args()
@@ -550,7 +552,10 @@ def run_distributed(a):
     # rank r's block of the reference input x = seeded_input(n, 1), generated on the device
     x = torch.view_as_complex(fg.seeded_input(n, 1, "interleaved", seed0=1, device=local)[0][rank * m:(rank + 1) * m])
     x = x.contiguous()
-    d = DistributedFFT(n, device=local)
+    d = DistributedFFT(n, device=local, transport=a.transport)
+    if a.transport == "p2p":
+        d.input_block().copy_(x)
+        x = d.input_block()  # zero-copy input: the symmetric block itself
     out = torch.empty_like(x)
     direction = fg.FORWARD if a.direction == "forward" else fg.INVERSE
     for _ in range(a.warmup):
@@ -569,24 +574,39 @@ def run_distributed(a):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t[0])
     # per-stage device times of one execute (events between the stages)
-    w0, w1 = d.workspace(x)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-    ev[0].record()
-    d.exchange(x, w0); ev[1].record()
-    d.stages.butterfly(w0, w1, direction); ev[2].record()
-    d.exchange(w1, w0); ev[3].record()
-    d.stages.local(w0, w1, direction); ev[4].record()
-    d.exchange(w1, w0); ev[5].record()
-    d.stages.unpack(w0, out); ev[6].record()
+    if a.transport == "p2p":
+        names = ["barrier1", "butterfly+exchanges1,2", "barrier2", "local", "barrier3", "unpack+exchange3"]
+        xb, rb, zb = d._blocks[0], d._blocks[1], d._blocks[2]
+        ev[0].record()
+        d._barrier(); ev[1].record()
+        d.stages.butterfly_peers(d._peer["x"], d._peer["recv"], direction); ev[2].record()
+        d._barrier(); ev[3].record()
+        d.stages.local(rb, zb, direction); ev[4].record()
+        d._barrier(); ev[5].record()
+        d.stages.unpack_peers(d._peer["z"], out); ev[6].record()
+        d._barrier()
+    else:
+        names = ["exchange1", "butterfly", "exchange2", "local", "exchange3", "unpack"]
+        if world == 1:
+            w0, w1 = torch.empty_like(x), torch.empty_like(x)
+        else:
+            w0, w1 = d.workspace(x)
+        ev[0].record()
+        d.exchange(x, w0); ev[1].record()
+        d.stages.butterfly(w0, w1, direction); ev[2].record()
+        d.exchange(w1, w0); ev[3].record()
+        d.stages.local(w0, w1, direction); ev[4].record()
+        d.exchange(w1, w0); ev[5].record()
+        d.stages.unpack(w0, out); ev[6].record()
     torch.cuda.synchronize(dev)
-    names = ["exchange1", "butterfly", "exchange2", "local", "exchange3", "unpack"]
     stages = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(6)], device=dev, dtype=torch.float64)
     dist.all_reduce(stages, op=dist.ReduceOp.MAX)
     probe = a2a_probe(m, dev, world)
     # e2e: the rank's block from pinned host memory in, the result back out, every step
     h_in = x.cpu().pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
-    d_in = torch.empty_like(x)
+    d_in = x if a.transport == "p2p" else torch.empty_like(x)
     e2e_steps = max(1, a.e2e_steps)
     dist.barrier()
     t0 = time.perf_counter()
@@ -606,7 +626,7 @@ def run_distributed(a):
             pass
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         st = {k: round(float(v), 4) for k, v in zip(names, stages)}
-        xms = st["exchange1"] + st["exchange2"] + st["exchange3"]
+        xms = sum(v for k, v in st.items() if "exchange" in k)
         wire = 3 * 8 * m * (world - 1) / world
         local_plan = d.stages.describe_local().splitlines()
         print(json.dumps({
@@ -616,7 +636,9 @@ def run_distributed(a):
             "data": "synthetic: the reference's seeded_input(N, 1) (verify.cpp:55-78) generated on the device, "
                     "block-distributed", "impl": "ours",
             "config": {"workload": f"single c2c fp32 FFT N={n} block-distributed over {world} GPU(s): "
-                                   f"P-point butterfly + local N/P plan + unpack, 3 contiguous all-to-alls",
+                                   f"P-point butterfly + local N/P plan + unpack, 3 contiguous all-to-alls "
+                                   f"({'fused into the kernels over symmetric memory' if a.transport == 'p2p' else 'NCCL'})",
+                       "transport": a.transport,
                        "n": n, "block_per_gpu": m, "chunk": m // world, "direction": a.direction,
                        "l2": "blocks of 8N/P bytes exceed the 126 MB L2 for N >= 2^25; no flush"},
             "stages_ms": st,

@@ -195,6 +195,21 @@ typedef int (*fftgen_exchange_fn)(void *ctx, const void *send, void *recv, size_
 /* The whole pipeline above on one rank with the caller's exchange. */
 fftgen_status fftgen_dist_execute(const fftgen_dist_plan *plan, int direction, const void *in, void *out,
                                   void *work0, void *work1, fftgen_exchange_fn exchange, void *ctx, void *stream);
+/* Peer-memory transport: every rank's blocks are mapped into this process
+ * (CUDA IPC / symmetric memory over NVLink, or plain device buffers when the
+ * ranks are emulated on one GPU) and the exchanges run inside the kernels:
+ *   butterfly_peers: reads chunk `rank` of every rank's input block
+ *     (in_blocks[r], exchange 1 as loads) and writes row k_b into slot `rank`
+ *     of rank k_b's receive block (recv_blocks[k_b], exchange 2 as stores);
+ *   local (fftgen_dist_local) on the rank's own receive block -> z;
+ *   unpack_peers: reads slot `rank` of every rank's z block (z_blocks[q'],
+ *     exchange 3 as loads) into the rank's natural-order output.
+ * Tables hold `world` device pointers; the caller orders the stages across
+ * ranks (a barrier between them when the ranks are separate processes). */
+fftgen_status fftgen_dist_butterfly_peers(const fftgen_dist_plan *plan, int direction, const void *const *in_blocks,
+                                          void *const *recv_blocks, void *stream);
+fftgen_status fftgen_dist_unpack_peers(const fftgen_dist_plan *plan, const void *const *z_blocks, void *out,
+                                       void *stream);
 /* Elements per exchange chunk (n/world^2) and the rank's block (n/world). */
 int64_t fftgen_dist_chunk_elems(const fftgen_dist_plan *plan);
 int64_t fftgen_dist_block_elems(const fftgen_dist_plan *plan);

@@ -46,7 +46,7 @@ ABI_SYMBOLS = (
     "fftgen_twiddle_multiply", "fftgen_dist_plan_create", "fftgen_dist_plan_destroy", "fftgen_dist_butterfly",
     "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
     "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input", "fftgen_program_text",
-    "fftgen_plan_group_twiddles",
+    "fftgen_plan_group_twiddles", "fftgen_dist_butterfly_peers", "fftgen_dist_unpack_peers",
 )
 
 
@@ -154,6 +154,8 @@ def _load() -> C.CDLL:
     L.fftgen_seeded_input.argtypes = [C.c_int, i64, i64, C.c_uint64, vp, vp, i64, C.c_int, vp]
     L.fftgen_program_text.argtypes = [C.POINTER(_Config), C.c_int, C.c_char_p, C.c_size_t]
     L.fftgen_plan_group_twiddles.argtypes = [vp, C.c_int, C.c_int, vp, i64]
+    L.fftgen_dist_butterfly_peers.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp), vp]
+    L.fftgen_dist_unpack_peers.argtypes = [vp, C.POINTER(vp), vp, vp]
     L.fftgen_plan_group_twiddles.restype = i64
     return L
 
@@ -526,6 +528,26 @@ class DistPlan:
     def unpack(self, recv, out, stream=None) -> None:
         _check(lib.fftgen_dist_unpack(self._h, self._buf("recv", recv), self._buf("out", out),
                                       self._stream(stream, self.device)))
+
+    # ---- peer-memory transport (exchanges fused into the kernels) --------
+    def _table(self, name, blocks):
+        if len(blocks) != self.world:
+            raise DimensionError(f"{name}: {len(blocks)} blocks for world {self.world}")
+        ptrs = [int(b) if isinstance(b, int) else self._buf(name, b) for b in blocks]
+        return (C.c_void_p * self.world)(*ptrs)
+
+    def butterfly_peers(self, in_blocks, recv_blocks, direction: int = FORWARD, stream=None) -> None:
+        """Exchange 1 + butterfly + exchange 2 in one kernel: in_blocks[r] /
+        recv_blocks[r] are rank r's input / receive blocks (tensors on this
+        device, or raw peer-mapped addresses)."""
+        _check(lib.fftgen_dist_butterfly_peers(self._h, direction, self._table("in", in_blocks),
+                                               self._table("recv", recv_blocks), self._stream(stream, self.device)))
+
+    def unpack_peers(self, z_blocks, out, stream=None) -> None:
+        """Exchange 3 + unpack in one kernel: pulls slot `rank` of every rank's
+        local-result block z_blocks[q] into this rank's output."""
+        _check(lib.fftgen_dist_unpack_peers(self._h, self._table("z", z_blocks), self._buf("out", out),
+                                            self._stream(stream, self.device)))
 
     def describe_local(self) -> str:
         buf = C.create_string_buffer(1 << 16)

@@ -162,6 +162,49 @@ fftgen_status fftgen_dist_unpack(const fftgen_dist_plan *p, const void *recv, vo
   return e == cudaSuccess ? FFTGEN_OK : dcuda(e, "distributed unpack");
 }
 
+// pointer tables of the P ranks' blocks, 16-byte aligned, disjoint from out
+static fftgen_status check_peers(const fftgen_dist_plan *p, const void *const *peers, const char *what) {
+  if (!p) return dfail(FFTGEN_ERR_INVALID, "NULL plan");
+  if (!peers) return dfail(FFTGEN_ERR_EXEC, std::string("NULL ") + what + " pointer table");
+  for (int r = 0; r < p->world; ++r) {
+    if (!peers[r]) return dfail(FFTGEN_ERR_EXEC, std::string(what) + " block of rank " + std::to_string(r) + " is NULL");
+    if ((uintptr_t)peers[r] % 16) return dfail(FFTGEN_ERR_EXEC, "distributed buffers must be 16-byte aligned");
+  }
+  return FFTGEN_OK;
+}
+
+fftgen_status fftgen_dist_butterfly_peers(const fftgen_dist_plan *p, int direction, const void *const *in_blocks,
+                                          void *const *recv_blocks, void *stream) {
+  fftgen_status st;
+  if ((st = check_peers(p, in_blocks, "input")) != FFTGEN_OK ||
+      (st = check_peers(p, (const void *const *)recv_blocks, "receive")) != FFTGEN_OK)
+    return st;
+  if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
+    return dfail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
+  Guard g(p->device);
+  if (g.err != cudaSuccess) return dcuda(g.err, "cudaSetDevice");
+  cudaError_t e = dist_butterfly_peers(p->world, direction, (const float2 *const *)in_blocks,
+                                       (float2 *const *)recv_blocks, p->l1, (int64_t)p->rank * p->l1, p->d_tlo,
+                                       p->d_thi, p->h, p->log2n, (cudaStream_t)stream);
+  return e == cudaSuccess ? FFTGEN_OK : dcuda(e, "distributed peer butterfly");
+}
+
+fftgen_status fftgen_dist_unpack_peers(const fftgen_dist_plan *p, const void *const *z_blocks, void *out,
+                                       void *stream) {
+  fftgen_status st = check_peers(p, z_blocks, "local-result");
+  if (st != FFTGEN_OK) return st;
+  if (!out || (uintptr_t)out % 16) return dfail(FFTGEN_ERR_EXEC, "output block NULL or not 16-byte aligned");
+  for (int r = 0; r < p->world; ++r) {
+    const uintptr_t a = (uintptr_t)z_blocks[r], b = (uintptr_t)out, bytes = (uintptr_t)p->m * 8;
+    if (a < b + bytes && b < a + bytes) return dfail(FFTGEN_ERR_EXEC, "distributed stages are out of place");
+  }
+  Guard g(p->device);
+  if (g.err != cudaSuccess) return dcuda(g.err, "cudaSetDevice");
+  cudaError_t e = dist_unpack_peers(p->world, (const float2 *const *)z_blocks, (float2 *)out, p->l1,
+                                    (int64_t)p->rank * p->l1, (cudaStream_t)stream);
+  return e == cudaSuccess ? FFTGEN_OK : dcuda(e, "distributed peer unpack");
+}
+
 fftgen_status fftgen_dist_execute(const fftgen_dist_plan *p, int direction, const void *in, void *out, void *w0,
                                   void *w1, fftgen_exchange_fn exchange, void *ctx, void *stream) {
   if (!p) return dfail(FFTGEN_ERR_INVALID, "NULL plan");

@@ -97,6 +97,71 @@ __global__ void __launch_bounds__(256) dist_unpack_kernel(const float2 *__restri
   }
 }
 
+// ---- peer-memory variants: the exchanges fused into the kernels -----------
+// With every rank's blocks mapped into this process (CUDA IPC / symmetric
+// memory over NVLink; or plain device buffers when the ranks are emulated on
+// one GPU), exchange 1 becomes the butterfly's loads (chunk q of each rank's
+// input block, read over NVLink), exchange 2 its stores (row k_b straight
+// into slot q of rank k_b's receive block), and exchange 3 + unpack one pull
+// kernel: no NCCL kernels, no staging copies -- each element crosses NVLink
+// once per exchange, inside the compute kernel.
+struct PeerPtrs {
+  const float2 *p[16];
+};
+struct PeerOut {
+  float2 *p[16];
+};
+
+template <int P, int DIR>
+__global__ void __launch_bounds__(256) dist_butterfly_peer_kernel(PeerPtrs src, PeerOut dst, int64_t l1, int64_t a0,
+                                                                  const float2 *__restrict__ tlo,
+                                                                  const float2 *__restrict__ thi, int h, int64_t nmask) {
+  const int64_t step = 2 * (int64_t)gridDim.x * blockDim.x;
+  const int64_t lomask = (int64_t(1) << h) - 1;
+  for (int64_t j = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); j < l1; j += step) {
+    float2 v0[P], v1[P];
+#pragma unroll
+    for (int r = 0; r < P; ++r) {  // chunk q (offset a0) of rank r's block
+      const float4 t = __ldcs(reinterpret_cast<const float4 *>(src.p[r] + a0 + j));
+      v0[r] = make_float2(t.x, t.y);
+      v1[r] = make_float2(t.z, t.w);
+    }
+    reg_fft<P, DIR>(v0);
+    reg_fft<P, DIR>(v1);
+    const int64_t a = a0 + j;
+#pragma unroll
+    for (int kb = 1; kb < P; ++kb) {
+      const int64_t e0 = (a * kb) & nmask, e1 = ((a + 1) * kb) & nmask;
+      v0[kb] = mul_tw<DIR>(v0[kb], cprod(__ldg(tlo + (e0 & lomask)), __ldg(thi + (e0 >> h))));
+      v1[kb] = mul_tw<DIR>(v1[kb], cprod(__ldg(tlo + (e1 & lomask)), __ldg(thi + (e1 >> h))));
+    }
+#pragma unroll
+    for (int kb = 0; kb < P; ++kb)  // slot q of rank k_b's receive block
+      __stcs(reinterpret_cast<float4 *>(dst.p[kb] + a0 + j), make_float4(v0[kb].x, v0[kb].y, v1[kb].x, v1[kb].y));
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) dist_unpack_peer_kernel(PeerPtrs src, float2 *__restrict__ out, int64_t l1,
+                                                               int64_t s0) {
+  const int64_t step = 2 * (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); j < l1; j += step) {
+    float4 t[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) t[q] = __ldcs(reinterpret_cast<const float4 *>(src.p[q] + s0 + j));
+    float4 *o = reinterpret_cast<float4 *>(out + P * j);
+    if constexpr (P == 1) {
+      __stcs(o, t[0]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < P; q += 2) {
+        __stcs(o + q / 2, make_float4(t[q].x, t[q].y, t[q + 1].x, t[q + 1].y));
+        __stcs(o + (P + q) / 2, make_float4(t[q].z, t[q].w, t[q + 1].z, t[q + 1].w));
+      }
+    }
+  }
+}
+
 // out[i] = w_n^{(i step) mod n}: fp64 sincospi of an exact argument, exact at
 // quadrant multiples (unit_root, matrix.cpp:14-35), rounded once to fp32
 __global__ void gen_pow_kernel(float2 *__restrict__ out, int64_t count, int64_t step, int64_t n) {
@@ -136,9 +201,54 @@ cudaError_t butterfly_dispatch(int p, const float2 *in, float2 *out, int64_t l1,
   return cudaGetLastError();
 }
 
+template <int DIR>
+cudaError_t butterfly_peer_dispatch(int p, const PeerPtrs &src, const PeerOut &dst, int64_t l1, int64_t a0,
+                                    const float2 *tlo, const float2 *thi, int h, int64_t nmask, cudaStream_t s) {
+  const unsigned g = stream_grid(l1);
+  switch (p) {
+  case 1: dist_butterfly_peer_kernel<1, DIR><<<g, 256, 0, s>>>(src, dst, l1, a0, tlo, thi, h, nmask); break;
+  case 2: dist_butterfly_peer_kernel<2, DIR><<<g, 256, 0, s>>>(src, dst, l1, a0, tlo, thi, h, nmask); break;
+  case 4: dist_butterfly_peer_kernel<4, DIR><<<g, 256, 0, s>>>(src, dst, l1, a0, tlo, thi, h, nmask); break;
+  case 8: dist_butterfly_peer_kernel<8, DIR><<<g, 256, 0, s>>>(src, dst, l1, a0, tlo, thi, h, nmask); break;
+  case 16: dist_butterfly_peer_kernel<16, DIR><<<g, 256, 0, s>>>(src, dst, l1, a0, tlo, thi, h, nmask); break;
+  default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool dist_world_supported(int p) { return p == 1 || p == 2 || p == 4 || p == 8 || p == 16; }
+
+cudaError_t dist_butterfly_peers(int p, int dir, const float2 *const *src, float2 *const *dst, int64_t l1,
+                                 int64_t a0, const float2 *tlo, const float2 *thi, int h, int log2n, cudaStream_t s) {
+  if (p < 1 || p > 16) return cudaErrorInvalidValue;
+  PeerPtrs sp{};
+  PeerOut dp{};
+  for (int r = 0; r < p; ++r) {
+    sp.p[r] = src[r];
+    dp.p[r] = dst[r];
+  }
+  const int64_t nmask = (int64_t(1) << log2n) - 1;
+  return dir < 0 ? butterfly_peer_dispatch<-1>(p, sp, dp, l1, a0, tlo, thi, h, nmask, s)
+                 : butterfly_peer_dispatch<1>(p, sp, dp, l1, a0, tlo, thi, h, nmask, s);
+}
+
+cudaError_t dist_unpack_peers(int p, const float2 *const *src, float2 *out, int64_t l1, int64_t s0, cudaStream_t s) {
+  if (p < 1 || p > 16) return cudaErrorInvalidValue;
+  PeerPtrs sp{};
+  for (int r = 0; r < p; ++r) sp.p[r] = src[r];
+  const unsigned g = stream_grid(l1);
+  switch (p) {
+  case 1: dist_unpack_peer_kernel<1><<<g, 256, 0, s>>>(sp, out, l1, s0); break;
+  case 2: dist_unpack_peer_kernel<2><<<g, 256, 0, s>>>(sp, out, l1, s0); break;
+  case 4: dist_unpack_peer_kernel<4><<<g, 256, 0, s>>>(sp, out, l1, s0); break;
+  case 8: dist_unpack_peer_kernel<8><<<g, 256, 0, s>>>(sp, out, l1, s0); break;
+  case 16: dist_unpack_peer_kernel<16><<<g, 256, 0, s>>>(sp, out, l1, s0); break;
+  default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t dist_gen_tables(float2 *tlo, float2 *thi, int log2n, int h, cudaStream_t s) {
   const int64_t n = int64_t(1) << log2n, nlo = int64_t(1) << h, nhi = n >> h;

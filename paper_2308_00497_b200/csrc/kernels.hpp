@@ -116,6 +116,11 @@ cudaError_t dist_gen_tables(float2 *tlo, float2 *thi, int log2n, int h, cudaStre
 cudaError_t dist_butterfly(int p, int dir, const float2 *in, float2 *out, int64_t l1, int64_t a0, const float2 *tlo,
                            const float2 *thi, int h, int log2n, cudaStream_t s);
 cudaError_t dist_unpack(int p, const float2 *in, float2 *out, int64_t l1, cudaStream_t s);
+// peer-memory variants (exchanges fused into the loads / stores): src / dst
+// hold the P ranks' block base pointers
+cudaError_t dist_butterfly_peers(int p, int dir, const float2 *const *src, float2 *const *dst, int64_t l1,
+                                 int64_t a0, const float2 *tlo, const float2 *thi, int h, int log2n, cudaStream_t s);
+cudaError_t dist_unpack_peers(int p, const float2 *const *src, float2 *out, int64_t l1, int64_t s0, cudaStream_t s);
 
 // seeded_input (verify.cpp:55-78) for transforms b < batch, seed seed0 + b, fp32
 cudaError_t seeded_input(bool split, void *out0, void *out1, int64_t n, int64_t batch, uint64_t seed0, int64_t dist,

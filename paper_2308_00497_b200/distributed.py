@@ -26,6 +26,15 @@
   stages) and `EmulatedDistributedFFT` runs P ranks in lockstep on ONE GPU
   with the real kernels, the exchanges being device copies of the same
   chunks (tests/test_gpu_distributed.py).
+
+  transport="p2p" runs the same algebra with the exchanges INSIDE the
+  kernels over peer memory (torch symmetric memory: every rank's blocks are
+  mapped into every process over NVLink): the butterfly pulls chunk q of
+  every rank's input and pushes row k_b into rank k_b's receive block
+  (exchanges 1 and 2), the local plan runs on the rank's own block, and the
+  unpack pulls slot q of every rank's result (exchange 3) -- three kernels
+  (+ the local plan) and four device barriers, no NCCL kernels or staging
+  copies.
 """
 from __future__ import annotations
 
@@ -86,10 +95,13 @@ class DistributedFFT:
     `stages` supplies butterfly(recv, send, direction), local(inp, out,
     direction) and unpack(recv, out) on this rank's blocks; the default is the
     sm_100a DistPlan.  `exchange(send, recv)` defaults to
-    all_to_all_single over the group (a copy when the world is 1)."""
+    all_to_all_single over the group (a copy when the world is 1).
+    transport="p2p" fuses the exchanges into the kernels over symmetric
+    (peer-mapped) memory instead; `input_block()` is then the zero-copy
+    input buffer."""
 
     def __init__(self, n: int, group=None, device: Optional[int] = None, rank: Optional[int] = None,
-                 world: Optional[int] = None, stages=None):
+                 world: Optional[int] = None, stages=None, transport: str = "nccl"):
         r, w = _rank_world(group)
         self.group = group
         self.rank = r if rank is None else rank
@@ -104,6 +116,50 @@ class DistributedFFT:
             stages = DistPlan(n, self.world, self.rank, device)
         self.stages = stages
         self._work: dict = {}
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        self.transport = transport
+        self._symm = None
+        if transport == "p2p":
+            self._init_symmetric(device if device is not None else torch.cuda.current_device())
+
+    # ---- peer-memory transport ----------------------------------------------
+    def _init_symmetric(self, device: int) -> None:
+        """One symmetric allocation [input | receive | local result] per rank,
+        rendezvoused over the group: every rank's blocks become addressable
+        here (NVLink peer mappings)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        m = self.m
+        buf = symm_mem.empty(3 * m, dtype=torch.complex64, device=torch.device("cuda", device))
+        group = self.group if self.group is not None else dist.group.WORLD
+        handle = symm_mem.rendezvous(buf, group)
+        ptrs = [int(p) for p in handle.buffer_ptrs]
+        self._symm = (buf, handle)
+        self._blocks = buf.view(3, m)
+        self._peer = {name: [p + i * 8 * m for p in ptrs] for i, name in enumerate(("x", "recv", "z"))}
+
+    def input_block(self) -> torch.Tensor:
+        """p2p: this rank's input block in symmetric memory (fill it, then call
+        execute(input_block()) to skip the copy-in)."""
+        if self._symm is None:
+            raise RuntimeError("input_block() needs transport='p2p'")
+        return self._blocks[0]
+
+    def _barrier(self) -> None:
+        self._symm[1].barrier()
+
+    def _execute_p2p(self, x_local: torch.Tensor, direction: int, out: torch.Tensor) -> torch.Tensor:
+        x_blk, recv_blk, z_blk = self._blocks[0], self._blocks[1], self._blocks[2]
+        if x_local.data_ptr() != x_blk.data_ptr():
+            x_blk.copy_(x_local)
+        self._barrier()                       # every rank's input is in place
+        self.stages.butterfly_peers(self._peer["x"], self._peer["recv"], direction)
+        self._barrier()                       # every receive block is complete
+        self.stages.local(recv_blk, z_blk, direction)
+        self._barrier()                       # every local result is complete
+        self.stages.unpack_peers(self._peer["z"], out)
+        self._barrier()                       # no rank still reads this rank's blocks
+        return out
 
     def exchange(self, send: torch.Tensor, recv: torch.Tensor) -> None:
         """All-to-all of `world` contiguous chunks: send chunk q -> rank q, recv chunk r <- rank r."""
@@ -127,11 +183,13 @@ class DistributedFFT:
         x_local = x_local.reshape(-1)
         if out is None:
             out = torch.empty_like(x_local)
-        if self.world == 1:
+        if self.world == 1 and self.transport == "nccl":
             # P = 1: both exchanges, the 1-point butterfly (w^0 = 1) and the
             # stride-1 unpack are identities; the local plan is the transform
             self.stages.local(x_local, out, direction)
             return out
+        if self.transport == "p2p":
+            return self._execute_p2p(x_local, direction, out)
         w0, w1 = self.workspace(x_local)
         self.exchange(x_local, w0)
         self.stages.butterfly(w0, w1, direction)
@@ -157,8 +215,12 @@ class EmulatedDistributedFFT:
     three all-to-alls as device copies.  Tests the composition the NCCL path
     runs, on one GPU."""
 
-    def __init__(self, n: int, world: int, device: Optional[int] = None, stages_factory=None):
+    def __init__(self, n: int, world: int, device: Optional[int] = None, stages_factory=None,
+                 transport: str = "nccl"):
         check_geometry(n, world)
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        self.transport = transport
         self.n, self.world = n, world
         self.m = n // world
         self.l1 = self.m // world
@@ -175,6 +237,16 @@ class EmulatedDistributedFFT:
         w0 = [torch.empty_like(b) for b in blocks]
         w1 = [torch.empty_like(b) for b in blocks]
         out = [torch.empty_like(b) for b in blocks]
+        if self.transport == "p2p":
+            # the same peer-pointer kernels the multi-process path runs; stream
+            # order on one device stands in for the barriers between stages
+            for r in range(P):
+                self.stages[r].butterfly_peers(blocks, w0, direction)
+            for r in range(P):
+                self.stages[r].local(w0[r], w1[r], direction)
+            for r in range(P):
+                self.stages[r].unpack_peers(w1, out[r])
+            return out
         emulated_exchange(blocks, w0, self.l1)
         for r in range(P):
             self.stages[r].butterfly(w0[r], w1[r], direction)

@@ -165,6 +165,76 @@ def test_emulated_round_trip_2p22(fg, orc):
     assert np.linalg.norm(got - z) / np.linalg.norm(z) < 1e-6
 
 
+# ------------------------------------- peer-memory transport (fused exchanges)
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_emulated_p2p_bitwise_equals_nccl_path(fg, orc, world):
+    """The peer-pointer kernels (exchanges as loads / stores inside the
+    butterfly and unpack) compute exactly what the contiguous-chunk NCCL
+    pipeline computes: same arithmetic, other addresses -> bitwise equal."""
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    n = 1 << 20
+    x, z = seeded_complex(orc, n, seed=6)
+    blocks = blocks_of(z, world)
+    a = torch.cat(EmulatedDistributedFFT(n, world).execute(blocks))
+    b = torch.cat(EmulatedDistributedFFT(n, world, transport="p2p").execute(blocks))
+    assert torch.equal(a, b)
+    want = oracle.as_complex(orc.forward(x[None], "stockham", 4, threads=4))[0]
+    got = b.cpu().numpy()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 3e-6
+
+
+def test_emulated_p2p_2p30_tone(fg):
+    """C5 size through the fused peer kernels: the inverse of the tone
+    exp(+2 pi i k0 t / N) is N delta[k + k0 mod N]."""
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    n, world, k0 = 1 << 30, 4, 987654
+    outs = EmulatedDistributedFFT(n, world, transport="p2p").execute(tone_blocks(n, world, k0), 1)
+    m, peak = n // world, (-k0) % n
+    err2 = 0.0
+    for r, o in enumerate(outs):
+        o = o.to(torch.complex128)
+        if r * m <= peak < (r + 1) * m:
+            o[peak - r * m] -= n
+        err2 += float(torch.sum(o.real ** 2 + o.imag ** 2))
+        del o
+    assert math.sqrt(err2) / n < tol(n)
+
+
+def test_peer_tables_validated(fg):
+    p = fg.DistPlan(1 << 12, 2, 0)
+    x = torch.zeros(p.block, dtype=torch.complex64, device="cuda")
+    y = torch.zeros_like(x)
+    with pytest.raises(fg.DimensionError):
+        p.butterfly_peers([x], [y])
+    with pytest.raises(fg.ExecError):
+        p.butterfly_peers([x, 0], [y, y])
+    with pytest.raises(fg.ExecError):
+        p.unpack_peers([x, y], y)                  # out aliases a source block
+
+
+def test_distributed_p2p_symmetric_memory_world1(fg, orc):
+    """transport='p2p' under a real process group: torch symmetric memory
+    rendezvous, device barriers, the fused kernels (world 1 on this box)."""
+    import torch.distributed as dist
+    from paper_2308_00497_b200.distributed import DistributedFFT
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 1 << 22
+        try:
+            d = DistributedFFT(n, transport="p2p")
+        except Exception as e:  # symmetric memory unavailable in this configuration
+            pytest.skip(f"symmetric memory rendezvous failed: {e}")
+        x, z = seeded_complex(orc, n, seed=8)
+        d.input_block().copy_(torch.from_numpy(z).cuda())
+        got = d.execute(d.input_block()).cpu().numpy()
+        want = oracle.as_complex(orc.forward(x[None], "stockham", 4, threads=8))[0]
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) < 4e-6
+    finally:
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------- one rank, real NCCL
 def _free_port():
     s = socket.socket()
