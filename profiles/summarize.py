@@ -95,6 +95,17 @@ def summarize_rep(rep: str) -> tuple[str, list[dict]]:
                     continue
                 op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
                 byop[op.split(".")[0]] += to_float(r[iall]) or 0
+            # shared-memory wavefronts of the LSU instructions themselves
+            # (ld/st.shared): the kernel-level bank-conflict counter also
+            # counts the TMA / bulk-copy engine's smem traffic
+            try:
+                iw, ii = h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Ideal")
+                w = sum(to_float(r[iw]) or 0 for r in body if len(r) > max(iw, ii))
+                wi = sum(to_float(r[ii]) or 0 for r in body if len(r) > max(iw, ii))
+                lines.append(f"\nshared wavefronts of LSU instructions: {w:.0f}, ideal {wi:.0f}, "
+                             f"excess {w - wi:.0f} ({100 * (w - wi) / max(w, 1):.1f}%)")
+            except ValueError:
+                pass
             lines.append("\nstall samples by SASS opcode:")
             for op, v in sorted(byop.items(), key=lambda kv: -kv[1])[:12]:
                 lines.append(f"  {op:10s} {100 * v / max(tot, 1):5.1f}%")
