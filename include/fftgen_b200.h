@@ -29,14 +29,13 @@
  *   out-of-place, or exactly in place (out0 == in0, out1 == in1); partially
  *   overlapping input and output ranges are rejected with FFTGEN_ERR_EXEC.
  *   Kernels are enqueued on the caller's stream; the plan owns its twiddle
- *   tables and scratch.  Plan creation and destruction are thread-safe; a
- *   plan may be executed concurrently from several host threads on
- *   different streams only when it needs no scratch
- *   (fftgen_plan_scratch_bytes() == 0) and the data are 16-byte aligned with
- *   dist * element size a multiple of 16 (otherwise cluster plans fall back
- *   to the two-launch path, whose scratch is allocated by the first such
- *   execute; during CUDA-graph capture that first execute fails with
- *   FFTGEN_ERR_EXEC instead of allocating).
+ *   tables and scratch, all allocated at plan creation (an execute never
+ *   allocates, so executes can be captured in CUDA graphs).  Plan creation
+ *   and destruction are thread-safe; a plan may be executed concurrently from
+ *   several host threads on different streams only when its executes use no
+ *   scratch: block (N <= 2^14) plans, and cluster plans (2^15) on 16-byte
+ *   aligned data with dist * element size a multiple of 16 (unaligned data
+ *   takes the two-launch path through the plan's bounded fallback scratch).
  */
 #ifndef FFTGEN_B200_H
 #define FFTGEN_B200_H

@@ -89,14 +89,16 @@ struct fftgen_plan {
   // K3 four-step: device-generated group twiddles and intermediate buffers
   float2 *d_twg = nullptr;
   float2 *d_scratch = nullptr;
-  float2 *d_fallback = nullptr;  // scratch of cluster plans, on the first unaligned execute
+  // cluster plans: a bounded two-launch scratch (allocated with the plan) for
+  // data the TMA tiles cannot address (unaligned), used chunk by chunk
+  float2 *d_fallback = nullptr;
   size_t scratch_bytes = 0, fallback_bytes = 0;
+  int64_t fallback_chunk = 0;  // transforms per two-launch chunk
   // K3 groups: persistent TMA variant (resident CTAs per group, 0 = off)
   std::vector<int> group_tma_grid;
   // K5: 2-group plans run as one cluster per transform (DSMEM intermediate)
   bool use_cluster = false;
   int max_clusters = 0, cluster_size = 0;
-  std::mutex scratch_mu;  // lazy two-launch scratch of cluster plans (unaligned data)
   // host-buffer pipeline scratch (lazily allocated, guarded by mu)
   std::mutex mu;
   void *d_stage = nullptr;
@@ -212,6 +214,9 @@ cudaError_t launch_group(const fftgen_plan *p, int g, int direction, const void 
   return group_launch(d.log2ns, shape, direction, a, batch, s);
 }
 
+cudaError_t run_groups(const fftgen_plan *p, int direction, const void *in0, const void *in1, void *out0,
+                       void *out1, int64_t dist, int64_t batch, float2 *scratch, size_t per, cudaStream_t s);
+
 // Enqueue one execute over `batch` transforms on stream s (device pointers).
 cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const void *in1, void *out0,
                     void *out1, int64_t dist, int64_t batch, cudaStream_t s) {
@@ -277,33 +282,17 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
         return cluster_launch(gs[0].log2ns, gs[1].log2ns, p->cluster_size, layout, direction, c, batch,
                               p->max_clusters, s);
     }
-    float2 *scratch = p->d_scratch;
-    if (p->use_cluster) {
-      // TMA tiles need 16-byte aligned rows: unaligned data takes the
-      // two-launch path, whose full-batch scratch is allocated on first use
-      // (never inside a CUDA-graph capture, where cudaMalloc would break it)
-      auto *mp = const_cast<fftgen_plan *>(p);
-      std::lock_guard<std::mutex> lk(mp->scratch_mu);
-      if (!mp->d_fallback) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaError_t e = cudaStreamIsCapturing(s, &cs);
-        if (e != cudaSuccess) return e;
-        if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
-        const size_t need = (size_t)p->ex.scratch_buffers * (size_t)p->cfg.batch * (size_t)n * sizeof(float2);
-        if ((e = cudaMalloc(&mp->d_fallback, need)) != cudaSuccess) return e;
-        mp->fallback_bytes = need;
-      }
-      scratch = mp->d_fallback;
-    }
-    // groups ping-pong through interleaved scratch: in -> S0 [-> S1 -> S0 ...] -> out
-    const size_t per = (size_t)p->cfg.batch * (size_t)n;  // float2 per scratch buffer
-    for (size_t g = 0; g < gs.size(); ++g) {
-      const bool first = g == 0, last = g + 1 == gs.size();
-      float2 *src = first ? nullptr : scratch + ((g - 1) % p->ex.scratch_buffers) * per;
-      float2 *dst = last ? nullptr : scratch + (g % p->ex.scratch_buffers) * per;
-      cudaError_t e = launch_group(p, (int)g, direction, first ? in0 : src, first ? in1 : nullptr,
-                                   last ? out0 : dst, last ? out1 : nullptr, first ? dist : n, last ? dist : n,
-                                   batch, s);
+    // two-launch (K3) path; cluster plans run it chunk by chunk through
+    // their bounded fallback scratch (no allocation at execute time)
+    float2 *scratch = p->use_cluster ? p->d_fallback : p->d_scratch;
+    const int64_t chunk = p->use_cluster ? p->fallback_chunk : batch;
+    const int64_t esz_in = split ? 1 : 2;  // floats per element of a user plane
+    for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+      const int64_t cnt = std::min(chunk, batch - b0);
+      const int64_t off = b0 * dist * esz_in;  // float offset of the chunk in the user planes
+      const float *i0 = (const float *)in0 + off, *i1 = in1 ? (const float *)in1 + off : nullptr;
+      float *o0 = (float *)out0 + off, *o1 = out1 ? (float *)out1 + off : nullptr;
+      cudaError_t e = run_groups(p, direction, i0, i1, o0, o1, dist, cnt, scratch, (size_t)chunk * (size_t)n, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -311,6 +300,24 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
   default:
     return cudaErrorNotSupported;
   }
+}
+
+// The K3 group launches of one chunk of `batch` transforms; the groups
+// ping-pong through interleaved scratch buffers of `per` float2 each:
+// in -> S0 [-> S1 -> S0 ...] -> out.
+cudaError_t run_groups(const fftgen_plan *p, int direction, const void *in0, const void *in1, void *out0,
+                       void *out1, int64_t dist, int64_t batch, float2 *scratch, size_t per, cudaStream_t s) {
+  const auto &gs = p->ex.groups;
+  const int64_t n = p->cfg.n;
+  for (size_t g = 0; g < gs.size(); ++g) {
+    const bool first = g == 0, last = g + 1 == gs.size();
+    float2 *src = first ? nullptr : scratch + ((g - 1) % p->ex.scratch_buffers) * per;
+    float2 *dst = last ? nullptr : scratch + (g % p->ex.scratch_buffers) * per;
+    cudaError_t e = launch_group(p, (int)g, direction, first ? in0 : src, first ? in1 : nullptr, last ? out0 : dst,
+                                 last ? out1 : nullptr, first ? dist : n, last ? dist : n, batch, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 size_t elem_bytes(const fftgen_plan *p) { return 8; }  // fp32 complex, either layout
@@ -354,8 +361,9 @@ fftgen_status host_pipeline(fftgen_plan *p, size_t slot_bytes_per_transform, F &
     for (int r = 1; r <= ramp && left <= (chunk >> r) * 2 && (chunk >> r) > 0; ++r) tail = chunk >> r;
     cnt = std::min(std::min(want, tail), left);
     char *slot_ptr = (char *)p->d_stage + (i % K) * slot;
-    // two-launch four-step plans share one scratch buffer: keep their chunks
-    // stream-ordered (the K5 cluster path has no scratch)
+    // four-step plans share one scratch buffer (the two-launch scratch, or a
+    // cluster plan's fallback for unaligned chunks): keep their chunks
+    // stream-ordered; aligned cluster chunks use no scratch
     const int sid = (p->ex.strategy == STRAT_FOURSTEP && !p->use_cluster) ? 0 : (i % K);
     if ((e = stage(b0, cnt, slot_ptr, p->streams[sid])) != cudaSuccess) {
       // drain what was already enqueued: no copy may still touch the
@@ -531,6 +539,15 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       if (p->scratch_bytes > 0 && (e = cudaMalloc(&p->d_scratch, p->scratch_bytes)) != cudaSuccess)
         return bail(FFTGEN_ERR_NOMEM, "four-step scratch (" + std::to_string(p->scratch_bytes) +
                                           " bytes): " + cudaGetErrorString(e));
+      if (p->use_cluster) {
+        // data the TMA tiles cannot address (not 16-byte aligned) runs the
+        // two-launch path in chunks through <= 64 MiB of plan-owned scratch
+        const int64_t per_transform = p->ex.scratch_buffers * cfg->n * (int64_t)sizeof(float2);
+        p->fallback_chunk = std::max<int64_t>(1, std::min<int64_t>(cfg->batch, (int64_t(64) << 20) / per_transform));
+        p->fallback_bytes = (size_t)p->fallback_chunk * (size_t)per_transform;
+        if ((e = cudaMalloc(&p->d_fallback, p->fallback_bytes)) != cudaSuccess)
+          return bail(FFTGEN_ERR_NOMEM, "cluster fallback scratch: " + std::string(cudaGetErrorString(e)));
+      }
     }
     const auto &tw = p->ex.tw_block;
     if (!tw.empty()) {
@@ -574,9 +591,6 @@ fftgen_status fftgen_execute(const fftgen_plan *p, int direction, const void *in
   DeviceGuard g(p->cfg.device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   cudaError_t e = enqueue(p, direction, in0, in1, out0, out1, dist, p->cfg.batch, (cudaStream_t)stream);
-  if (e == cudaErrorStreamCaptureUnsupported)
-    return fail(FFTGEN_ERR_EXEC, "unaligned execute of a cluster plan needs the two-launch scratch: run it once "
-                                 "outside stream capture first (16-byte aligned data never needs it)");
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return FFTGEN_OK;
 }
