@@ -117,7 +117,15 @@ typedef struct {
                               or a compiled size (4, 8, 16)                  */
   int32_t host_chunk_mb;   /* fftgen_execute_host chunk (in + out per slot),
                               0 = 128 MiB                                    */
-  int32_t reserved0;
+  int32_t pass_radix;      /* radix hint for the sm_100a register passes of
+                              N <= 2^14: 0 = the measured default plan (radix 8
+                              at 2^7 .. 2^9, radix <= 64 elsewhere); 8, 16, 32
+                              = passes of at most that radix in the
+                              reference's Stockham shape (remainder radix
+                              first) where that takes <= 3 passes and differs
+                              from the radix-64 plan (N = 2^7 .. 2^12); 64 =
+                              the radix-<=64 two / three-pass plans (with the
+                              TMA kernels).  Four-step sizes ignore it.      */
 } fftgen_config;
 
 /* Fills the PipelineConfig defaults (driver.hpp:26-35) plus batch=1, device=0. */

@@ -119,6 +119,7 @@ struct PipelineConfig {
   int64_t batch = 1;      // transforms per execute
   int device = 0;         // CUDA device ordinal
   uint32_t tuning = 0;    // FFTGEN_TUNE_* kernel-selection bits (0 = measured defaults)
+  int pass_radix = 0;     // radix hint for the register passes (fftgen_config.pass_radix)
 };
 
 inline std::string algorithm_name(Algorithm a) { return a == Algorithm::CooleyTukey ? "cooley-tukey" : "stockham"; }
@@ -313,6 +314,7 @@ inline CompiledPipeline compile_pipeline(const PipelineConfig &config) {
   c.batch = config.batch;
   c.device = config.device;
   c.tuning = config.tuning;
+  c.pass_radix = config.pass_radix;
   fftgen_plan *p = nullptr;
   check(fftgen_plan_create(&p, &c));
   std::shared_ptr<fftgen_plan> plan(p, [](fftgen_plan *q) { fftgen_plan_destroy(q); });

@@ -98,7 +98,7 @@ class _Config(C.Structure):
                 ("vec", C.c_int32), ("vector_width", C.c_int32), ("interleaved_opt", C.c_int32),
                 ("tile_kind", C.c_int32), ("tile_value", C.c_int64),
                 ("tuning", C.c_uint32), ("cluster_size", C.c_int32), ("host_chunk_mb", C.c_int32),
-                ("reserved0", C.c_int32)]
+                ("pass_radix", C.c_int32)]
 
 
 def build(jobs: int = 8, quiet: bool = True) -> str:
@@ -190,6 +190,7 @@ class PipelineConfig:
     tuning: int = 0
     cluster_size: int = 0
     host_chunk_mb: int = 0
+    pass_radix: int = 0                   # radix hint for the register passes (0 = measured default)
 
 
 def _ptr(x) -> int:
@@ -223,6 +224,7 @@ def _to_config(cfg: PipelineConfig) -> "_Config":
     c.tuning = int(cfg.tuning)
     c.cluster_size = int(cfg.cluster_size)
     c.host_chunk_mb = int(cfg.host_chunk_mb)
+    c.pass_radix = int(cfg.pass_radix)
     return c
 
 

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #ifdef __CUDACC__
 #define FFTGEN_HD __host__ __device__
@@ -39,6 +40,32 @@ template <> struct BlockPlan<2048> : PlanT<2, 32, 64, 1> {};
 template <> struct BlockPlan<4096> : PlanT<2, 64, 64, 1> {};
 template <> struct BlockPlan<8192> : PlanT<3, 32, 16, 16> {};
 template <> struct BlockPlan<16384> : PlanT<3, 32, 32, 16> {};
+
+// Pass plans under a register-radix cap (the radix hint,
+// fftgen_config.pass_radix = 8 / 16 / 32): the default plan when its radices
+// already fit the cap, else the reference's own Stockham shape for that
+// radix -- the remainder radix first, then CAP-point passes (plan_stockham,
+// formula.cpp:182-195) -- when that needs at most three register passes;
+// otherwise the default (a hint never fails a plan).
+constexpr int clog2(int n) {
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+template <class PL> constexpr int plan_rmax() {
+  int m = 1;
+  for (int p = 0; p < PL::P; ++p) m = PL::r(p) > m ? PL::r(p) : m;
+  return m;
+}
+template <int N, int CAP> struct CapPlanGeom {
+  static constexpr int L = clog2(N), C = clog2(CAP);
+  static constexpr bool DEFAULT_FITS = plan_rmax<BlockPlan<N>>() <= CAP;
+  static constexpr int NP = L == 0 ? 1 : (L + C - 1) / C;
+  static constexpr bool DISTINCT = !DEFAULT_FITS && NP <= 3;
+  static constexpr int R0 = N >> (C * (NP - 1));
+  using Cap = PlanT<NP, R0, (NP >= 2 ? CAP : 1), (NP >= 3 ? CAP : 1)>;
+  using type = std::conditional_t<DISTINCT, Cap, BlockPlan<N>>;
+};
 
 // Plans of the K3 group sub-FFTs: the block plan of the same size.  (Three
 // 8/16-point register passes for NS = 512 / 1024 measured slower on B200:

@@ -75,6 +75,49 @@ cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, int flags, cudaStre
   }
 }
 
+// direct kernel under a pass-radix cap (CapPlanGeom): only the (N, CAP)
+// pairs whose plan differs from the default are instantiated
+template <int N, int LAYOUT, int DIR, int CAP>
+cudaError_t block_cap_launch_n(const BlockArgs &a, cudaStream_t s) {
+  if constexpr (CapPlanGeom<N, CAP>::DISTINCT) {
+    using PL = typename CapPlanGeom<N, CAP>::type;
+    using G = BlockGeom<N, 0, PL>;
+    const int64_t grid = (a.batch + G::TPB - 1) / G::TPB;
+    constexpr int smem = SmemGeom<N, PL>::BYTES;
+    if (grid <= 0) return cudaSuccess;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    fft_block_kernel<N, LAYOUT, DIR, PL><<<(unsigned)grid, G::THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
+template <int N, int LAYOUT, int DIR, int CAP>
+cudaError_t block_cap_prepare_n() {
+  if constexpr (CapPlanGeom<N, CAP>::DISTINCT) {
+    using PL = typename CapPlanGeom<N, CAP>::type;
+    constexpr int smem = SmemGeom<N, PL>::BYTES;
+    if (smem > 48 * 1024)
+      return cudaFuncSetAttribute(fft_block_kernel<N, LAYOUT, DIR, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  smem);
+    return cudaSuccess;
+  } else {
+    return cudaErrorInvalidValue;
+  }
+}
+
+#define FFTGEN_CAP_SWITCH(FN, LAYOUT, DIR, CAP, ...)             \
+  switch (log2n) {                                               \
+  case 7: return FN<128, LAYOUT, DIR, CAP>(__VA_ARGS__);         \
+  case 8: return FN<256, LAYOUT, DIR, CAP>(__VA_ARGS__);         \
+  case 9: return FN<512, LAYOUT, DIR, CAP>(__VA_ARGS__);         \
+  case 10: return FN<1024, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
+  case 11: return FN<2048, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
+  case 12: return FN<4096, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
+  default: return cudaErrorInvalidValue;                         \
+  }
+
 #define FFTGEN_BLOCK_SWITCH(FN, LAYOUT, DIR, ...)          \
   switch (log2n) {                                         \
   case 0: return FN<1, LAYOUT, DIR>(__VA_ARGS__);          \
@@ -105,6 +148,22 @@ cudaError_t block_tma_launch_n(const BlockArgs &a, int grid, int flags, cudaStre
   cudaError_t block_tma_launch_##SUFFIX(int log2n, const BlockArgs &a, int grid, int flags, \
                                         cudaStream_t s) {                                     \
     FFTGEN_BLOCK_SWITCH(block_tma_launch_n, LAYOUT, DIR, a, grid, flags, s)               \
+  }                                                                                           \
+  cudaError_t block_cap_launch_##SUFFIX(int log2n, int cap, const BlockArgs &a, cudaStream_t s) { \
+    switch (cap) {                                                                            \
+    case 8: FFTGEN_CAP_SWITCH(block_cap_launch_n, LAYOUT, DIR, 8, a, s)                       \
+    case 16: FFTGEN_CAP_SWITCH(block_cap_launch_n, LAYOUT, DIR, 16, a, s)                     \
+    case 32: FFTGEN_CAP_SWITCH(block_cap_launch_n, LAYOUT, DIR, 32, a, s)                     \
+    default: return cudaErrorInvalidValue;                                                    \
+    }                                                                                         \
+  }                                                                                           \
+  cudaError_t block_cap_prepare_##SUFFIX(int log2n, int cap) {                                \
+    switch (cap) {                                                                            \
+    case 8: FFTGEN_CAP_SWITCH(block_cap_prepare_n, LAYOUT, DIR, 8)                            \
+    case 16: FFTGEN_CAP_SWITCH(block_cap_prepare_n, LAYOUT, DIR, 16)                          \
+    case 32: FFTGEN_CAP_SWITCH(block_cap_prepare_n, LAYOUT, DIR, 32)                          \
+    default: return cudaErrorInvalidValue;                                                    \
+    }                                                                                         \
   }
 
 }  // namespace fftgen_b200

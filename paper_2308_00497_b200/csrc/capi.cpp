@@ -246,6 +246,7 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                          (dist * esz) % 16 == 0;
     const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
+    if (p->ex.block_cap) return block_cap_launch(p->ex.log2n, p->ex.block_cap, layout, direction, a, s);
     if (p->use_tma && p->tma_grid > 0 && aligned) {
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
       const int64_t groups = (batch + tp - 1) / tp;
@@ -439,9 +440,11 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
     auto ops = fuse_ops(cfg->n, cfg->algorithm, cfg->radix);
     auto radices = stockham_radices(cfg->n, cfg->radix);
     check_schedule(cfg->vec, cfg->vector_width, cfg->tile_kind, cfg->tile_value);
-    ExecPlan ex = build_exec_plan(cfg->n, (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
-                                              ? SPLIT_GROUPS_1024
-                                              : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT));
+    ExecPlan ex = build_exec_plan(cfg->n,
+                                  (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
+                                      ? SPLIT_GROUPS_1024
+                                      : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT),
+                                  cfg->pass_radix);
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -470,6 +473,11 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       if ((e = block_prepare(p->ex.log2n, &per_sm)) != cudaSuccess)
         return bail(FFTGEN_ERR_GPUMAP, std::string("block kernel attributes: ") + cudaGetErrorString(e));
       p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
+      if (p->ex.block_cap) {  // the radix hint's plan runs on the direct kernel
+        if ((e = block_cap_prepare(p->ex.log2n, p->ex.block_cap)) != cudaSuccess)
+          return bail(FFTGEN_ERR_GPUMAP, std::string("capped block kernel attributes: ") + cudaGetErrorString(e));
+        p->tma_grid = 0;
+      }
       p->use_tma = !(tune & FFTGEN_TUNE_NO_TMA);
       p->use_tma_store = !(tune & FFTGEN_TUNE_NO_TMA_STORE);
     }
@@ -715,9 +723,11 @@ fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf,
     case FFTGEN_TEXT_FORMULA: text = formula_text(cfg->n, cfg->algorithm, cfg->radix) + "\n"; break;
     case FFTGEN_TEXT_PIPELINE: text = pipeline_text(ops, cfg->n); break;
     case FFTGEN_TEXT_LOOPS:
-      text = program_text(cfg->n, (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
-                                      ? SPLIT_GROUPS_1024
-                                      : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT));
+      text = program_text(cfg->n,
+                          (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
+                              ? SPLIT_GROUPS_1024
+                              : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT),
+                          cfg->pass_radix);
       break;
     case FFTGEN_TEXT_RADICES: {
       std::ostringstream o;
@@ -798,9 +808,11 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
         << (single ? " (persistent, cp.async.bulk single stage + plane exchange; direct kernel if unaligned)\n"
                    : " (persistent, cp.async.bulk double-buffered; direct kernel if unaligned)\n");
     } else {
-      block_launch_geom(p->ex.log2n, &threads, &tpb, &smem);
+      block_launch_geom(p->ex.log2n, &threads, &tpb, &smem, p->ex.block_cap);
       o << "kernel fft_block_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + tpb - 1) / tpb << "] block["
-        << threads << "] smem=" << smem << "B transforms/CTA=" << tpb << "\n";
+        << threads << "] smem=" << smem << "B transforms/CTA=" << tpb;
+      if (p->ex.block_cap) o << " (pass radix hint " << p->ex.block_cap << ")";
+      o << "\n";
     }
     for (size_t i = 0; i < p->ex.passes.size(); ++i) {
       const auto &d = p->ex.passes[i];

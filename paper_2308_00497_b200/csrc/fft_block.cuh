@@ -175,9 +175,9 @@ FFTGEN_FI void middle_passes(float2 *sx, int t, const float2 *__restrict__ tw, f
 }
 
 // ---- variant 1: direct ---------------------------------------------------
-template <int N, int LAYOUT, int DIR>
-__global__ void __launch_bounds__(BlockGeom<N>::THREADS) fft_block_kernel(const BlockArgs args) {
-  using G = BlockGeom<N>;
+template <int N, int LAYOUT, int DIR, class PL = BlockPlan<N>>
+__global__ void __launch_bounds__(BlockGeom<N, 0, PL>::THREADS) fft_block_kernel(const BlockArgs args) {
+  using G = BlockGeom<N, 0, PL>;
   extern __shared__ float4 smem_f4[];
   const int tid = threadIdx.x;
   const int f = tid / G::T;
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(BlockGeom<N>::THREADS) fft_block_kernel(const 
 
   float2 v[G::RMAX];
   pass0<G, DIR>(t, v, [&](int e) { return live ? GIO<LAYOUT>::load(args, ibase + e) : make_float2(0.f, 0.f); });
-  float2 *sx = reinterpret_cast<float2 *>(smem_f4) + f * SmemGeom<N>::REGION;
+  float2 *sx = reinterpret_cast<float2 *>(smem_f4) + f * SmemGeom<N, PL>::REGION;
   if constexpr (G::P == 2) {
     TwPQ<G> pq;
     pq.load(args.tw, t);

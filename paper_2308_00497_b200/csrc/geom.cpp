@@ -9,52 +9,69 @@
 namespace fftgen_b200 {
 
 namespace {
-template <int N> struct GeomQuery {
-  static int passes() { return BlockGeom<N>::P; }
+template <int N, class PL = BlockPlan<N>> struct GeomQuery {
+  using G = BlockGeom<N, 0, PL>;
+  static int passes() { return G::P; }
   static void pass(int p, int64_t *R, int64_t *cols, int64_t *k) {
-    *R = BlockGeom<N>::R(p);
-    *cols = BlockGeom<N>::COLS(p);
-    *k = BlockGeom<N>::K(p);
+    *R = G::R(p);
+    *cols = G::COLS(p);
+    *k = G::K(p);
   }
   static void launch(int64_t *threads, int64_t *tpb, int64_t *smem) {
-    *threads = BlockGeom<N>::THREADS;
-    *tpb = BlockGeom<N>::TPB;
-    *smem = SmemGeom<N>::BYTES;
+    *threads = G::THREADS;
+    *tpb = G::TPB;
+    *smem = SmemGeom<N, PL>::BYTES;
   }
 };
-#define FFTGEN_GEOM_SWITCH(EXPR)                 \
-  switch (log2n) {                               \
-  case 0: { using Q = GeomQuery<1>; EXPR; }      \
-  case 1: { using Q = GeomQuery<2>; EXPR; }      \
-  case 2: { using Q = GeomQuery<4>; EXPR; }      \
-  case 3: { using Q = GeomQuery<8>; EXPR; }      \
-  case 4: { using Q = GeomQuery<16>; EXPR; }     \
-  case 5: { using Q = GeomQuery<32>; EXPR; }     \
-  case 6: { using Q = GeomQuery<64>; EXPR; }     \
-  case 7: { using Q = GeomQuery<128>; EXPR; }    \
-  case 8: { using Q = GeomQuery<256>; EXPR; }    \
-  case 9: { using Q = GeomQuery<512>; EXPR; }    \
-  case 10: { using Q = GeomQuery<1024>; EXPR; }  \
-  case 11: { using Q = GeomQuery<2048>; EXPR; }  \
-  case 12: { using Q = GeomQuery<4096>; EXPR; }  \
-  case 13: { using Q = GeomQuery<8192>; EXPR; }  \
-  case 14: { using Q = GeomQuery<16384>; EXPR; } \
-  default: throw PlanError("no block kernel for 2^" + std::to_string(log2n)); \
+// the plan a (N, pass-radix cap) pair runs: the capped plan when it differs
+// from the default (CapPlanGeom::DISTINCT), else the default
+template <int N, class F> decltype(auto) with_plan(int cap, F &&f) {
+  if (cap == 8 && CapPlanGeom<N, 8>::DISTINCT) return f(GeomQuery<N, typename CapPlanGeom<N, 8>::type>{});
+  if (cap == 16 && CapPlanGeom<N, 16>::DISTINCT) return f(GeomQuery<N, typename CapPlanGeom<N, 16>::type>{});
+  if (cap == 32 && CapPlanGeom<N, 32>::DISTINCT) return f(GeomQuery<N, typename CapPlanGeom<N, 32>::type>{});
+  return f(GeomQuery<N>{});
+}
+template <int N> bool cap_distinct(int cap) {
+  return (cap == 8 && CapPlanGeom<N, 8>::DISTINCT) || (cap == 16 && CapPlanGeom<N, 16>::DISTINCT) ||
+         (cap == 32 && CapPlanGeom<N, 32>::DISTINCT);
+}
+#define FFTGEN_GEOM_CASE(L, NN, BODY) \
+  case L: return with_plan<NN>(cap, [&](auto q) { using Q = decltype(q); BODY; });
+#define FFTGEN_GEOM_SWITCH(BODY)                                                                             \
+  switch (log2n) {                                                                                           \
+    FFTGEN_GEOM_CASE(0, 1, BODY) FFTGEN_GEOM_CASE(1, 2, BODY) FFTGEN_GEOM_CASE(2, 4, BODY)                   \
+    FFTGEN_GEOM_CASE(3, 8, BODY) FFTGEN_GEOM_CASE(4, 16, BODY) FFTGEN_GEOM_CASE(5, 32, BODY)                 \
+    FFTGEN_GEOM_CASE(6, 64, BODY) FFTGEN_GEOM_CASE(7, 128, BODY) FFTGEN_GEOM_CASE(8, 256, BODY)              \
+    FFTGEN_GEOM_CASE(9, 512, BODY) FFTGEN_GEOM_CASE(10, 1024, BODY) FFTGEN_GEOM_CASE(11, 2048, BODY)         \
+    FFTGEN_GEOM_CASE(12, 4096, BODY) FFTGEN_GEOM_CASE(13, 8192, BODY) FFTGEN_GEOM_CASE(14, 16384, BODY)      \
+  default: throw PlanError("no block kernel for 2^" + std::to_string(log2n));                               \
   }
 }  // namespace
 
-int block_num_passes(int log2n) { FFTGEN_GEOM_SWITCH(return Q::passes()) }
+int block_num_passes(int log2n, int cap) { FFTGEN_GEOM_SWITCH(return Q::passes()) }
 
-void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k) {
-  FFTGEN_GEOM_SWITCH(Q::pass(p, R, cols, k); return)
+void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k, int cap) {
+  FFTGEN_GEOM_SWITCH(Q::pass(p, R, cols, k))
 }
 
-void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem) {
-  FFTGEN_GEOM_SWITCH(Q::launch(threads, tpb, smem); return)
+void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem, int cap) {
+  FFTGEN_GEOM_SWITCH(Q::launch(threads, tpb, smem))
+}
+
+bool block_cap_distinct(int log2n, int cap) {
+  switch (log2n) {
+  case 7: return cap_distinct<128>(cap);
+  case 8: return cap_distinct<256>(cap);
+  case 9: return cap_distinct<512>(cap);
+  case 10: return cap_distinct<1024>(cap);
+  case 11: return cap_distinct<2048>(cap);
+  case 12: return cap_distinct<4096>(cap);
+  default: return false;
+  }
 }
 
 // [A][m] tables of w_s^{A m} for passes 1..P-1, fp64 -> fp32 (forward sign).
-std::vector<float> block_twiddles(int log2n) {
+std::vector<float> block_twiddles(int log2n, int cap) {
   std::vector<float> out;
   auto push = [&](int64_t s, int64_t e) {
     double re, im;
@@ -62,10 +79,10 @@ std::vector<float> block_twiddles(int log2n) {
     out.push_back(static_cast<float>(re));
     out.push_back(static_cast<float>(im));
   };
-  const int np = block_num_passes(log2n);
+  const int np = block_num_passes(log2n, cap);
   for (int p = 1; p < np; ++p) {
     int64_t R, cols, k;
-    block_pass(log2n, p, &R, &cols, &k);
+    block_pass(log2n, p, &R, &cols, &k, cap);
     for (int64_t A = 0; A < R; ++A)
       for (int64_t m = 0; m < cols; ++m) push(R * cols, A * m);
   }
@@ -73,7 +90,7 @@ std::vector<float> block_twiddles(int log2n) {
   // [A][h] = w_s^{A 32 h}, then [A][l] = w_s^{A l}, h, l < 32
   for (int p = 1; p < np; ++p) {
     int64_t R, cols, k;
-    block_pass(log2n, p, &R, &cols, &k);
+    block_pass(log2n, p, &R, &cols, &k, cap);
     if (cols < FFTGEN_TW_FACTOR_COLS) continue;
     for (int64_t A = 0; A < R; ++A)
       for (int64_t h = 0; h < 32; ++h) push(R * cols, A * 32 * h);

@@ -24,6 +24,10 @@ struct BlockArgs {
 // K2: one CTA per TPB whole transforms, N = 2^log2n <= 2^14.
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
 cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm);
+// K2 direct kernel under a pass-radix cap (8 / 16 / 32; CapPlanGeom) for the
+// sizes whose capped plan differs from the default
+cudaError_t block_cap_launch(int log2n, int cap, int layout, int dir, const BlockArgs &a, cudaStream_t s);
+cudaError_t block_cap_prepare(int log2n, int cap);
 // persistent TMA-pipelined variant (fft_block_tma_kernel); grid = CTAs;
 // flags: BLOCK_TMA_STORE (bulk-store epilogue)
 constexpr int BLOCK_TMA_STORE = 1;
@@ -33,7 +37,7 @@ bool block_tma_enabled(int log2n);
 bool block_tma1(int log2n);  // the size runs the single-stage fft_block_tma1_kernel
 int block_tma_transforms_per_cta(int log2n);
 void block_tma_geom(int log2n, int64_t *threads, int64_t *tp, int64_t *smem);
-void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem);
+void block_launch_geom(int log2n, int64_t *threads, int64_t *tpb, int64_t *smem, int cap = 0);
 
 // Arguments of the K3 group kernel (fft_group.cuh): one radix-NS Stockham
 // stage of the whole transform with global (cols, k).

@@ -24,6 +24,29 @@ cudaError_t block_tma_launch_i_b(int, const BlockArgs &, int, int, cudaStream_t)
 cudaError_t block_tma_launch_s_f(int, const BlockArgs &, int, int, cudaStream_t);
 cudaError_t block_tma_launch_s_b(int, const BlockArgs &, int, int, cudaStream_t);
 
+cudaError_t block_cap_launch_i_f(int, int, const BlockArgs &, cudaStream_t);
+cudaError_t block_cap_launch_i_b(int, int, const BlockArgs &, cudaStream_t);
+cudaError_t block_cap_launch_s_f(int, int, const BlockArgs &, cudaStream_t);
+cudaError_t block_cap_launch_s_b(int, int, const BlockArgs &, cudaStream_t);
+cudaError_t block_cap_prepare_i_f(int, int);
+cudaError_t block_cap_prepare_i_b(int, int);
+cudaError_t block_cap_prepare_s_f(int, int);
+cudaError_t block_cap_prepare_s_b(int, int);
+
+cudaError_t block_cap_launch(int log2n, int cap, int layout, int dir, const BlockArgs &a, cudaStream_t s) {
+  if (layout == LAYOUT_INTERLEAVED)
+    return dir < 0 ? block_cap_launch_i_f(log2n, cap, a, s) : block_cap_launch_i_b(log2n, cap, a, s);
+  return dir < 0 ? block_cap_launch_s_f(log2n, cap, a, s) : block_cap_launch_s_b(log2n, cap, a, s);
+}
+
+cudaError_t block_cap_prepare(int log2n, int cap) {
+  cudaError_t e;
+  if ((e = block_cap_prepare_i_f(log2n, cap)) != cudaSuccess) return e;
+  if ((e = block_cap_prepare_i_b(log2n, cap)) != cudaSuccess) return e;
+  if ((e = block_cap_prepare_s_f(log2n, cap)) != cudaSuccess) return e;
+  return block_cap_prepare_s_b(log2n, cap);
+}
+
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s) {
   if (layout == LAYOUT_INTERLEAVED)
     return dir < 0 ? block_launch_i_f(log2n, a, s) : block_launch_i_b(log2n, a, s);

@@ -157,10 +157,10 @@ std::string formula_text(int64_t n, int algorithm, int64_t radix) {
   return out;
 }
 
-std::string program_text(int64_t n, int split_mode) {
+std::string program_text(int64_t n, int split_mode, int pass_radix) {
   // the sm_100a execution plan as loop nests: one Stockham stage of radix R
   // per register pass (K2) or per four-step group launch (K3)
-  const ExecPlan p = build_exec_plan(n, split_mode);
+  const ExecPlan p = build_exec_plan(n, split_mode, pass_radix);
   std::ostringstream out;
   if (p.strategy == STRAT_IDENTITY) {
     out << "copy: y[0] = x[0]\n";
@@ -234,7 +234,7 @@ void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_v
   }
 }
 
-ExecPlan build_exec_plan(int64_t n, int split_mode) {
+ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix) {
   if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
   ExecPlan p;
   p.n = n;
@@ -243,16 +243,24 @@ ExecPlan build_exec_plan(int64_t n, int split_mode) {
     p.strategy = STRAT_IDENTITY;
     return p;
   }
+  if (pass_radix != 0 && pass_radix != 8 && pass_radix != 16 && pass_radix != 32 && pass_radix != 64)
+    throw PlanError("pass radix hint must be 0, 8, 16, 32 or 64, got " + std::to_string(pass_radix));
   if (p.log2n <= 14) {
     p.strategy = STRAT_BLOCK;
-    const int np = block_num_passes(p.log2n);
+    // measured default: 2^7 .. 2^9 as radix-8 three-pass plans on the direct
+    // kernel (1 GiB batches, split / interleaved fraction of HBM: 2^7 0.90 /
+    // 1.05 vs 0.85 / 1.01, 2^8 0.99 / 1.05 vs 0.92 / 1.00 (TMA), 2^9 0.98 /
+    // 1.04 vs 0.93 / 1.00 (TMA)); pass_radix 64 selects the two-pass plans
+    const int cap = pass_radix == 0 ? (p.log2n >= 7 && p.log2n <= 9 ? 8 : 0) : (pass_radix == 64 ? 0 : pass_radix);
+    p.block_cap = block_cap_distinct(p.log2n, cap) ? cap : 0;
+    const int np = block_num_passes(p.log2n, p.block_cap);
     for (int q = 0; q < np; ++q) {
       PassDesc d{};
-      block_pass(p.log2n, q, &d.R, &d.cols, &d.k);
+      block_pass(p.log2n, q, &d.R, &d.cols, &d.k, p.block_cap);
       d.s = d.R * d.cols;
       p.passes.push_back(d);
     }
-    p.tw_block = block_twiddles(p.log2n);
+    p.tw_block = block_twiddles(p.log2n, p.block_cap);
     return p;
   }
   if (p.log2n > 30)

@@ -75,6 +75,7 @@ struct GroupDesc {
 
 struct ExecPlan {
   int64_t n = 0;
+  int block_cap = 0;  // K2: pass-radix cap in effect (0 = the default plan)
   Strategy strategy = STRAT_BLOCK;
   int log2n = 0;
   std::vector<PassDesc> passes;
@@ -94,15 +95,18 @@ std::vector<int> group_split(int log2n, int mode = SPLIT_DEFAULT);
 bool group_prefers_tma(int log2ns, bool first, bool rows);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
-ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT);
+ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0);
 // the sm_100a pass / group program as loop nests (the --emit loops text)
-std::string program_text(int64_t n, int split_mode = SPLIT_DEFAULT);
+std::string program_text(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0);
 
 // K2 pass structure of an N-point block kernel (defined in kernels_common.cu
 // from the compile-time BlockPlan), and its [A][m] twiddle table in floats.
-int block_num_passes(int log2n);
-void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k);
-std::vector<float> block_twiddles(int log2n);
+// cap: the pass-radix hint (0 = default; 8 / 16 / 32 select the capped plan
+// where block_cap_distinct says it differs from the default)
+int block_num_passes(int log2n, int cap = 0);
+void block_pass(int log2n, int p, int64_t *R, int64_t *cols, int64_t *k, int cap = 0);
+std::vector<float> block_twiddles(int log2n, int cap = 0);
+bool block_cap_distinct(int log2n, int cap);
 std::vector<float> group_twiddles(int log2ns);
 
 }  // namespace fftgen_b200

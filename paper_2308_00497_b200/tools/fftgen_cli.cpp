@@ -9,7 +9,8 @@
 //
 // stage flags (StageFlags, main.cpp:28-85): --algorithm cooley-tukey|stockham,
 // --radix R, --layout interleaved|split, --vectorize none|inner|outer,
-// --vector-width W, --interleaved-opt, --tile-size T | --tile-cache BYTES.
+// --vector-width W, --interleaved-opt, --tile-size T | --tile-cache BYTES; and
+// the B200 radix hint --pass-radix 8|16|32 (register passes of at most that radix).
 //
 // Exit codes: 0 success, 1 failed verification or runtime error (an
 // fftgen::Error), 2 usage error (main.cpp:250-258).  `verify` is the
@@ -109,6 +110,7 @@ PipelineConfig config_from(const Args &a, bool with_size = true) {
   if (ts > 0) c.tile = TilePolicy::exact(ts);
   else if (tcache > 0) c.tile = TilePolicy::cache(tcache);
   c.batch = std::stoll(a.get("--batch", "1"));
+  c.pass_radix = std::stoi(a.get("--pass-radix", "0"));  // B200 extension: radix hint for the register passes
   return c;
 }
 
@@ -122,6 +124,7 @@ fftgen_config c_config(const PipelineConfig &c) {
   f.vec = c.vec == VecMode::Inner ? FFTGEN_VEC_INNER : (c.vec == VecMode::Outer ? FFTGEN_VEC_OUTER : FFTGEN_VEC_NONE);
   f.vector_width = static_cast<int32_t>(c.vector_width);
   f.interleaved_opt = c.interleaved_opt;
+  f.pass_radix = c.pass_radix;
   if (c.tile) {
     f.tile_kind = c.tile->kind == TilePolicy::ExactSize ? FFTGEN_TILE_EXACT : FFTGEN_TILE_CACHE;
     f.tile_value = c.tile->value;
@@ -301,7 +304,7 @@ int main(int argc, char **argv) {
     static const char *kValueFlags[] = {"--size", "--algorithm", "--radix", "--layout", "--vectorize",
                                         "--vector-width", "--tile-size", "--tile-cache", "--emit", "--input",
                                         "--random", "--sizes", "--inputs", "--repeats", "--csv", "--batch",
-                                        "--batch-bytes", "--peak-gbs"};
+                                        "--batch-bytes", "--peak-gbs", "--pass-radix"};
     for (size_t k = 0; k < a.v.size(); ++k)
       for (const char *f : kValueFlags)
         if (a.v[k] == f && (k + 1 >= a.v.size() || a.v[k + 1].rfind("--", 0) == 0))

@@ -35,10 +35,10 @@ def dft_rows(n, rows, direction):
     return torch.complex(torch.cos(ph), torch.sin(ph))
 
 
-def run_impulses(fg, n, rows, layout, direction, tuning=0):
+def run_impulses(fg, n, rows, layout, direction, tuning=0, pass_radix=0):
     batch = len(rows)
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, algorithm="stockham",
-                                                 tuning=tuning))
+                                                 tuning=tuning, pass_radix=pass_radix))
     idx = torch.as_tensor(rows, device="cuda", dtype=torch.int64)
     if layout == "interleaved":
         x = torch.zeros(batch, n, 2, device="cuda")
@@ -78,6 +78,20 @@ def test_full_dft_matrix_block_sizes(fg, l2, layout, direction):
             worst = max(worst, max_err(got, dft_rows(n, rs, direction)))
             del got
         assert worst <= 2e-6, (n, layout, direction, tuning, worst)
+
+
+@pytest.mark.parametrize("l2,hint", [(7, 8), (8, 8), (9, 8), (9, 16), (10, 16), (11, 16), (11, 32), (12, 16),
+                                     (12, 32)])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+@pytest.mark.parametrize("direction", [-1, 1])
+def test_full_dft_matrix_radix_hint_plans(fg, l2, hint, layout, direction):
+    """The radix hint's plans (register passes of radix <= 8 / 16 / 32 in the
+    reference's Stockham shape, fftgen_config.pass_radix): complete matrix."""
+    n = 1 << l2
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=1, pass_radix=hint))
+    assert max(r for r, *_ in plan.passes()) <= hint and f"pass radix hint {hint}" in plan.describe()
+    got = run_impulses(fg, n, list(range(n)), layout, direction, pass_radix=hint)
+    assert max_err(got, dft_rows(n, list(range(n)), direction)) <= 2e-6
 
 
 @pytest.mark.parametrize("l2,tuning", [(15, 0), (16, 0), (17, 0), (18, 0), (19, 0), (20, 0), (20, 1), (21, 0), (21, 8),

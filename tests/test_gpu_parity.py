@@ -62,10 +62,10 @@ def from_device(bufs, layout, n):
     return out
 
 
-def run(n, layout, direction, x, dist=None, radix=2, tuning=0):
+def run(n, layout, direction, x, dist=None, radix=2, tuning=0, pass_radix=0):
     batch = x.shape[0]
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=batch, radix=radix,
-                                                 algorithm="stockham", tuning=tuning))
+                                                 algorithm="stockham", tuning=tuning, pass_radix=pass_radix))
     src = to_device(x, layout, dist)
     dst = tuple(torch.full_like(t, float("nan")) if t is not None else None for t in src)
     plan.execute(src[0], dst[0], src[1], dst[1], direction=direction, dist=dist or n)
@@ -280,10 +280,11 @@ def test_tma_and_direct_kernels_bitwise_equal(orc, n):
     """The persistent TMA variants (bulk-store epilogue or register stores) and
     the direct variant run the same passes: bitwise equal results."""
     x = seeded_batch(orc, n, 37)
+    hint = 64 if n <= 512 else 0  # 2^8 / 2^9 default to radix-8 direct plans; 64 keeps the TMA ones
     for layout in ("interleaved", "split"):
-        a = run(n, layout, -1, x)
-        b = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA)
-        c = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA_STORE)
+        a = run(n, layout, -1, x, pass_radix=hint)
+        b = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA, pass_radix=hint)
+        c = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA_STORE, pass_radix=hint)
         assert np.array_equal(a, b) and np.array_equal(a, c), layout
         check(a, orc.forward(x, "stockham", 4), n)
 
