@@ -394,6 +394,58 @@ inline ComplexBuffer interpret(const CompiledPipeline &prog, const ComplexBuffer
   return interpret(prog.final_ir, input, o);
 }
 
+// ---- the distributed four-step of one transform over `world` ranks ----------
+// (fftgen_dist_*).  Device blocks of block_elems()
+// interleaved fp32 complex values; the exchange is the caller's all-to-all of
+// `world` contiguous chunks of chunk_bytes (NCCL grouped send/recv), any
+// callable `int(const void *send, void *recv, size_t chunk_bytes, void *stream)`
+// returning 0 on success.
+class DistributedPlan {
+ public:
+  DistributedPlan(int64_t n, int world, int rank, int device = 0) {
+    fftgen_dist_plan *p = nullptr;
+    check(fftgen_dist_plan_create(&p, n, world, rank, device));
+    plan_.reset(p, [](fftgen_dist_plan *q) { fftgen_dist_plan_destroy(q); });
+  }
+  int64_t block_elems() const { return fftgen_dist_block_elems(plan_.get()); }
+  int64_t chunk_elems() const { return fftgen_dist_chunk_elems(plan_.get()); }
+  fftgen_dist_plan *handle() const { return plan_.get(); }
+
+  template <class Exchange>
+  void execute(Direction dir, const void *in, void *out, void *work0, void *work1, Exchange &&exchange,
+               void *stream = nullptr) const {
+    struct Ctx {
+      Exchange *f;
+    } ctx{&exchange};
+    auto tramp = [](void *c, const void *send, void *recv, size_t bytes, void *s) -> int {
+      return (*static_cast<Ctx *>(c)->f)(send, recv, bytes, s);
+    };
+    check(fftgen_dist_execute(plan_.get(), static_cast<int>(dir), in, out, work0, work1, tramp, &ctx, stream));
+  }
+  // the stages one by one (the exchanges in between are the caller's)
+  void butterfly(Direction dir, const void *recv, void *send, void *stream = nullptr) const {
+    check(fftgen_dist_butterfly(plan_.get(), static_cast<int>(dir), recv, send, stream));
+  }
+  void local(Direction dir, const void *in, void *out, void *stream = nullptr) const {
+    check(fftgen_dist_local(plan_.get(), static_cast<int>(dir), in, out, stream));
+  }
+  void unpack(const void *recv, void *out, void *stream = nullptr) const {
+    check(fftgen_dist_unpack(plan_.get(), recv, out, stream));
+  }
+  // peer-memory transport: every rank's blocks mapped into this process
+  void butterfly_peers(Direction dir, const std::vector<const void *> &in_blocks,
+                       const std::vector<void *> &recv_blocks, void *stream = nullptr) const {
+    check(fftgen_dist_butterfly_peers(plan_.get(), static_cast<int>(dir), in_blocks.data(), recv_blocks.data(),
+                                      stream));
+  }
+  void unpack_peers(const std::vector<const void *> &z_blocks, void *out, void *stream = nullptr) const {
+    check(fftgen_dist_unpack_peers(plan_.get(), z_blocks.data(), out, stream));
+  }
+
+ private:
+  std::shared_ptr<fftgen_dist_plan> plan_;
+};
+
 }  // namespace fftgen
 
 #endif  // FFTGEN_B200_HPP

@@ -174,10 +174,62 @@ static void gpu_tests() {
   }
 }
 
+// fftgen::DistributedPlan: the distributed four-step through the C++ API
+// with an exchange callable (world 1: the all-to-all is a device copy), and
+// its argument validation.
+extern "C" int cudaMalloc(void **, size_t);
+extern "C" int cudaFree(void *);
+extern "C" int cudaMemcpy(void *, const void *, size_t, int);
+extern "C" int cudaMemcpyAsync(void *, const void *, size_t, int, void *);
+extern "C" int cudaDeviceSynchronize();
+
+static void dist_tests() {
+  CHECK(throws<DimensionError>([] { DistributedPlan(1 << 12, 3, 0); }));
+  CHECK(throws<PlanError>([] { DistributedPlan(3000, 2, 0); }));
+  const int64_t n = 1 << 16;
+  DistributedPlan dp(n, 1, 0);
+  CHECK(dp.block_elems() == n && dp.chunk_elems() == n);
+  std::vector<double> d(2 * n);
+  orc_seeded_input(n, 11, d.data());
+  std::vector<float> h(2 * n);
+  for (int64_t i = 0; i < 2 * n; ++i) h[i] = (float)d[i];
+  void *x = nullptr, *y = nullptr, *w0 = nullptr, *w1 = nullptr;
+  cudaMalloc(&x, 8 * n);
+  cudaMalloc(&y, 8 * n);
+  cudaMalloc(&w0, 8 * n);
+  cudaMalloc(&w1, 8 * n);
+  cudaMemcpy(x, h.data(), 8 * n, 1);
+  int calls = 0;
+  dp.execute(Direction::Forward, x, y, w0, w1, [&](const void *s, void *r, size_t bytes, void *st) {
+    ++calls;
+    return cudaMemcpyAsync(r, s, bytes, 3, st);
+  });
+  cudaDeviceSynchronize();
+  std::vector<float> out(2 * n);
+  cudaMemcpy(out.data(), y, 8 * n, 2);
+  std::vector<double> in64(2 * n), want(2 * n);
+  for (int64_t i = 0; i < 2 * n; ++i) in64[i] = h[i];
+  orc_forward_batch(n, 1, 4, 1, in64.data(), want.data(), 4);
+  std::vector<cplx> got(n), w(n);
+  for (int64_t j = 0; j < n; ++j) got[j] = {out[2 * j], out[2 * j + 1]}, w[j] = {want[2 * j], want[2 * j + 1]};
+  CHECK(calls == 3);
+  CHECK(rel_l2(got, w) < 3e-6);
+  // a failing exchange surfaces as ExecError
+  CHECK(throws<ExecError>([&] { dp.execute(Direction::Forward, x, y, w0, w1, [](const void *, void *, size_t, void *) { return 7; }); }));
+  CHECK(throws<ExecError>([&] { dp.butterfly(Direction::Forward, x, x); }));  // out of place only
+  cudaFree(x);
+  cudaFree(y);
+  cudaFree(w0);
+  cudaFree(w1);
+}
+
 int main(int argc, char **argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
   cpu_tests();
-  if (mode == "gpu") gpu_tests();
+  if (mode == "gpu") {
+    gpu_tests();
+    dist_tests();
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

@@ -16,9 +16,12 @@ BIN = os.path.join(ROOT, "paper_2308_00497_b200", "build", "api_test")
 @pytest.fixture(scope="module")
 def api_test():
     os.makedirs(os.path.dirname(BIN), exist_ok=True)
+    # cudart (the toolkit's shared runtime) only for the test's own device
+    # buffers in the DistributedPlan case; the library links its own statically
+    cudalib = "/usr/local/cuda/lib64"
     subprocess.run(["g++", "-std=c++17", "-O1", "-Wall", "-I", os.path.join(ROOT, "include"), "-o", BIN, SRC,
-                    "-L", LIBDIR, "-lfftgen_b200", "-L", ORCDIR, "-lfftgen_oracle",
-                    f"-Wl,-rpath,{LIBDIR}", f"-Wl,-rpath,{ORCDIR}"], check=True)
+                    "-L", LIBDIR, "-lfftgen_b200", "-L", ORCDIR, "-lfftgen_oracle", "-L", cudalib, "-lcudart",
+                    f"-Wl,-rpath,{LIBDIR}", f"-Wl,-rpath,{ORCDIR}", f"-Wl,-rpath,{cudalib}"], check=True)
     return BIN
 
 
