@@ -18,9 +18,9 @@ namespace fftgen_b200 {
 // Pass plans: radices per pass for each N handled by one CTA.  Any grouping
 // of the reference's radix-2 Stockham stage list is a valid regrouping; the
 // register radix is capped at 64 (128 registers of float2 data per thread).
-template <int NP, int R0, int R1, int R2> struct PlanT {
+template <int NP, int R0, int R1, int R2, int R3 = 1> struct PlanT {
   static constexpr int P = NP;
-  FFTGEN_HD static constexpr int r(int p) { return p == 0 ? R0 : (p == 1 ? R1 : R2); }
+  FFTGEN_HD static constexpr int r(int p) { return p == 0 ? R0 : (p == 1 ? R1 : (p == 2 ? R2 : R3)); }
 };
 template <int N> struct BlockPlan;
 template <> struct BlockPlan<1> : PlanT<1, 1, 1, 1> {};
@@ -61,9 +61,9 @@ template <int N, int CAP> struct CapPlanGeom {
   static constexpr int L = clog2(N), C = clog2(CAP);
   static constexpr bool DEFAULT_FITS = plan_rmax<BlockPlan<N>>() <= CAP;
   static constexpr int NP = L == 0 ? 1 : (L + C - 1) / C;
-  static constexpr bool DISTINCT = !DEFAULT_FITS && NP <= 3;
+  static constexpr bool DISTINCT = !DEFAULT_FITS && NP <= 4;
   static constexpr int R0 = N >> (C * (NP - 1));
-  using Cap = PlanT<NP, R0, (NP >= 2 ? CAP : 1), (NP >= 3 ? CAP : 1)>;
+  using Cap = PlanT<NP, R0, (NP >= 2 ? CAP : 1), (NP >= 3 ? CAP : 1), (NP >= 4 ? CAP : 1)>;
   using type = std::conditional_t<DISTINCT, Cap, BlockPlan<N>>;
 };
 
@@ -88,8 +88,7 @@ template <> struct GroupPlan<4096> : PlanT<3, 16, 16, 16> {};
 template <int N, int TP_ = 0, class PL_ = BlockPlan<N>> struct BlockGeom {
   using PL = PL_;
   static constexpr int P = PL::P;
-  static constexpr int RMAX = PL::r(0) > PL::r(1) ? (PL::r(0) > PL::r(2) ? PL::r(0) : PL::r(2))
-                                                  : (PL::r(1) > PL::r(2) ? PL::r(1) : PL::r(2));
+  static constexpr int RMAX = plan_rmax<PL>();
   static constexpr int T = N / RMAX;  // threads per transform
   static constexpr int TPB = TP_ ? TP_ : (T >= 128 ? 1 : 128 / T);
   static constexpr int THREADS = T * TPB;
@@ -207,8 +206,9 @@ template <int N, class PL> struct StrideSearch {
     else return 0;
   }
   static constexpr int worst(int stride) {
-    const int c0 = boundary_cost<0>(stride), c1 = boundary_cost<1>(stride);
-    return c0 > c1 ? c0 : c1;
+    const int c0 = boundary_cost<0>(stride), c1 = boundary_cost<1>(stride), c2 = boundary_cost<2>(stride);
+    const int c01 = c0 > c1 ? c0 : c1;
+    return c01 > c2 ? c01 : c2;
   }
   static constexpr int best(int base) {
     int bf = 0, bw = worst(base);
@@ -222,7 +222,9 @@ template <int N, class PL = BlockPlan<N>> struct SmemGeom {
   using G = BlockGeom<N, 0, PL>;
   static constexpr int r0 = BoundaryPad<N, 0, 8, PL>::region;
   static constexpr int r1 = G::P > 2 ? BoundaryPad<N, 1, 8, PL>::region : 0;
-  static constexpr int BASE = G::P > 1 ? (r0 > r1 ? r0 : r1) : 0;
+  static constexpr int r2 = G::P > 3 ? BoundaryPad<N, 2, 8, PL>::region : 0;
+  static constexpr int r01 = r0 > r1 ? r0 : r1;
+  static constexpr int BASE = G::P > 1 ? (r01 > r2 ? r01 : r2) : 0;
   static constexpr int REGION = (G::P > 1 && G::T < 16) ? BASE + StrideSearch<N, PL>::best(BASE) : BASE;  // float2 per transform
   static constexpr int BYTES = G::TPB * REGION * 8;
 };

@@ -115,6 +115,8 @@ cudaError_t block_cap_prepare_n() {
   case 10: return FN<1024, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
   case 11: return FN<2048, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
   case 12: return FN<4096, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
+  case 13: return FN<8192, LAYOUT, DIR, CAP>(__VA_ARGS__);       \
+  case 14: return FN<16384, LAYOUT, DIR, CAP>(__VA_ARGS__);      \
   default: return cudaErrorInvalidValue;                         \
   }
 

@@ -171,6 +171,12 @@ FFTGEN_FI void middle_passes(float2 *sx, int t, const float2 *__restrict__ tw, f
       __syncthreads();
       smem_read_pass<G, N, 2, DIR>(sx, t, tw, v);
     }
+    if constexpr (G::P > 3) {
+      __syncthreads();
+      smem_write<G, N, 2>(sx, t, v);
+      __syncthreads();
+      smem_read_pass<G, N, 3, DIR>(sx, t, tw, v);
+    }
   }
 }
 

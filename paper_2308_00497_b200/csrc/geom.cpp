@@ -66,6 +66,8 @@ bool block_cap_distinct(int log2n, int cap) {
   case 10: return cap_distinct<1024>(cap);
   case 11: return cap_distinct<2048>(cap);
   case 12: return cap_distinct<4096>(cap);
+  case 13: return cap_distinct<8192>(cap);
+  case 14: return cap_distinct<16384>(cap);
   default: return false;
   }
 }

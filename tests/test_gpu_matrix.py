@@ -80,8 +80,8 @@ def test_full_dft_matrix_block_sizes(fg, l2, layout, direction):
         assert worst <= 2e-6, (n, layout, direction, tuning, worst)
 
 
-@pytest.mark.parametrize("l2,hint", [(7, 8), (8, 8), (9, 8), (9, 16), (10, 16), (11, 16), (11, 32), (12, 16),
-                                     (12, 32)])
+@pytest.mark.parametrize("l2,hint", [(7, 8), (8, 8), (9, 8), (9, 16), (10, 8), (10, 16), (11, 8), (11, 16), (11, 32),
+                                     (12, 8), (12, 16), (12, 32), (13, 16), (14, 16)])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 @pytest.mark.parametrize("direction", [-1, 1])
 def test_full_dft_matrix_radix_hint_plans(fg, l2, hint, layout, direction):

@@ -163,11 +163,14 @@ def test_pass_radix_hint_steers_block_passes(plan_tool):
     # measured defaults: radix-8 three-pass plans at 2^7..2^9; 64 keeps the two-pass ones
     assert passes(256) == [4, 8, 8] and passes(512) == [8, 8, 8] and passes(128) == [2, 8, 8]
     assert passes(256, 64) == [16, 16] and passes(512, 64) == [16, 32] and passes(128, 64) == [8, 16]
-    assert passes(4096, 16) == [16, 16, 16] and passes(4096, 32) == [4, 32, 32] and passes(4096, 8) == [64, 64]
+    assert passes(4096, 16) == [16, 16, 16] and passes(4096, 32) == [4, 32, 32]
     assert passes(2048, 16) == [8, 16, 16] and passes(2048, 32) == [2, 32, 32]
     assert passes(1024, 16) == [4, 16, 16] and passes(512, 16) == [2, 16, 16]
     assert passes(512, 8) == [8, 8, 8] and passes(256, 8) == [4, 8, 8] and passes(128, 8) == [2, 8, 8]
-    assert passes(256, 16) == passes(256, 64) and passes(1 << 13, 16) == passes(1 << 13)  # default fits / > 3
+    assert passes(1024, 8) == [2, 8, 8, 8] and passes(2048, 8) == [4, 8, 8, 8]
+    assert passes(256, 16) == passes(256, 64)                                            # the default fits
+    assert passes(1 << 13, 16) == [2, 16, 16, 16] and passes(1 << 14, 16) == [4, 16, 16, 16]
+    assert passes(4096, 8) == [8, 8, 8, 8] and passes(1 << 13, 8) == passes(1 << 13)    # > 4 passes: default
     assert passes(1 << 14, 32) == passes(1 << 14) and passes(64, 64) == passes(64)
     assert plan_tool("passes", 4096, 12)[0] == 1                                        # PlanError
     for n in (128, 256, 512, 1024, 2048, 4096):
@@ -176,7 +179,7 @@ def test_pass_radix_hint_steers_block_passes(plan_tool):
             prod = 1
             for r in rs:
                 prod *= r
-            assert prod == n and len(rs) <= 3
+            assert prod == n and len(rs) <= 4
 
 
 def test_fourstep_groups_cover_large_sizes(plan_tool):
