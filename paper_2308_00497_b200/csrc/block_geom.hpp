@@ -243,18 +243,18 @@ template <int N, class PL = BlockPlan<N>> struct SmemGeom {
 // are large and the compute of one group covers the next one's load.  N =
 // 4096 keeps one transform per CTA, single-buffered, six warps more per SM
 // (0.95-0.97; 2 x 2 transforms: 0.95), and 8192 is one transform per stage.
-template <int N> struct TmaGeom {
+template <int N, class PL = BlockPlan<N>> struct TmaGeom {
   static constexpr bool ENABLED = N >= 64 && N <= 8192;
-  static constexpr int T = BlockGeom<N>::T;
+  static constexpr int T = BlockGeom<N, 0, PL>::T;
   static constexpr int tp_bytes = (65536 / (8 * N)) > 0 ? 65536 / (8 * N) : 1;
   static constexpr int TP = N == 4096 ? 1 : tp_bytes;
-  using G = BlockGeom<N, TP>;
+  using G = BlockGeom<N, TP, PL>;
   static constexpr int THREADS = G::THREADS;
   // (three stages: 2^13 0.69 vs 0.86, 2^10 0.88 vs 0.98; single-buffered
   // 2^13: 0.77 / 0.81 vs 0.86 / 0.86)
   static constexpr int STAGES = N == 4096 ? 1 : 2;
   static constexpr int RAW = 8 * N;                                   // bytes per transform
-  static constexpr int XCH = 8 * SmemGeom<N>::REGION;                 // padded exchange bytes
+  static constexpr int XCH = 8 * SmemGeom<N, PL>::REGION;             // padded exchange bytes
   static constexpr int SLOT = ((RAW > XCH ? RAW : XCH) + 127) / 128 * 128;
   static constexpr int STAGE_BYTES = TP * SLOT;
   static constexpr int BYTES = STAGES * STAGE_BYTES + 128;            // + mbarriers

@@ -93,6 +93,9 @@ cudaError_t block_cap_launch_n(const BlockArgs &a, cudaStream_t s) {
   }
 }
 
+// (the persistent TMA kernel with these plans measured slower than both the
+// direct kernel and the default TMA plans -- DESIGN.md section 6 -- so the
+// capped plans run on the direct kernel only)
 template <int N, int LAYOUT, int DIR, int CAP>
 cudaError_t block_cap_prepare_n() {
   if constexpr (CapPlanGeom<N, CAP>::DISTINCT) {

@@ -246,14 +246,13 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                          (dist * esz) % 16 == 0;
     const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
-    if (p->ex.block_cap) return block_cap_launch(p->ex.log2n, p->ex.block_cap, layout, direction, a, s);
     if (p->use_tma && p->tma_grid > 0 && aligned) {
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
-      const int64_t groups = (batch + tp - 1) / tp;
-      const int grid = (int)std::min<int64_t>(groups, p->tma_grid);
-      return block_tma_launch(p->ex.log2n, layout, direction, a, grid,
-                              p->use_tma_store && out_aligned ? BLOCK_TMA_STORE : 0, s);
+      const int grid = (int)std::min<int64_t>((batch + tp - 1) / tp, p->tma_grid);
+      const int flags = p->use_tma_store && out_aligned ? BLOCK_TMA_STORE : 0;
+      return block_tma_launch(p->ex.log2n, layout, direction, a, grid, flags, s);
     }
+    if (p->ex.block_cap) return block_cap_launch(p->ex.log2n, p->ex.block_cap, layout, direction, a, s);
     return block_launch(p->ex.log2n, layout, direction, a, s);
   }
   case STRAT_FOURSTEP: {
@@ -473,7 +472,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       if ((e = block_prepare(p->ex.log2n, &per_sm)) != cudaSuccess)
         return bail(FFTGEN_ERR_GPUMAP, std::string("block kernel attributes: ") + cudaGetErrorString(e));
       p->tma_grid = block_tma_enabled(p->ex.log2n) ? per_sm * sms : 0;
-      if (p->ex.block_cap) {  // the radix hint's plan runs on the direct kernel
+      if (p->ex.block_cap) {  // the radix hint's plan runs on the direct kernel (measured fastest for it)
         if ((e = block_cap_prepare(p->ex.log2n, p->ex.block_cap)) != cudaSuccess)
           return bail(FFTGEN_ERR_GPUMAP, std::string("capped block kernel attributes: ") + cudaGetErrorString(e));
         p->tma_grid = 0;

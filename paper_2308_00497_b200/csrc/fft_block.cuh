@@ -243,8 +243,8 @@ FFTGEN_FI void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta
 // group's transforms are one contiguous run): interleaved at f * 8N, split re
 // at f * 4N and im at TP * 4N + f * 4N, so one bulk copy per plane moves the
 // whole group; otherwise transform f sits in its slot at f * SLOT.
-template <int N, int LAYOUT> struct RawAt {
-  using TG = TmaGeom<N>;
+template <int N, int LAYOUT, class PL = BlockPlan<N>> struct RawAt {
+  using TG = TmaGeom<N, PL>;
   static FFTGEN_FI char *re(char *stage, int f, bool packed) {
     return stage + (packed ? f * (LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N) : f * TG::SLOT);
   }
@@ -253,9 +253,9 @@ template <int N, int LAYOUT> struct RawAt {
   }
 };
 
-template <int N, int LAYOUT>
+template <int N, int LAYOUT, class PL = BlockPlan<N>>
 FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t group) {
-  using TG = TmaGeom<N>;
+  using TG = TmaGeom<N, PL>;
   const int64_t b0 = group * TG::TP;
   const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
@@ -263,7 +263,7 @@ FFTGEN_FI void tma_issue(const BlockArgs &a, char *stage, uint64_t *bar, int64_t
   if (a.idist == N) {  // packed: one copy per plane for the whole group
     if (LAYOUT == LAYOUT_SPLIT) {
       bulk_g2s(stage, reinterpret_cast<const float *>(a.in0) + b0 * N, cnt * plane, bar);
-      bulk_g2s(RawAt<N, LAYOUT>::im(stage, 0, true), reinterpret_cast<const float *>(a.in1) + b0 * N,
+      bulk_g2s(RawAt<N, LAYOUT, PL>::im(stage, 0, true), reinterpret_cast<const float *>(a.in1) + b0 * N,
                cnt * plane, bar);
     } else {
       bulk_g2s(stage, reinterpret_cast<const float2 *>(a.in0) + b0 * N, cnt * plane, bar);
@@ -295,9 +295,10 @@ FFTGEN_FI void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "me
 // Stage the last pass's outputs in the raw layout (RawAt) for a bulk store.
 template <class G, int N, int LAYOUT>
 FFTGEN_FI void smem_write_out(char *stage, int f, bool packed, int t, const float2 *v) {
+  using RA = RawAt<N, LAYOUT, typename G::PL>;
   constexpr int q = G::P - 1;
   constexpr int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / R;
-  char *re = RawAt<N, LAYOUT>::re(stage, f, packed);
+  char *re = RA::re(stage, f, packed);
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
@@ -306,7 +307,7 @@ FFTGEN_FI void smem_write_out(char *stage, int f, bool packed, int t, const floa
       const int e = (B * cols + m) * k + c;
       if constexpr (LAYOUT == LAYOUT_SPLIT) {
         reinterpret_cast<float *>(re)[e] = v[j * R + B].x;
-        reinterpret_cast<float *>(RawAt<N, LAYOUT>::im(stage, f, packed))[e] = v[j * R + B].y;
+        reinterpret_cast<float *>(RA::im(stage, f, packed))[e] = v[j * R + B].y;
       } else {
         reinterpret_cast<float2 *>(re)[e] = v[j * R + B];
       }
@@ -314,16 +315,16 @@ FFTGEN_FI void smem_write_out(char *stage, int f, bool packed, int t, const floa
   }
 }
 
-template <int N, int LAYOUT>
+template <int N, int LAYOUT, class PL = BlockPlan<N>>
 FFTGEN_FI void tma_store(const BlockArgs &a, char *stage, int64_t group) {
-  using TG = TmaGeom<N>;
+  using TG = TmaGeom<N, PL>;
   const int64_t b0 = group * TG::TP;
   const int cnt = (int)(a.batch - b0 < TG::TP ? a.batch - b0 : TG::TP);
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
   if (a.odist == N) {  // packed
     if (LAYOUT == LAYOUT_SPLIT) {
       bulk_s2g(reinterpret_cast<float *>(a.out0) + b0 * N, stage, cnt * plane);
-      bulk_s2g(reinterpret_cast<float *>(a.out1) + b0 * N, RawAt<N, LAYOUT>::im(stage, 0, true), cnt * plane);
+      bulk_s2g(reinterpret_cast<float *>(a.out1) + b0 * N, RawAt<N, LAYOUT, PL>::im(stage, 0, true), cnt * plane);
     } else {
       bulk_s2g(reinterpret_cast<float2 *>(a.out0) + b0 * N, stage, cnt * plane);
     }
@@ -345,9 +346,9 @@ FFTGEN_FI void tma_store(const BlockArgs &a, char *stage, int64_t group) {
 
 // STORE_TMA: outputs go smem -> HBM by cp.async.bulk (needs 16-byte aligned
 // output rows) instead of per-thread coalesced st.global.
-template <int N, int LAYOUT, int DIR, bool STORE_TMA>
-__global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
-  using TG = TmaGeom<N>;
+template <int N, int LAYOUT, int DIR, bool STORE_TMA, class PL = BlockPlan<N>>
+__global__ void __launch_bounds__(TmaGeom<N, PL>::THREADS) fft_block_tma_kernel(const BlockArgs args) {
+  using TG = TmaGeom<N, PL>;
   using G = typename TG::G;
   static_assert(TG::STAGES >= 1 && TG::STAGES <= 4, "1-4 stages");
   constexpr int NST = TG::STAGES;
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
   if (tid == 0) {
     for (int s = 0; s < TG::STAGES; ++s) {
       const int64_t g = blockIdx.x + s * stride;
-      if (g < groups) tma_issue<N, LAYOUT>(args, smem + s * TG::STAGE_BYTES, &bars[s], g);
+      if (g < groups) tma_issue<N, LAYOUT, PL>(args, smem + s * TG::STAGE_BYTES, &bars[s], g);
     }
   }
   // 2-pass plans: this thread's pass-1 twiddle bases live in registers
@@ -385,11 +386,11 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
 
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
-      const float *re = reinterpret_cast<const float *>(RawAt<N, LAYOUT>::re(stage, f, packed_in));
-      const float *im = reinterpret_cast<const float *>(RawAt<N, LAYOUT>::im(stage, f, packed_in));
+      const float *re = reinterpret_cast<const float *>(RawAt<N, LAYOUT, PL>::re(stage, f, packed_in));
+      const float *im = reinterpret_cast<const float *>(RawAt<N, LAYOUT, PL>::im(stage, f, packed_in));
       pass0<G, DIR>(t, v, [&](int e) { return make_float2(re[e], im[e]); });
     } else {
-      const float2 *x = reinterpret_cast<const float2 *>(RawAt<N, LAYOUT>::re(stage, f, packed_in));
+      const float2 *x = reinterpret_cast<const float2 *>(RawAt<N, LAYOUT, PL>::re(stage, f, packed_in));
       pass0<G, DIR>(t, v, [&](int e) { return x[e]; });
     }
     __syncthreads();  // raw stage fully consumed; reuse it as the exchange
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       if (gn < groups) {
         const int sp = (it - 1) % NST;
         bulk_wait_read0();
-        tma_issue<N, LAYOUT>(args, smem + sp * TG::STAGE_BYTES, &bars[sp], gn);
+        tma_issue<N, LAYOUT, PL>(args, smem + sp * TG::STAGE_BYTES, &bars[sp], gn);
       }
     }
     float2 *sx = reinterpret_cast<float2 *>(slot);
@@ -419,10 +420,10 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
       fence_proxy_async();  // make generic-proxy writes visible to the bulk copy
       __syncthreads();
       if (tid == 0) {
-        tma_store<N, LAYOUT>(args, stage, g);
+        tma_store<N, LAYOUT, PL>(args, stage, g);
         if (NST == 1 && g + stride < groups) {  // refill once the store has read the stage
           bulk_wait_read0();
-          tma_issue<N, LAYOUT>(args, stage, &bars[0], g + stride);
+          tma_issue<N, LAYOUT, PL>(args, stage, &bars[0], g + stride);
         }
       }
       (void)b;
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(TmaGeom<N>::THREADS) fft_block_tma_kernel(cons
         const int64_t gn = g + TG::STAGES * stride;
         if (gn < groups) {
           fence_proxy_async();
-          tma_issue<N, LAYOUT>(args, stage, &bars[s], gn);
+          tma_issue<N, LAYOUT, PL>(args, stage, &bars[s], gn);
         }
       }
       if (b < args.batch) store_last<G, LAYOUT>(args, b * args.odist, t, v);
