@@ -12,11 +12,13 @@ def main():
     import torch
     import paper_2308_00497_b200 as fg
 
-    cases = [(64, 5), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 150),  # K2 direct / TMA
+    cases = [(64, 5), (256, 7), (512, 3), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 150),  # K2
              (1 << 15, 3), (1 << 16, 2), (1 << 18, 1), (1 << 21, 1)]          # K5, K3 (+TMA groups)
     # non-default kernel selections: (PipelineConfig overrides, n, batch)
     optin = [(dict(tuning=fg.TUNE_NO_TMA), 1 << 14, 3), (dict(tuning=fg.TUNE_NO_TMA_STORE), 1 << 14, 150),
-             (dict(cluster_size=16), 1 << 16, 3), (dict(tuning=fg.TUNE_GROUP_TMA_ALL, cluster_size=-1), 1 << 16, 2)]
+             (dict(cluster_size=16), 1 << 16, 3), (dict(tuning=fg.TUNE_GROUP_TMA_ALL, cluster_size=-1), 1 << 16, 2),
+             (dict(pass_radix=16), 4096, 3), (dict(pass_radix=8), 2048, 3), (dict(pass_radix=16), 1 << 14, 2),
+             (dict(tuning=16), 1 << 22, 1), (dict(tuning=16 | 4), 1 << 24, 1)]
     runs = [({}, n, b) for n, b in cases] + (optin if os.environ.get("SANITIZE_OPTIN") else [])
     for env, n, batch in runs:
         for layout in ("interleaved", "split"):
@@ -33,6 +35,17 @@ def main():
             torch.cuda.synchronize()
             print(env, n, batch, layout, plan.describe().splitlines()[2][:60], flush=True)
             plan.close()
+    # device input generator and the distributed stages (NCCL-chunk and peer variants), 4 emulated ranks
+    fg.seeded_input(4096, 3, "split")
+    fg.seeded_input(1000, 2, "interleaved", dist=1003)
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    n, world = 1 << 16, 4
+    blocks = [torch.complex(torch.rand(n // world, device="cuda"), torch.rand(n // world, device="cuda"))
+              for _ in range(world)]
+    for t in ("nccl", "p2p"):
+        EmulatedDistributedFFT(n, world, transport=t).execute(blocks)
+    torch.cuda.synchronize()
+    print("seeded_input + distributed stages ok", flush=True)
 
 
 if __name__ == "__main__":
