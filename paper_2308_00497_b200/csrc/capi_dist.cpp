@@ -179,6 +179,16 @@ fftgen_status fftgen_dist_butterfly_peers(const fftgen_dist_plan *p, int directi
   if ((st = check_peers(p, in_blocks, "input")) != FFTGEN_OK ||
       (st = check_peers(p, (const void *const *)recv_blocks, "receive")) != FFTGEN_OK)
     return st;
+  // every receive block is written while other ranks still read every input
+  // block: the two sets must not share a byte
+  const uintptr_t bytes = (uintptr_t)p->m * 8;
+  for (int r = 0; r < p->world; ++r)
+    for (int s = 0; s < p->world; ++s) {
+      const uintptr_t a = (uintptr_t)in_blocks[r], b = (uintptr_t)recv_blocks[s];
+      if (a < b + bytes && b < a + bytes)
+        return dfail(FFTGEN_ERR_EXEC, "receive block of rank " + std::to_string(s) + " overlaps the input block of rank " +
+                                          std::to_string(r));
+    }
   if (direction != FFTGEN_FORWARD && direction != FFTGEN_INVERSE)
     return dfail(FFTGEN_ERR_EXEC, "direction must be FFTGEN_FORWARD (-1) or FFTGEN_INVERSE (+1)");
   Guard g(p->device);
@@ -233,6 +243,9 @@ fftgen_status fftgen_seeded_input(int layout, int64_t n, int64_t batch, uint64_t
     return dfail(FFTGEN_ERR_EXEC, "unknown complex layout " + std::to_string(layout));
   if (n < 1 || batch < 0 || dist < n) return dfail(FFTGEN_ERR_DIMENSION, "bad seeded_input geometry");
   if (!out0 || (split && !out1)) return dfail(FFTGEN_ERR_EXEC, "NULL data pointer");
+  const uintptr_t al = split ? 4 : 8;
+  if ((uintptr_t)out0 % al || (split && (uintptr_t)out1 % al))
+    return dfail(FFTGEN_ERR_EXEC, "data pointer not aligned to its " + std::to_string(al) + "-byte element");
   Guard g(device);
   if (g.err != cudaSuccess) return dcuda(g.err, "cudaSetDevice");
   cudaError_t e = seeded_input(split, out0, out1, n, batch, seed0, dist, (cudaStream_t)stream);

@@ -210,6 +210,8 @@ def test_peer_tables_validated(fg):
         p.butterfly_peers([x, 0], [y, y])
     with pytest.raises(fg.ExecError):
         p.unpack_peers([x, y], y)                  # out aliases a source block
+    with pytest.raises(fg.ExecError):
+        p.butterfly_peers([x, y], [y, torch.zeros_like(x)])   # a receive block is an input block
 
 
 def test_distributed_p2p_symmetric_memory_world1(fg, orc):
