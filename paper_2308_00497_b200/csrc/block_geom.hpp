@@ -312,10 +312,11 @@ template <int N> struct Tma1Geom {
 // tiles) a half-warp mixes f and t, so the stride is searched here by
 // simulating every pass boundary's accesses like PadSearch (ideal: 2
 // wavefronts per warp access).
-template <int NS, int TC, class PL> struct GroupRegSearch {
+template <int NS, int TC, class PL, int ELEM = 8> struct GroupRegSearch {
   using G = BlockGeom<NS, 0, PL>;
-  static constexpr Pad PAD0 = BoundaryPad<NS, 0, 8, PL>::value;
-  static constexpr Pad PAD1 = G::P > 2 ? BoundaryPad<NS, 1, 8, PL>::value : Pad{16, 0};
+  static constexpr int WAVE = 128 / ELEM;  // lanes one shared-memory wavefront serves
+  static constexpr Pad PAD0 = BoundaryPad<NS, 0, ELEM, PL>::value;
+  static constexpr Pad PAD1 = G::P > 2 ? BoundaryPad<NS, 1, ELEM, PL>::value : Pad{16, 0};
   static constexpr int side_cost(int p, int side, bool rows_map, int reg) {
     const int T = G::T, q = p + side;
     const int R = G::R(q), cols = G::COLS(q), k = G::K(q), J = G::RMAX / G::R(q);
@@ -326,15 +327,15 @@ template <int NS, int TC, class PL> struct GroupRegSearch {
     for (int jj = 0; jj < 2; ++jj)
       for (int xx = 0; xx < 4; ++xx) {
         int wavefronts = 0;
-        for (int half = 0; half < 2; ++half) {
-          int cnt[16] = {};
+        for (int half = 0; half < 32 / WAVE; ++half) {
+          int cnt[32] = {};
           int deg = 0;
-          for (int l = 16 * half; l < 16 * half + 16; ++l) {
+          for (int l = WAVE * half; l < WAVE * half + WAVE; ++l) {
             const int f = rows_map ? l / T : l % TC, t = rows_map ? l % T : l / TC;
             if (f >= TC || t >= T) continue;
             const int u = t + js[jj] * T, m = u / k, c = u % k, x = xs[xx];
             const int idx = side == 0 ? (x * cols + m) * k + c : (m * R + x) * k + c;
-            const int b = (padded(idx, pd) + f * reg) % 16;
+            const int b = (padded(idx, pd) + f * reg) % WAVE;
             cnt[b]++;
             deg = cnt[b] > deg ? cnt[b] : deg;
           }

@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(TmaGeom<N, PL>::THREADS) fft_block_tma_kernel(
 template <class G, int N, int p, int COMP>
 FFTGEN_FI void plane_write(float *X, int t, const float2 *v) {
   constexpr int R = G::R(p), cols = G::COLS(p), k = G::K(p), J = G::RMAX / R;
-  constexpr Pad pd = BoundaryPad<N, p, 4>::value;
+  constexpr Pad pd = BoundaryPad<N, p, 4, typename G::PL>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;
@@ -461,7 +461,7 @@ FFTGEN_FI void plane_write(float *X, int t, const float2 *v) {
 template <class G, int N, int p, int COMP>  // reader of pass p (pad of boundary p-1)
 FFTGEN_FI void plane_read(const float *X, int t, float2 *v) {
   constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R;
-  constexpr Pad pd = BoundaryPad<N, p - 1, 4>::value;
+  constexpr Pad pd = BoundaryPad<N, p - 1, 4, typename G::PL>::value;
 #pragma unroll
   for (int j = 0; j < J; ++j) {
     const int u = t + j * G::T, m = u / k, c = u % k;

@@ -230,4 +230,120 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
   }
 }
 
+// ---- NS >= 2^11: one raw stage + an fp32 exchange plane --------------------
+// The 128 KB tiles of the 2^11 / 2^12 groups leave room for one raw stage
+// only; exchanging through the stage itself (fft_group_tma_kernel) delays the
+// next tile's TMA load until pass 1 has read the exchange.  Here the exchange
+// goes through a separate padded fp32 plane (re, then im: the 2^14 block
+// kernel's schedule), so the stage is refilled right after pass 0 and the
+// load overlaps the exchange, pass 1 and the stores.
+template <int NS> struct GroupPlaneGeom {
+  using GG = GroupGeom<NS>;
+  using PL = typename GG::PL;
+  using G = typename GG::G;
+  static constexpr int TC = GG::TC, THREADS = GG::THREADS;
+  static constexpr Pad PAD = BoundaryPad<NS, 0, 4, PL>::value;
+  static constexpr int EXP = padded(NS - 1, PAD) + 1;  // plane floats per column
+  static constexpr int REGP = GroupRegSearch<NS, TC, PL, 4>::best(EXP | 1);
+  static constexpr int RAW = TC * NS * 8;
+  static constexpr int PLANE = (TC * REGP * 4 + 127) / 128 * 128;
+  static constexpr int BYTES = RAW + PLANE + 64;
+  static constexpr bool ENABLED = NS >= 2048 && G::P == 2 && BYTES <= 227 * 1024;
+};
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
+__global__ void __launch_bounds__(GroupPlaneGeom<NS>::THREADS, 1)
+fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
+  using PG = GroupPlaneGeom<NS>;
+  using G = typename PG::G;
+  static_assert(PG::ENABLED, "plane-exchange group kernel: NS >= 2048, two passes");
+  static_assert(GroupTmaGeom<NS>::RAW == PG::RAW, "same raw tile as the TMA issue helper");
+  constexpr int TC = PG::TC, T = G::T, REGP = PG::REGP;
+  constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
+  constexpr int R1 = G::R(1), COLS1 = G::COLS(1);
+  const GroupArgs &a = ta.g;
+  extern __shared__ float4 smem_f4[];
+  char *stage = reinterpret_cast<char *>(smem_f4);
+  float *P = reinterpret_cast<float *>(stage + PG::RAW);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(stage + PG::RAW + PG::PLANE);
+  const int tid = threadIdx.x;
+  const int64_t total = ta.items, stride = gridDim.x;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < total) group_tma_issue<NS, LIN, ROWS>(ta, stage, bar, blockIdx.x);
+  int it = 0;
+  for (int64_t item = blockIdx.x; item < total; item += stride, ++it) {
+    const int64_t b = item / a.tiles_per_outer, tt = item - b * a.tiles_per_outer;
+    int64_t m0, c0;
+    if (ROWS) {
+      m0 = tt * TC;
+      c0 = 0;
+    } else {
+      const int64_t u0 = tt * TC;
+      m0 = u0 / a.k;
+      c0 = u0 - m0 * a.k;
+    }
+    mbar_wait(bar, it & 1);
+    // ---- pass 0: raw tile -> registers, global twiddle, radix-R0 codelets ----
+    float2 v[G::RMAX];
+    const int f0 = ROWS ? tid / T : tid % TC;
+    const int t0 = ROWS ? tid % T : tid / TC;
+    {
+      const int64_t m = ROWS ? m0 + f0 : m0;
+      const bool tw = a.cols > 1;
+      const float2 *qm = a.tw_q + m;
+#pragma unroll
+      for (int j = 0; j < J0; ++j) {
+        const int c = t0 + j * T;
+#pragma unroll
+        for (int A0 = 0; A0 < R0; ++A0) {
+          const int A = A0 * K0 + c;
+          const int e = ROWS ? f0 * NS + A : A * TC + f0;
+          if constexpr (LIN == LAYOUT_SPLIT) {
+            const float *sp = reinterpret_cast<const float *>(stage);
+            v[j * R0 + A0] = make_float2(sp[e], sp[NS * TC + e]);
+          } else {
+            v[j * R0 + A0] = reinterpret_cast<const float2 *>(stage)[e];
+          }
+        }
+        if (tw) {
+          const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
+#pragma unroll
+          for (int A0 = 0; A0 < R0; ++A0) {
+            float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
+            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+          }
+        }
+        reg_fft<R0, DIR>(v + j * R0);
+      }
+    }
+    __syncthreads();  // raw tile consumed: fetch the next one behind the exchange
+    if (tid == 0 && item + stride < total) {
+      fence_proxy_async();
+      group_tma_issue<NS, LIN, ROWS>(ta, stage, bar, item + stride);
+    }
+    // ---- exchange through the plane (re, then im) and pass 1 ----------------
+    const int f = tid % TC, t = tid / TC;
+    plane_write<G, NS, 0, 0>(P + f0 * REGP, t0, v);
+    __syncthreads();
+    plane_read<G, NS, 1, 0>(P + f * REGP, t, v);
+    __syncthreads();
+    plane_write<G, NS, 0, 1>(P + f0 * REGP, t0, v);
+    __syncthreads();
+    plane_read<G, NS, 1, 1>(P + f * REGP, t, v);
+    pass_compute<G, 1, DIR>(t, a.tw_local, v);
+    const int64_t ob = b * a.odist;
+#pragma unroll
+    for (int B = 0; B < R1; ++B) {
+      const int64_t e = B * COLS1 + t;
+      const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
+      SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+    }
+    // the next iteration's plane writes follow its post-pass-0 barrier
+  }
+}
+
 }  // namespace fftgen_b200

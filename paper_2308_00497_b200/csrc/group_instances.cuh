@@ -50,21 +50,39 @@ cudaError_t group_prepare_ns() {
   return group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>();
 }
 
+// NS >= 2^11: the TMA-tile variant is the plane-exchange kernel (next tile
+// fetched right after pass 0); -DFFTGEN_GROUP_PLANE=0 keeps the stage-exchange one
+#ifndef FFTGEN_GROUP_PLANE
+#define FFTGEN_GROUP_PLANE 1
+#endif
+template <int NS> constexpr bool use_plane() { return FFTGEN_GROUP_PLANE && GroupPlaneGeom<NS>::ENABLED; }
+
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
 cudaError_t group_tma_launch_t(const GroupTmaArgs &ta, int grid, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
-  fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS><<<grid, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES, s>>>(ta);
+  if constexpr (use_plane<NS>())
+    fft_group_plane_kernel<NS, LIN, LOUT, DIR, ROWS>
+        <<<grid, GroupPlaneGeom<NS>::THREADS, GroupPlaneGeom<NS>::BYTES, s>>>(ta);
+  else
+    fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS><<<grid, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES, s>>>(ta);
   return cudaGetLastError();
 }
 
-template <int NS, int LIN, int LOUT, int DIR, bool ROWS> cudaError_t group_tma_prepare_t(int *bps) {
-  auto k = fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GroupTmaGeom<NS>::BYTES);
+template <class K> cudaError_t prepare_kernel(K k, int threads, int bytes, int *bps) {
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   int n = 0;
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, bytes);
   if (n < *bps) *bps = n;
   return e;
+}
+
+template <int NS, int LIN, int LOUT, int DIR, bool ROWS> cudaError_t group_tma_prepare_t(int *bps) {
+  if constexpr (use_plane<NS>())
+    return prepare_kernel(fft_group_plane_kernel<NS, LIN, LOUT, DIR, ROWS>, GroupPlaneGeom<NS>::THREADS,
+                          GroupPlaneGeom<NS>::BYTES, bps);
+  else
+    return prepare_kernel(fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS>, GroupTmaGeom<NS>::THREADS,
+                          GroupTmaGeom<NS>::BYTES, bps);
 }
 
 template <int NS, int DIR>

@@ -308,18 +308,21 @@ ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix) {
 }
 
 std::vector<int> group_split(int log2n, int mode) {
-  // 2 groups up to 2^21 (NS <= 2^11), 3 groups up to 2^28, 4 groups up to
+  // 2 groups up to 2^22 (NS <= 2^11), 3 groups up to 2^28, 4 groups up to
   // 2^30; sizes as even as possible.  mode SPLIT_GROUPS_1024: NS <= 2^10 (2
   // groups up to 2^20); SPLIT_TWO_PASS: 2 groups up to 2^24 (NS <= 2^12, 32 N
   // bytes of HBM traffic instead of 48 N).  Measured on B200 (1 GiB batches,
   // split / interleaved ms): 2^21 10+11 1.05 / 1.00 vs 7+7+7 1.17 / 1.14;
   // 2^22 11+11 1.23 / 1.16 vs 7+7+8 1.15 / 1.08; 2^24 12+12 1.95 / 1.54 vs
   // 8+8+8 1.15 / 1.07 (the 128 KB NS = 4096 tiles leave one CTA per SM).
+  // With the plane-exchange TMA kernel for NS >= 2^11 (round 2): 2^22 11+11
+  // 1.09 / 1.00 vs 7+7+8 1.13 / 1.10; 2^23 11+12 1.37 / 1.13 vs 1.14 / 1.07
+  // and 2^24 12+12 1.58 / 1.27 vs 1.14 / 1.08 stay three-pass.
   // Earlier:
   // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
   // 64-byte segments).
-  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : 21);
+  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : 22);
   const int g = log2n <= two ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs
@@ -331,6 +334,9 @@ std::vector<int> group_split(int log2n, int mode) {
   return out;
 }
 
-bool group_prefers_tma(int log2ns, bool first, bool rows) { return !rows && first && log2ns >= 9; }
+// TMA tiles for first-group columns at NS >= 2^9 and for every NS >= 2^11
+// group (the plane-exchange kernel: 2^21 rows 0.339 / 0.363 vs 0.335 / 0.351
+// with the plain rows kernel, 2^22 1.09 / 1.00 vs 1.12 / 1.04 ms per GiB)
+bool group_prefers_tma(int log2ns, bool first, bool rows) { return (!rows && first && log2ns >= 9) || log2ns >= 11; }
 
 }  // namespace fftgen_b200
