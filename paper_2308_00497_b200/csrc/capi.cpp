@@ -836,13 +836,14 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
       group_geom(d.log2ns, &threads, &tc, &smem, &r0);
       const bool tma = i < p->group_tma_grid.size() && p->group_tma_grid[i] > 0;
       o << "  group " << i << ": "
-        << (tma ? (d.log2ns >= 11 ? "fft_group_plane_kernel<" : "fft_group_tma_kernel<") : "fft_group_kernel<") << d.ns
+        << (tma ? (group_plane(d.log2ns) ? "fft_group_plane_kernel<" : "fft_group_tma_kernel<") : "fft_group_kernel<")
+        << d.ns
         << "> radix "
         << d.ns << " s=" << d.s
         << " cols=" << d.cols << " k=" << d.k << (d.rows ? " rows (transposed store)" : " columns")
         << " grid[" << p->cfg.batch * (d.cols * d.k / tc) << "] block[" << threads << "] smem=" << smem
         << "B tile=" << tc
-        << (tma ? (d.log2ns >= 11 ? " (persistent, TMA tensor tile + fp32 exchange plane, next tile fetched after pass 0; "
+        << (tma ? (group_plane(d.log2ns) ? " (persistent, TMA tensor tile + fp32 exchange plane, next tile fetched after pass 0; "
                                     "plain kernel if unaligned)"
                                   : " (persistent, TMA tensor tiles double-buffered; plain kernel if unaligned)")
                 : "")

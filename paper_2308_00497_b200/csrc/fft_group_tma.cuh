@@ -237,6 +237,12 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
 // goes through a separate padded fp32 plane (re, then im: the 2^14 block
 // kernel's schedule), so the stage is refilled right after pass 0 and the
 // load overlaps the exchange, pass 1 and the stores.
+#ifndef FFTGEN_PLANE_MIN_LOG2
+#define FFTGEN_PLANE_MIN_LOG2 11
+#endif
+#ifndef FFTGEN_GROUP_PLANE
+#define FFTGEN_GROUP_PLANE 1
+#endif
 template <int NS> struct GroupPlaneGeom {
   using GG = GroupGeom<NS>;
   using PL = typename GG::PL;
@@ -248,15 +254,16 @@ template <int NS> struct GroupPlaneGeom {
   static constexpr int RAW = TC * NS * 8;
   static constexpr int PLANE = (TC * REGP * 4 + 127) / 128 * 128;
   static constexpr int BYTES = RAW + PLANE + 64;
-  static constexpr bool ENABLED = NS >= 2048 && G::P == 2 && BYTES <= 227 * 1024;
+  static constexpr bool ENABLED = NS >= (1 << FFTGEN_PLANE_MIN_LOG2) && G::P == 2 && BYTES <= 227 * 1024;
+  static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 1 ? 2 : 1;
 };
 
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
-__global__ void __launch_bounds__(GroupPlaneGeom<NS>::THREADS, 1)
+__global__ void __launch_bounds__(GroupPlaneGeom<NS>::THREADS, GroupPlaneGeom<NS>::MIN_BLOCKS)
 fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
   using PG = GroupPlaneGeom<NS>;
   using G = typename PG::G;
-  static_assert(PG::ENABLED, "plane-exchange group kernel: NS >= 2048, two passes");
+  static_assert(PG::ENABLED, "plane-exchange group kernel: NS >= 2^FFTGEN_PLANE_MIN_LOG2, two passes");
   static_assert(GroupTmaGeom<NS>::RAW == PG::RAW, "same raw tile as the TMA issue helper");
   constexpr int TC = PG::TC, T = G::T, REGP = PG::REGP;
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;

@@ -50,11 +50,9 @@ cudaError_t group_prepare_ns() {
   return group_prepare_t<NS, LAYOUT_SCRATCH, LAYOUT_SCRATCH, DIR, false>();
 }
 
-// NS >= 2^11: the TMA-tile variant is the plane-exchange kernel (next tile
-// fetched right after pass 0); -DFFTGEN_GROUP_PLANE=0 keeps the stage-exchange one
-#ifndef FFTGEN_GROUP_PLANE
-#define FFTGEN_GROUP_PLANE 1
-#endif
+// NS >= 2^FFTGEN_PLANE_MIN_LOG2: the TMA-tile variant is the plane-exchange
+// kernel (next tile fetched right after pass 0); -DFFTGEN_GROUP_PLANE=0 keeps
+// the stage-exchange one
 template <int NS> constexpr bool use_plane() { return FFTGEN_GROUP_PLANE && GroupPlaneGeom<NS>::ENABLED; }
 
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>

@@ -76,6 +76,8 @@ bool encode_tile_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, 
                       unsigned char (*tmap)[128]);
 cudaError_t group_tma_launch(int log2ns, int shape, int dir, const GroupTmaArgs &ta, int grid, cudaStream_t s);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
+// whether the NS-point group's TMA variant is the plane-exchange kernel
+bool group_plane(int log2ns);
 
 // K5: one transform per thread-block cluster, N = NS0 * NS1 (2^14 .. 2^17),
 // intermediate exchanged through distributed shared memory (fft_cluster.cuh).

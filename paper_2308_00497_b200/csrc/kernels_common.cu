@@ -181,6 +181,7 @@ cudaError_t strided_copy(const float *in, float *out, int64_t rows, int width, i
 
 // ---- K3 group kernels ------------------------------------------------------
 #include "fft_group.cuh"
+#include "fft_group_tma.cuh"
 
 namespace fftgen_b200 {
 
@@ -208,6 +209,15 @@ cudaError_t group_tma_prepare(int log2ns, int *bps) {
   *bps = 1 << 30;
   cudaError_t e = group_tma_prepare_f(log2ns, bps);
   return e != cudaSuccess ? e : group_tma_prepare_b(log2ns, bps);
+}
+
+bool group_plane(int log2ns) {
+  switch (log2ns) {
+  case 10: return FFTGEN_GROUP_PLANE && GroupPlaneGeom<1024>::ENABLED;
+  case 11: return FFTGEN_GROUP_PLANE && GroupPlaneGeom<2048>::ENABLED;
+  case 12: return FFTGEN_GROUP_PLANE && GroupPlaneGeom<4096>::ENABLED;
+  default: return false;
+  }
 }
 
 cudaError_t group_tma_launch(int log2ns, int shape, int dir, const GroupTmaArgs &ta, int grid, cudaStream_t s) {

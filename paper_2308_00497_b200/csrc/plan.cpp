@@ -337,6 +337,11 @@ std::vector<int> group_split(int log2n, int mode) {
 // TMA tiles for first-group columns at NS >= 2^9 and for every NS >= 2^11
 // group (the plane-exchange kernel: 2^21 rows 0.339 / 0.363 vs 0.335 / 0.351
 // with the plain rows kernel, 2^22 1.09 / 1.00 vs 1.12 / 1.04 ms per GiB)
-bool group_prefers_tma(int log2ns, bool first, bool rows) { return (!rows && first && log2ns >= 9) || log2ns >= 11; }
+#ifndef FFTGEN_PLANE_MIN_LOG2
+#define FFTGEN_PLANE_MIN_LOG2 11
+#endif
+bool group_prefers_tma(int log2ns, bool first, bool rows) {
+  return (!rows && first && log2ns >= 9) || log2ns >= FFTGEN_PLANE_MIN_LOG2;
+}
 
 }  // namespace fftgen_b200
