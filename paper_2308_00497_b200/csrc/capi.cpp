@@ -443,7 +443,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
                                   (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
                                       ? SPLIT_GROUPS_1024
                                       : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT),
-                                  cfg->pass_radix);
+                                  cfg->pass_radix, cfg->layout);
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -726,7 +726,7 @@ fftgen_status fftgen_program_text(const fftgen_config *cfg, int what, char *buf,
                           (cfg->tuning & FFTGEN_TUNE_GROUPS_1024)
                               ? SPLIT_GROUPS_1024
                               : ((cfg->tuning & FFTGEN_TUNE_TWO_PASS) ? SPLIT_TWO_PASS : SPLIT_DEFAULT),
-                          cfg->pass_radix);
+                          cfg->pass_radix, cfg->layout);
       break;
     case FFTGEN_TEXT_RADICES: {
       std::ostringstream o;

@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
     if (tid < CG::THREADS0) smem_write<G0, NS0, 0>(S + f0 * CG::REG0, t0, w);
   };
 
+  // pass-1 twiddle bases of both group sub-FFTs (fft_group.cuh, FFTGEN_GROUP_PQ):
+  // this thread's butterflies t0 / tid / TC1 are the same for every transform
+  GroupTw<G0> gtw0;
+  if (tid < CG::THREADS0) gtw0.load(a.tw_local0, t0);
+  GroupTw<G1> gtw1;
+  if (tid < CG::THREADS1) gtw1.load(a.tw_local1, tid / CG::TC1);
   int it = 0;
   if (b0 < a.batch) g0_front(0);
   for (int64_t b = b0; b < a.batch; b += stride, ++it) {
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
     float2 v[G0::RMAX > G1::RMAX ? G0::RMAX : G1::RMAX];
     // ---- group 0, pass 1: padded exchange in S -> registers ---------------
     __syncthreads();
-    if (tid < CG::THREADS0) smem_read_pass<G0, NS0, 1, DIR>(S + f0 * CG::REG0, t0, a.tw_local0, v);
+    if (tid < CG::THREADS0) group_passes_rest<G0, NS0, DIR, 0, 0>(S + f0 * CG::REG0, t0, a.tw_local0, v, gtw0);
     __syncthreads();  // S free: fetch the next transform's tile behind the rest of this one
     if (tid == 0 && b + stride < a.batch) {
       fence_proxy_async();
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(ClusterGeom<NS0, NS1, C>::THREADS, ClusterGeom
     if (tid < CG::THREADS1) smem_write<G1, NS1, 0>(X + f1 * CG::REG1, t1, v);
     __syncthreads();
     const int f = tid % CG::TC1, t = tid / CG::TC1;
-    if (tid < CG::THREADS1) smem_read_pass<G1, NS1, 1, DIR>(X + f * CG::REG1, t, a.tw_local1, v);
+    if (tid < CG::THREADS1) group_passes_rest<G1, NS1, DIR, 0, 0>(X + f * CG::REG1, t, a.tw_local1, v, gtw1);
     if constexpr (TSTORE) {
       // output rows e of this CTA's TC1 columns m: box [e][f] in X, one tensor store
       static_assert(NS1 * CG::TC1 <= CG::XLEN, "the output box fits X");

@@ -81,6 +81,33 @@ template <int BARID, int THREADS> FFTGEN_FI void compute_sync() {
 
 // One tile of one group: TC adjacent transforms (tile index tt) of the
 // transform whose input / output start at element offsets ib / ob.
+// Factored pass-1 twiddles for the 2-pass group sub-FFTs of NS >= 2^11: the
+// last pass has k == 1, so thread t's butterfly m = t is the same for every
+// tile and its 63 twiddles w^{A m} are products Q[a] P[b] of 14 base values
+// (TwPQ, the 2-pass K2 scheme) held in registers instead of table loads per
+// tile.  Every kernel of a given NS (plain, TMA, plane) uses the same form,
+// so their results stay bitwise equal.  Measured on B200 (1 GiB batches):
+// 2^21 / 2^22 0.338 / 0.302 -> 0.364 / 0.360 split, 0.363 / 0.329 -> 0.385 /
+// 0.396 interleaved; for NS <= 1024 (16 / 32-point pass 1) it was slower
+// (2^17 0.450 / 0.471 -> 0.433 / 0.448, 2^23 three-pass 1.13 -> 1.21 ms).
+#ifndef FFTGEN_GROUP_PQ
+#define FFTGEN_GROUP_PQ 1
+#endif
+#ifndef FFTGEN_GROUP_PQ_MIN
+#define FFTGEN_GROUP_PQ_MIN 2048
+#endif
+template <class G> constexpr bool group_pq() {
+  return FFTGEN_GROUP_PQ && G::P == 2 && G::S(G::P - 1) >= FFTGEN_GROUP_PQ_MIN;
+}
+template <class G, bool ON = group_pq<G>()> struct GroupTw;
+template <class G> struct GroupTw<G, true> {
+  TwPQ<G> pq;
+  FFTGEN_FI void load(const float2 *__restrict__ tw, int m) { pq.load(tw, m); }
+};
+template <class G> struct GroupTw<G, false> {
+  FFTGEN_FI void load(const float2 *__restrict__, int) {}
+};
+
 // Passes 1 .. P-1 of a group sub-FFT whose pass-0 results sit in the padded
 // exchange (this column at Xf); lanes run over the tile's columns, thread t
 // owns the pass-p butterflies t + j T.
@@ -95,6 +122,15 @@ FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ t
   }
 }
 
+template <class G, int NS, int DIR, int BARID, int THREADS>
+FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ tw, float2 *v, const GroupTw<G> &gt) {
+  if constexpr (group_pq<G>()) {
+    smem_read_pass1_pq<G, NS, DIR>(Xf, t, gt.pq, v);
+    return;
+  }
+  group_passes_rest<G, NS, DIR, BARID, THREADS>(Xf, t, tw, v);
+}
+
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG = GroupGeom<NS>, int BARID = 0>
 FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt, float2 *smem) {
   using G = typename GG::G;
@@ -104,6 +140,8 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
   constexpr int R1 = G::R(G::P - 1), COLS1 = G::COLS(G::P - 1);  // the last pass
   const int tid = threadIdx.x;
+  GroupTw<G> gtw;  // pass-1 twiddle bases of butterfly m = tid / TC (issued early)
+  gtw.load(a.tw_local, tid / TC);
   int64_t m0, c0;
   if (ROWS) {
     m0 = tt * TC;
@@ -151,7 +189,7 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
     const int f = tid % TC;
     const int t = tid / TC;  // pass-1 butterfly m1 = t (k == 1, J == 1)
     // local pass twiddles w^{A t}: lanes share t -> L1 broadcast loads
-    group_passes_rest<G, NS, DIR, BARID, GG::THREADS>(smem + f * REG, t, a.tw_local, v);
+    group_passes_rest<G, NS, DIR, BARID, GG::THREADS>(smem + f * REG, t, a.tw_local, v, gtw);
 #pragma unroll
     for (int B = 0; B < R1; ++B) {
       const int64_t e = B * COLS1 + t;  // local output index

@@ -72,64 +72,6 @@ FFTGEN_FI void group_tma_issue(const GroupTmaArgs &ta, char *stage, uint64_t *ba
   }
 }
 
-// One tile whose raw input already sits in `stage` (columns [A][f], rows
-// [f][A]; split planes re then im): pass 0 with the group twiddle, padded
-// exchange in the same stage, pass 1, stores to a.out* at element offset ob.
-// The caller synchronises before the stage is refilled.
-template <int NS, int LIN, int LOUT, int DIR, bool ROWS, class GG>
-FFTGEN_FI void tile_from_stage(const GroupArgs &a, char *stage, int64_t ob, int64_t m0, int64_t c0) {
-  using G = typename GG::G;
-  constexpr int TC = GG::TC, REG = GG::REG, T = G::T;
-  constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
-  constexpr int R1 = G::R(G::P - 1), COLS1 = G::COLS(G::P - 1);  // the last pass
-  const int tid = threadIdx.x;
-  float2 *X = reinterpret_cast<float2 *>(stage);
-  float2 v[G::RMAX];
-  const int f0 = ROWS ? tid / T : tid % TC;
-  const int t0 = ROWS ? tid % T : tid / TC;
-  {
-    const int64_t m = ROWS ? m0 + f0 : m0;
-    const bool tw = a.cols > 1;
-    const float2 *qm = a.tw_q + m;
-#pragma unroll
-    for (int j = 0; j < J0; ++j) {
-      const int c = t0 + j * T;
-#pragma unroll
-      for (int A0 = 0; A0 < R0; ++A0) {
-        const int A = A0 * K0 + c;
-        const int e = ROWS ? f0 * NS + A : A * TC + f0;
-        if constexpr (LIN == LAYOUT_SPLIT) {
-          const float *sp = reinterpret_cast<const float *>(stage);
-          v[j * R0 + A0] = make_float2(sp[e], sp[NS * TC + e]);
-        } else {
-          v[j * R0 + A0] = X[e];
-        }
-      }
-      if (tw) {
-        const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
-#pragma unroll
-        for (int A0 = 0; A0 < R0; ++A0) {
-          float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
-        }
-      }
-      reg_fft<R0, DIR>(v + j * R0);
-    }
-  }
-  __syncthreads();  // raw tile consumed: the stage becomes the padded exchange
-  smem_write<G, NS, 0>(X + f0 * REG, t0, v);
-  __syncthreads();
-  const int f = tid % TC;
-  const int t = tid / TC;
-  group_passes_rest<G, NS, DIR, 0, GG::THREADS>(X + f * REG, t, a.tw_local, v);
-#pragma unroll
-  for (int B = 0; B < R1; ++B) {
-    const int64_t e = B * COLS1 + t;
-    const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
-    SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
-  }
-}
-
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
 __global__ void __launch_bounds__(GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::MIN_BLOCKS)
 fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
@@ -156,6 +98,8 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     for (int s = 0; s < NST; ++s)
       if (blockIdx.x + s * stride < total)
         group_tma_issue<NS, LIN, ROWS>(ta, smem + s * TG::STAGE, &bars[s], blockIdx.x + s * stride);
+  GroupTw<G> gtw;  // pass-1 twiddle bases of butterfly m = tid / TC, for every tile
+  gtw.load(a.tw_local, tid / TC);
 
   int it = 0;
   for (int64_t item = blockIdx.x; item < total; item += stride, ++it) {
@@ -214,7 +158,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     // ---- pass 1: exchange -> registers (lanes over f), codelet, HBM store ----
     const int f = tid % TC;
     const int t = tid / TC;
-    group_passes_rest<G, NS, DIR, 0, TG::THREADS>(X + f * REG, t, a.tw_local, v);
+    group_passes_rest<G, NS, DIR, 0, TG::THREADS>(X + f * REG, t, a.tw_local, v, gtw);
     __syncthreads();  // stage free: fetch the tile two items ahead
     if (tid == 0 && item + NST * stride < total) {
       fence_proxy_async();
@@ -243,6 +187,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
 #ifndef FFTGEN_GROUP_PLANE
 #define FFTGEN_GROUP_PLANE 1
 #endif
+
 template <int NS> struct GroupPlaneGeom {
   using GG = GroupGeom<NS>;
   using PL = typename GG::PL;
@@ -281,6 +226,8 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x < total) group_tma_issue<NS, LIN, ROWS>(ta, stage, bar, blockIdx.x);
+  GroupTw<G> gtw;  // pass-1 twiddle bases (fft_group.cuh, FFTGEN_GROUP_PQ)
+  gtw.load(a.tw_local, tid / TC);
   int it = 0;
   for (int64_t item = blockIdx.x; item < total; item += stride, ++it) {
     const int64_t b = item / a.tiles_per_outer, tt = item - b * a.tiles_per_outer;
@@ -341,7 +288,13 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
     plane_write<G, NS, 0, 1>(P + f0 * REGP, t0, v);
     __syncthreads();
     plane_read<G, NS, 1, 1>(P + f * REGP, t, v);
-    pass_compute<G, 1, DIR>(t, a.tw_local, v);
+    if constexpr (group_pq<G>()) {
+#pragma unroll
+      for (int A = 1; A < R1; ++A) v[A] = gtw.pq.template apply<DIR>(v[A], A);
+      reg_fft<R1, DIR>(v);
+    } else {
+      pass_compute<G, 1, DIR>(t, a.tw_local, v);
+    }
     const int64_t ob = b * a.odist;
 #pragma unroll
     for (int B = 0; B < R1; ++B) {

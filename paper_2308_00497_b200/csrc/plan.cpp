@@ -157,10 +157,10 @@ std::string formula_text(int64_t n, int algorithm, int64_t radix) {
   return out;
 }
 
-std::string program_text(int64_t n, int split_mode, int pass_radix) {
+std::string program_text(int64_t n, int split_mode, int pass_radix, int layout) {
   // the sm_100a execution plan as loop nests: one Stockham stage of radix R
   // per register pass (K2) or per four-step group launch (K3)
-  const ExecPlan p = build_exec_plan(n, split_mode, pass_radix);
+  const ExecPlan p = build_exec_plan(n, split_mode, pass_radix, layout);
   std::ostringstream out;
   if (p.strategy == STRAT_IDENTITY) {
     out << "copy: y[0] = x[0]\n";
@@ -234,7 +234,7 @@ void check_schedule(int vec, int64_t vector_width, int tile_kind, int64_t tile_v
   }
 }
 
-ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix) {
+ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix, int layout) {
   if (!is_pow2(n)) throw PlanError("size must be a power of two, got " + std::to_string(n));
   ExecPlan p;
   p.n = n;
@@ -267,7 +267,7 @@ ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix) {
     throw PlanError("size 2^" + std::to_string(p.log2n) + " exceeds the single-GPU limit 2^30");
   // K3 four-step: groups of consecutive Stockham stages, each one kernel
   p.strategy = STRAT_FOURSTEP;
-  const std::vector<int> split = group_split(p.log2n, split_mode);
+  const std::vector<int> split = group_split(p.log2n, split_mode, layout);
   int64_t s = 1;
   std::vector<int> seen_local;
   for (size_t g = 0; g < split.size(); ++g) {
@@ -307,7 +307,7 @@ ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix) {
   return p;
 }
 
-std::vector<int> group_split(int log2n, int mode) {
+std::vector<int> group_split(int log2n, int mode, int layout) {
   // 2 groups up to 2^22 (NS <= 2^11), 3 groups up to 2^28, 4 groups up to
   // 2^30; sizes as even as possible.  mode SPLIT_GROUPS_1024: NS <= 2^10 (2
   // groups up to 2^20); SPLIT_TWO_PASS: 2 groups up to 2^24 (NS <= 2^12, 32 N
@@ -322,7 +322,11 @@ std::vector<int> group_split(int log2n, int mode) {
   // 2^28 as 9+9+10 3.43 ms vs 7+7+7+7 3.65 ms; 2^30 as 10+10+10 19.3 ms vs
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
   // 64-byte segments).
-  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : 22);
+  // (+ factored pass-1 twiddles for NS >= 2^11: interleaved 2^23 11+12 0.94
+  // vs 1.07 ms per GiB three-pass; split 2^23 1.28 vs 1.13 -- its NS = 4096
+  // rows store 16-byte plane segments -- and 2^24 1.48 / 1.06 vs 1.14 / 1.07
+  // keep three passes)
+  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : (layout == 0 ? 23 : 22));
   const int g = log2n <= two ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs

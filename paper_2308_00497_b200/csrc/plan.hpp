@@ -90,14 +90,15 @@ struct ExecPlan {
 // The group split of log2 N used by the four-step path (2..4 groups of
 // 2^7..2^12 points).
 enum SplitMode { SPLIT_DEFAULT = 0, SPLIT_GROUPS_1024 = 1, SPLIT_TWO_PASS = 2 };
-std::vector<int> group_split(int log2n, int mode = SPLIT_DEFAULT);
+// layout: 0 interleaved, 1 split (the default split depends on it at 2^23)
+std::vector<int> group_split(int log2n, int mode = SPLIT_DEFAULT, int layout = 0);
 // whether a group runs the persistent TMA-tile kernel by default (measured)
 bool group_prefers_tma(int log2ns, bool first, bool rows);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
-ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0);
+ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0, int layout = 0);
 // the sm_100a pass / group program as loop nests (the --emit loops text)
-std::string program_text(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0);
+std::string program_text(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0, int layout = 0);
 
 // K2 pass structure of an N-point block kernel (defined in kernels_common.cu
 // from the compile-time BlockPlan), and its [A][m] twiddle table in floats.
