@@ -323,10 +323,10 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
   // 7+7+8+8 14.3 ms (1024-point columns at a 2^20 stride leave DRAM only
   // 64-byte segments).
   // (+ factored pass-1 twiddles for NS >= 2^11: interleaved 2^23 11+12 0.94
-  // vs 1.07 ms per GiB three-pass; split 2^23 1.28 vs 1.13 -- its NS = 4096
-  // rows store 16-byte plane segments -- and 2^24 1.48 / 1.06 vs 1.14 / 1.07
-  // keep three passes)
-  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : (layout == 0 ? 23 : 22));
+  // vs 1.07 ms per GiB three-pass, 2^24 12+12 1.06 vs 1.06 (batch 8) and
+  // 0.146 vs 0.149 ms (batch 1); split 2^23 / 2^24 1.28 / 1.48 vs 1.13 /
+  // 1.14 -- the NS = 4096 tiles move 16-byte plane segments -- keep three)
+  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : (layout == 0 ? 24 : 22));
   const int g = log2n <= two ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs

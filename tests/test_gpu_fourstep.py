@@ -100,6 +100,9 @@ def test_fourstep_plan_shape(fg):
     assert p.launches() == 3
     assert p.scratch_bytes() == 2 * (1 << 24) * 8
     assert "transposed store" in p.describe()
+    # interleaved 2^23 / 2^24 run two passes by default (NS = 2^11 / 2^12 plane kernels)
+    p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 24, layout="interleaved", batch=1))
+    assert [d[0] for d in p.passes()] == [4096, 4096] and "fft_group_plane_kernel<4096>" in p.describe()
     # two-pass plans: NS = 2^11 / 2^12 groups, one scratch buffer
     p = fg.compile_pipeline(fg.PipelineConfig(n=1 << 24, layout="split", batch=1, tuning=16))
     assert [d[0] for d in p.passes()] == [4096, 4096] and p.launches() == 2
