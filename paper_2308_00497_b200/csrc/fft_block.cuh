@@ -60,6 +60,9 @@ template <> struct GIO<LAYOUT_SPLIT> {
 };
 
 // ---- pass building blocks (G = BlockGeom<N, TP>) -----------------------
+#ifndef FFTGEN_K2_TWCACHE
+#define FFTGEN_K2_TWCACHE 1
+#endif
 
 // pass 0 from an element accessor: v[j*R + A] = x[A*k + c], c = t + j*T
 template <class G, int DIR, class Load>
@@ -115,17 +118,17 @@ FFTGEN_FI void smem_read_pass(const float2 *sx, int t, const float2 *__restrict_
 // thread t always owns butterfly m = t and needs w_s^{A m} for A < R only.
 // With A = a*RLO + b:  w^{A m} = Q[a] * P[b],  P[b] = w^{b m},  Q[a] = w^{RLO a m},
 // loaded once per thread from the [A][m] table (RLO-1 + RHI-1 values).
-template <class G> struct TwPQ {
-  static constexpr int R = G::R(1);
+template <class G, int PASS = 1> struct TwPQ {
+  static constexpr int R = G::R(PASS);
   static constexpr int RLO = R >= 16 ? 8 : (R >= 4 ? 4 : R);
   static constexpr int RHI = R / RLO;
   float2 p[RLO], q[RHI];
   FFTGEN_FI void load(const float2 *__restrict__ tw, int m) {
-    const float2 *base = tw + G::TW_OFF(1) + m;
+    const float2 *base = tw + G::TW_OFF(PASS) + m;
 #pragma unroll
-    for (int b = 1; b < RLO; ++b) p[b] = __ldg(base + b * G::COLS(1));
+    for (int b = 1; b < RLO; ++b) p[b] = __ldg(base + b * G::COLS(PASS));
 #pragma unroll
-    for (int a = 1; a < RHI; ++a) q[a] = __ldg(base + a * RLO * G::COLS(1));
+    for (int a = 1; a < RHI; ++a) q[a] = __ldg(base + a * RLO * G::COLS(PASS));
   }
   template <int DIR> FFTGEN_FI float2 apply(float2 x, int A) const {
     const int a = A / RLO, b = A % RLO;
@@ -134,6 +137,56 @@ template <class G> struct TwPQ {
     return x;
   }
 };
+
+// Three-pass plans in a persistent kernel: every pass-1 / pass-2 butterfly a
+// thread owns (m = (t + j T) / k) is the same for every transform, so their
+// twiddles are kept as factored bases in registers for the whole kernel
+// (unfactored last-pass tables only; the factored-table pass of 2^14 keeps
+// its own scheme).
+template <class G> struct TwCache3 {
+  static constexpr int J1 = G::RMAX / G::R(1), J2 = G::RMAX / G::R(2);
+  TwPQ<G, 1> a[J1];
+  TwPQ<G, 2> b[J2];
+  FFTGEN_FI void load(const float2 *__restrict__ tw, int t) {
+#pragma unroll
+    for (int j = 0; j < J1; ++j) a[j].load(tw, (t + j * G::T) / G::K(1));
+#pragma unroll
+    for (int j = 0; j < J2; ++j) b[j].load(tw, (t + j * G::T) / G::K(2));
+  }
+};
+
+template <class G, int N, int p, int DIR, class W>
+FFTGEN_FI void smem_read_pass_cached(const float2 *sx, int t, const W *w, float2 *v) {
+  constexpr int R = G::R(p), k = G::K(p), J = G::RMAX / R;
+  constexpr Pad pd = BoundaryPad<N, p - 1, 8, typename G::PL>::value;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int u = t + j * G::T, m = u / k, c = u % k;
+    v[j * R] = sx[padded((m * R) * k + c, pd)];
+#pragma unroll
+    for (int A = 1; A < R; ++A) v[j * R + A] = w[j].template apply<DIR>(sx[padded((m * R + A) * k + c, pd)], A);
+    reg_fft<R, DIR>(v + j * R);
+  }
+}
+
+template <class G> constexpr bool use_twcache3() {
+#if FFTGEN_K2_TWCACHE
+  return G::P == 3 && !G::TW_FACTORED(2);
+#else
+  return false;
+#endif
+}
+
+template <class G, int N, int DIR>
+FFTGEN_FI void middle_passes_cached(float2 *sx, int t, const TwCache3<G> &tc, float2 *v) {
+  smem_write<G, N, 0>(sx, t, v);
+  __syncthreads();
+  smem_read_pass_cached<G, N, 1, DIR>(sx, t, tc.a, v);
+  __syncthreads();
+  smem_write<G, N, 1>(sx, t, v);
+  __syncthreads();
+  smem_read_pass_cached<G, N, 2, DIR>(sx, t, tc.b, v);
+}
 
 template <class G, int N, int DIR>
 FFTGEN_FI void smem_read_pass1_pq(const float2 *sx, int t, const TwPQ<G> &w, float2 *v) {
@@ -201,6 +254,10 @@ __global__ void __launch_bounds__(BlockGeom<N, 0, PL>::THREADS) fft_block_kernel
     smem_write<G, N, 0>(sx, t, v);
     __syncthreads();
     smem_read_pass1_pq<G, N, DIR>(sx, t, pq, v);
+  } else if constexpr (use_twcache3<G>()) {  // same arithmetic as the TMA kernel
+    TwCache3<G> tc3;
+    tc3.load(args.tw, t);
+    middle_passes_cached<G, N, DIR>(sx, t, tc3, v);
   } else {
     middle_passes<G, N, DIR>(sx, t, args.tw, v);
   }
@@ -373,9 +430,13 @@ __global__ void __launch_bounds__(TmaGeom<N, PL>::THREADS) fft_block_tma_kernel(
       if (g < groups) tma_issue<N, LAYOUT, PL>(args, smem + s * TG::STAGE_BYTES, &bars[s], g);
     }
   }
-  // 2-pass plans: this thread's pass-1 twiddle bases live in registers
+  // 2-pass plans: this thread's pass-1 twiddle bases live in registers;
+  // 3-pass plans (2^13): those of passes 1 and 2 (TwCache3)
   TwPQ<G> pq;
   if constexpr (G::P == 2) pq.load(args.tw, t);
+  constexpr bool kCache3 = use_twcache3<G>();
+  TwCache3<G> tc3;
+  if constexpr (kCache3) tc3.load(args.tw, t);
 
   int it = 0;
   for (int64_t g = blockIdx.x; g < groups; g += stride, ++it) {
@@ -410,6 +471,8 @@ __global__ void __launch_bounds__(TmaGeom<N, PL>::THREADS) fft_block_tma_kernel(
       smem_write<G, N, 0>(sx, t, v);
       __syncthreads();
       smem_read_pass1_pq<G, N, DIR>(sx, t, pq, v);
+    } else if constexpr (kCache3) {
+      middle_passes_cached<G, N, DIR>(sx, t, tc3, v);
     } else {
       middle_passes<G, N, DIR>(sx, t, args.tw, v);
     }
