@@ -63,6 +63,11 @@ template <> struct GIO<LAYOUT_SPLIT> {
 #ifndef FFTGEN_K2_TWCACHE
 #define FFTGEN_K2_TWCACHE 1
 #endif
+// also for a factored last pass (2^14: split 0.722 / interleaved 0.714 vs
+// 0.667 / 0.695 with one hi * lo product per element)
+#ifndef FFTGEN_K2_TWCACHE_FACTORED
+#define FFTGEN_K2_TWCACHE_FACTORED 1
+#endif
 
 // pass 0 from an element accessor: v[j*R + A] = x[A*k + c], c = t + j*T
 template <class G, int DIR, class Load>
@@ -123,12 +128,12 @@ template <class G, int PASS = 1> struct TwPQ {
   static constexpr int RLO = R >= 16 ? 8 : (R >= 4 ? 4 : R);
   static constexpr int RHI = R / RLO;
   float2 p[RLO], q[RHI];
+  // (a factored pass table, TW_FACTORED: each base is itself hi * lo)
   FFTGEN_FI void load(const float2 *__restrict__ tw, int m) {
-    const float2 *base = tw + G::TW_OFF(PASS) + m;
 #pragma unroll
-    for (int b = 1; b < RLO; ++b) p[b] = __ldg(base + b * G::COLS(PASS));
+    for (int b = 1; b < RLO; ++b) p[b] = pass_tw<G, PASS>(tw, b, m);
 #pragma unroll
-    for (int a = 1; a < RHI; ++a) q[a] = __ldg(base + a * RLO * G::COLS(PASS));
+    for (int a = 1; a < RHI; ++a) q[a] = pass_tw<G, PASS>(tw, a * RLO, m);
   }
   template <int DIR> FFTGEN_FI float2 apply(float2 x, int A) const {
     const int a = A / RLO, b = A % RLO;
@@ -171,7 +176,7 @@ FFTGEN_FI void smem_read_pass_cached(const float2 *sx, int t, const W *w, float2
 
 template <class G> constexpr bool use_twcache3() {
 #if FFTGEN_K2_TWCACHE
-  return G::P == 3 && !G::TW_FACTORED(2);
+  return G::P == 3 && (FFTGEN_K2_TWCACHE_FACTORED || !G::TW_FACTORED(2));
 #else
   return false;
 #endif
@@ -551,6 +556,28 @@ FFTGEN_FI void pass_compute(int t, const float2 *__restrict__ tw, float2 *v) {
   }
 }
 
+template <class G, int p, int DIR, class W>
+FFTGEN_FI void pass_compute_cached(int t, const W *w, float2 *v) {
+  constexpr int R = G::R(p), J = G::RMAX / R;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+#pragma unroll
+    for (int A = 1; A < R; ++A) v[j * R + A] = w[j].template apply<DIR>(v[j * R + A], A);
+    reg_fft<R, DIR>(v + j * R);
+  }
+}
+
+template <class G, int N, int p>
+FFTGEN_FI void plane_exchange(float *X, int t, float2 *v) {
+  plane_write<G, N, p - 1, 0>(X, t, v);
+  __syncthreads();
+  plane_read<G, N, p, 0>(X, t, v);
+  __syncthreads();
+  plane_write<G, N, p - 1, 1>(X, t, v);
+  __syncthreads();
+  plane_read<G, N, p, 1>(X, t, v);
+}
+
 template <class G, int N, int p, int DIR>
 FFTGEN_FI void plane_exchange_pass(float *X, int t, const float2 *__restrict__ tw, float2 *v) {
   plane_write<G, N, p - 1, 0>(X, t, v);
@@ -600,6 +627,7 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS)
   float *X = reinterpret_cast<float *>(stage + TG::RAW);
   uint64_t *bar = reinterpret_cast<uint64_t *>(stage + TG::RAW + TG::PLANE);
   const int t = threadIdx.x;
+  constexpr bool kCache = use_twcache3<G>();
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
   auto issue = [&](int64_t b) {
     mbar_expect_tx(bar, 8 * N);
@@ -642,15 +670,31 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS)
       static_assert(BoundaryPad<N, 0, 8, typename G::PL>::region * 8 <= TG::RAW + TG::PLANE, "exchange 1 fits");
       float2 *sx = reinterpret_cast<float2 *>(stage);
       smem_write<G, N, 0>(sx, t, v);
-      __syncthreads();
-      smem_read_pass<G, N, 1, DIR>(sx, t, args.tw, v);
+      if constexpr (kCache) {
+        TwCache3<G> tc;
+#pragma unroll
+        for (int j = 0; j < TwCache3<G>::J1; ++j) tc.a[j].load(args.tw, (t + j * G::T) / G::K(1));
+        __syncthreads();
+        smem_read_pass_cached<G, N, 1, DIR>(sx, t, tc.a, v);
+      } else {
+        __syncthreads();
+        smem_read_pass<G, N, 1, DIR>(sx, t, args.tw, v);
+      }
       __syncthreads();  // stage free: fetch the next transform behind pass 2
       if (t == 0 && b + gridDim.x < args.batch) {
         fence_proxy_async();
         issue(b + gridDim.x);
       }
     }
-    plane_exchange_pass<G, N, 2, DIR>(X, t, args.tw, v);
+    if constexpr (kCache) {
+      TwCache3<G> tc;
+#pragma unroll
+      for (int j = 0; j < TwCache3<G>::J2; ++j) tc.b[j].load(args.tw, (t + j * G::T) / G::K(2));
+      plane_exchange<G, N, 2>(X, t, v);
+      pass_compute_cached<G, 2, DIR>(t, tc.b, v);
+    } else {
+      plane_exchange_pass<G, N, 2, DIR>(X, t, args.tw, v);
+    }
     if constexpr (STORE_TMA) {
       __syncthreads();  // pass-2 reads of X done
       plane_write_out<G, N, LAYOUT, 0>(X, t, v);

@@ -250,8 +250,12 @@ ExecPlan build_exec_plan(int64_t n, int split_mode, int pass_radix, int layout) 
     // measured default: 2^7 .. 2^9 as radix-8 three-pass plans on the direct
     // kernel (1 GiB batches, split / interleaved fraction of HBM: 2^7 0.90 /
     // 1.05 vs 0.85 / 1.01, 2^8 0.99 / 1.05 vs 0.92 / 1.00 (TMA), 2^9 0.98 /
-    // 1.04 vs 0.93 / 1.00 (TMA)); pass_radix 64 selects the two-pass plans
-    const int cap = pass_radix == 0 ? (p.log2n >= 7 && p.log2n <= 9 ? 8 : 0) : (pass_radix == 64 ? 0 : pass_radix);
+    // 1.04 vs 0.93 / 1.00 (TMA)); interleaved 2^10 / 2^11 as radix-16
+    // three-pass plans on the direct kernel (1.05 / 1.01 vs 0.98 / 0.98 TMA;
+    // split stays on TMA: 0.96 / 0.95 vs 0.98 / 0.98); pass_radix 64 selects
+    // the two-pass plans
+    const int dcap = p.log2n >= 7 && p.log2n <= 9 ? 8 : ((p.log2n == 10 || p.log2n == 11) && layout == 0 ? 16 : 0);
+    const int cap = pass_radix == 0 ? dcap : (pass_radix == 64 ? 0 : pass_radix);
     p.block_cap = block_cap_distinct(p.log2n, cap) ? cap : 0;
     const int np = block_num_passes(p.log2n, p.block_cap);
     for (int q = 0; q < np; ++q) {

@@ -6,7 +6,7 @@
 //   plan_tool formula N ALG RADIX   print_formula text of the planner
 //   plan_tool loops N               the sm_100a pass / group program
 //   plan_tool radices N RADIX       Stockham radices, application order
-//   plan_tool passes N [PASS_RADIX] sm_100a passes: R cols k s
+//   plan_tool passes N [PASS_RADIX [LAYOUT]] sm_100a passes: R cols k s
 //   plan_tool twiddles N            K2 pass twiddle table (hex floats)
 // Exit codes: 0 ok, 1 PlanError, 2 DimensionError, 4 FuseError.
 #include <cstdio>
@@ -49,7 +49,7 @@ int main(int argc, char **argv) {
       for (int64_t r : stockham_radices(n, std::atoll(argv[3]))) std::printf("%lld ", (long long)r);
       std::printf("\n");
     } else if (cmd == "passes") {
-      const ExecPlan p = build_exec_plan(n, SPLIT_DEFAULT, argc > 3 ? std::atoi(argv[3]) : 0);
+      const ExecPlan p = build_exec_plan(n, SPLIT_DEFAULT, argc > 3 ? std::atoi(argv[3]) : 0, argc > 4 ? std::atoi(argv[4]) : 0);
       for (const auto &d : p.passes)
         std::printf("%lld %lld %lld %lld\n", (long long)d.R, (long long)d.cols, (long long)d.k, (long long)d.s);
     } else if (cmd == "twiddles") {

@@ -280,7 +280,9 @@ def test_tma_and_direct_kernels_bitwise_equal(orc, n):
     """The persistent TMA variants (bulk-store epilogue or register stores) and
     the direct variant run the same passes: bitwise equal results."""
     x = seeded_batch(orc, n, 37)
-    hint = 64 if n <= 512 else 0  # 2^8 / 2^9 default to radix-8 direct plans; 64 keeps the TMA ones
+    # 2^8 / 2^9 (radix 8) and interleaved 2^10 / 2^11 (radix 16) default to
+    # three-pass direct plans; 64 keeps the two-pass TMA ones
+    hint = 64 if n <= 2048 else 0
     for layout in ("interleaved", "split"):
         a = run(n, layout, -1, x, pass_radix=hint)
         b = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA, pass_radix=hint)

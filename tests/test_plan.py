@@ -155,13 +155,16 @@ def test_pass_radix_hint_steers_block_passes(plan_tool):
     that radix in the reference's Stockham shape, remainder radix first
     (formula.cpp:182-195), where <= 3 passes suffice and the default differs;
     otherwise the default plan."""
-    def passes(n, hint=0):
-        rc, out, err = plan_tool("passes", n, hint)
+    def passes(n, hint=0, layout=0):
+        rc, out, err = plan_tool("passes", n, hint, layout)
         assert rc == 0, err
         return [int(ln.split()[0]) for ln in out.splitlines()]
     assert passes(4096) == [64, 64]
     # measured defaults: radix-8 three-pass plans at 2^7..2^9; 64 keeps the two-pass ones
     assert passes(256) == [4, 8, 8] and passes(512) == [8, 8, 8] and passes(128) == [2, 8, 8]
+    # interleaved 2^10 / 2^11: radix-16 three-pass (direct kernel); split keeps two passes
+    assert passes(1024) == [4, 16, 16] and passes(2048) == [8, 16, 16]
+    assert passes(1024, 0, 1) == [32, 32] and passes(2048, 0, 1) == [32, 64] and passes(2048, 64) == [32, 64]
     assert passes(256, 64) == [16, 16] and passes(512, 64) == [16, 32] and passes(128, 64) == [8, 16]
     assert passes(4096, 16) == [16, 16, 16] and passes(4096, 32) == [4, 32, 32]
     assert passes(2048, 16) == [8, 16, 16] and passes(2048, 32) == [2, 32, 32]
