@@ -65,6 +65,11 @@ template <> struct GIO<LAYOUT_SPLIT> {
 #endif
 // also for a factored last pass (2^14: split 0.722 / interleaved 0.714 vs
 // 0.667 / 0.695 with one hi * lo product per element)
+// 2^14 interleaved: pass-1 bases fetched before the stage wait (0.726 vs
+// 0.715; split 0.715 vs 0.724, so split fetches them after the pass-0 write)
+#ifndef FFTGEN_TMA1_EARLY_TW
+#define FFTGEN_TMA1_EARLY_TW 1
+#endif
 #ifndef FFTGEN_K2_TWCACHE_FACTORED
 #define FFTGEN_K2_TWCACHE_FACTORED 1
 #endif
@@ -628,6 +633,7 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS)
   uint64_t *bar = reinterpret_cast<uint64_t *>(stage + TG::RAW + TG::PLANE);
   const int t = threadIdx.x;
   constexpr bool kCache = use_twcache3<G>();
+  constexpr bool kEarly = kCache && FFTGEN_TMA1_EARLY_TW && LAYOUT == LAYOUT_INTERLEAVED;
   constexpr uint32_t plane = LAYOUT == LAYOUT_SPLIT ? 4 * N : 8 * N;
   auto issue = [&](int64_t b) {
     mbar_expect_tx(bar, 8 * N);
@@ -654,6 +660,11 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS)
   if (t == 0 && blockIdx.x < args.batch) issue(blockIdx.x);
   int it = 0;
   for (int64_t b = blockIdx.x; b < args.batch; b += gridDim.x, ++it) {
+    TwCache3<G> tc1;
+    if constexpr (kEarly) {
+#pragma unroll
+      for (int j = 0; j < TwCache3<G>::J1; ++j) tc1.a[j].load(args.tw, (t + j * G::T) / G::K(1));
+    }
     mbar_wait(bar, it & 1);
     float2 v[G::RMAX];
     if constexpr (LAYOUT == LAYOUT_SPLIT) {
@@ -671,9 +682,11 @@ __global__ void __launch_bounds__(Tma1Geom<N>::THREADS, Tma1Geom<N>::MIN_BLOCKS)
       float2 *sx = reinterpret_cast<float2 *>(stage);
       smem_write<G, N, 0>(sx, t, v);
       if constexpr (kCache) {
-        TwCache3<G> tc;
+        TwCache3<G> &tc = tc1;
+        if constexpr (!kEarly) {
 #pragma unroll
-        for (int j = 0; j < TwCache3<G>::J1; ++j) tc.a[j].load(args.tw, (t + j * G::T) / G::K(1));
+          for (int j = 0; j < TwCache3<G>::J1; ++j) tc.a[j].load(args.tw, (t + j * G::T) / G::K(1));
+        }
         __syncthreads();
         smem_read_pass_cached<G, N, 1, DIR>(sx, t, tc.a, v);
       } else {
