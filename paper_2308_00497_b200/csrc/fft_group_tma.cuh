@@ -27,17 +27,34 @@ namespace fftgen_b200 {
 #define FFTGEN_GROUP_TMA_STAGES 2
 #endif
 constexpr int kGroupTmaStages = FFTGEN_GROUP_TMA_STAGES;
+// Results staged in a separate output buffer ([e][f], the tile of the store
+// box) and written by TMA tensor stores instead of per-lane STGs of
+// TC-element segments, where measured faster (B200, 1 GiB batches,
+// `scripts/gpu_ab_st.sh`, `gpu_ab_rst.sh`): the NS = 512 rows group (through
+// this kernel instead of the plain one: 2^18 / 2^19 split 0.409 / 0.404 ->
+// 0.426 / 0.424, interleaved 0.419 / 0.421 -> 0.423 / 0.427) and the NS = 1024
+// column group of split input (2^20 / 2^21 split 0.383 / 0.363 -> 0.404 /
+// 0.386).  Slower elsewhere: NS = 512 columns (2^17 0.448 -> 0.427), NS = 1024
+// rows (2^20 split 0.383 -> 0.378), interleaved NS = 1024 columns (neutral).
+#ifndef FFTGEN_GROUP_TMA_STORE
+#define FFTGEN_GROUP_TMA_STORE 1
+#endif
+constexpr bool group_tma_store_rt(int ns, bool rows, int lin) {
+  return FFTGEN_GROUP_TMA_STORE && (rows ? ns == 512 : (ns == 1024 && lin == LAYOUT_SPLIT));
+}
+template <int NS, bool ROWS, int LIN> constexpr bool group_tma_store() { return group_tma_store_rt(NS, ROWS, LIN); }
 
 // STAGES = 2: one CTA per SM, the tile two items ahead is in flight;
 // STAGES = 1: two CTAs per SM, each refilling its stage after pass 1.
-template <int NS, int STAGES_ = kGroupTmaStages> struct GroupTmaGeom {
+template <int NS, int STAGES_ = kGroupTmaStages, bool STORE = false> struct GroupTmaGeom {
   using GG = GroupGeom<NS>;
   static constexpr int TC = GG::TC, REG = GG::REG, THREADS = GG::THREADS;
   static constexpr int RAW = TC * NS * 8;  // raw tile bytes
   static constexpr int STAGE = ((TC * REG * 8 > RAW ? TC * REG * 8 : RAW) + 127) / 128 * 128;
+  static constexpr int OUT = STORE ? RAW : 0;  // output staging buffer
   // 128 KB tiles (NS >= 2048) fit one stage: the refill overlaps the stores
-  static constexpr int STAGES = STAGES_ * STAGE + 64 > 227 * 1024 ? 1 : STAGES_;
-  static constexpr int BYTES = STAGES * STAGE + 64;
+  static constexpr int STAGES = STAGES_ * STAGE + OUT + 64 > 227 * 1024 ? 1 : STAGES_;
+  static constexpr int BYTES = STAGES * STAGE + OUT + 64;
   static constexpr int MIN_BLOCKS = (228 * 1024) / (BYTES + 1024) > 0 ? (228 * 1024) / (BYTES + 1024) : 1;
 };
 
@@ -47,6 +64,32 @@ FFTGEN_FI void tma_load_4d(void *dst, const void *tmap, int c0, int c1, int c2, 
       "%5}], [%6];" ::"r"(smem_u32(dst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
+}
+
+FFTGEN_FI void tma_store_4d(const void *tmap, const void *src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(tmap),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
+// store the staged results of a tile ([e][f] boxes of <= 256 rows e; split:
+// the re plane, then the im plane); maps from encode_out_maps
+template <int NS, int LOUT, bool ROWS>
+FFTGEN_FI void group_tma_store(const GroupTmaArgs &ta, const char *out, int64_t b, int64_t m0, int64_t c0) {
+  constexpr int TC = GroupTmaGeom<NS>::TC;
+  constexpr int CH = NS < 256 ? NS : 256;
+  constexpr int W = LOUT == LAYOUT_SPLIT ? 1 : 2;
+#pragma unroll
+  for (int q = 0; q < NS / CH; ++q) {
+    const char *src = out + q * CH * TC * W * 4;
+    if constexpr (ROWS) {  // {cols*W floats, NS, batch, 1}
+      tma_store_4d(ta.omap[0], src, (int)(m0 * W), q * CH, (int)b, 0);
+      if constexpr (LOUT == LAYOUT_SPLIT)
+        tma_store_4d(ta.omap[1], src + NS * TC * 4, (int)m0, q * CH, (int)b, 0);
+    } else {               // {k*2 floats, cols, NS, batch} (interleaved scratch)
+      tma_store_4d(ta.omap[0], src, (int)(c0 * 2), (int)m0, q * CH, (int)b);
+    }
+  }
 }
 
 // issue the raw tile of work item `item` into `stage`
@@ -73,9 +116,11 @@ FFTGEN_FI void group_tma_issue(const GroupTmaArgs &ta, char *stage, uint64_t *ba
 }
 
 template <int NS, int LIN, int LOUT, int DIR, bool ROWS>
-__global__ void __launch_bounds__(GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::MIN_BLOCKS)
+__global__ void __launch_bounds__(GroupTmaGeom<NS>::THREADS,
+                                  (GroupTmaGeom<NS, kGroupTmaStages, group_tma_store<NS, ROWS, LIN>()>::MIN_BLOCKS))
 fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
-  using TG = GroupTmaGeom<NS>;
+  constexpr bool ST = group_tma_store<NS, ROWS, LIN>();
+  using TG = GroupTmaGeom<NS, kGroupTmaStages, ST>;
   using G = typename TG::GG::G;
   constexpr int TC = TG::TC, REG = TG::REG, T = G::T;
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
@@ -84,7 +129,8 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
   extern __shared__ float4 smem_f4[];
   char *smem = reinterpret_cast<char *>(smem_f4);
   constexpr int NST = TG::STAGES;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NST * TG::STAGE);
+  char *obuf = smem + NST * TG::STAGE;  // output staging (FFTGEN_GROUP_TMA_STORE)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NST * TG::STAGE + TG::OUT);
   const int tid = threadIdx.x;
   const int64_t total = ta.items, stride = gridDim.x;
 
@@ -159,11 +205,34 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     const int f = tid % TC;
     const int t = tid / TC;
     group_passes_rest<G, NS, DIR, 0, TG::THREADS>(X + f * REG, t, a.tw_local, v, gtw);
+    if constexpr (ST)
+      if (tid == 0) bulk_wait_read0();  // the previous tile's store has read obuf
     __syncthreads();  // stage free: fetch the tile two items ahead
     if (tid == 0 && item + NST * stride < total) {
       fence_proxy_async();
       group_tma_issue<NS, LIN, ROWS>(ta, stage, &bars[s], item + NST * stride);
     }
+    if constexpr (ST) {
+    // [e][f] rows of the store box: lanes of a warp write 32 consecutive elements
+#pragma unroll
+    for (int B = 0; B < R1; ++B) {
+      const int e = B * COLS1 + t;
+      if constexpr (LOUT == LAYOUT_SPLIT) {
+        float *o = reinterpret_cast<float *>(obuf);
+        o[e * TC + f] = v[B].x;
+        o[NS * TC + e * TC + f] = v[B].y;
+      } else {
+        reinterpret_cast<float2 *>(obuf)[e * TC + f] = v[B];
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      group_tma_store<NS, LOUT, ROWS>(ta, obuf, b, m0, c0);
+      bulk_commit();
+    }
+    } else {
+    (void)obuf;
     const int64_t ob = b * a.odist;
 #pragma unroll
     for (int B = 0; B < R1; ++B) {
@@ -171,7 +240,10 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
       const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
       SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
     }
+    }
   }
+  if constexpr (ST)
+    if (tid == 0) bulk_wait0();
 }
 
 // ---- NS >= 2^11: one raw stage + an fp32 exchange plane --------------------

@@ -62,7 +62,8 @@ cudaError_t group_tma_launch_t(const GroupTmaArgs &ta, int grid, cudaStream_t s)
     fft_group_plane_kernel<NS, LIN, LOUT, DIR, ROWS>
         <<<grid, GroupPlaneGeom<NS>::THREADS, GroupPlaneGeom<NS>::BYTES, s>>>(ta);
   else
-    fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS><<<grid, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS>::BYTES, s>>>(ta);
+    fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS>
+        <<<grid, GroupTmaGeom<NS>::THREADS, GroupTmaGeom<NS, kGroupTmaStages, group_tma_store<NS, ROWS, LIN>()>::BYTES, s>>>(ta);
   return cudaGetLastError();
 }
 
@@ -80,7 +81,7 @@ template <int NS, int LIN, int LOUT, int DIR, bool ROWS> cudaError_t group_tma_p
                           GroupPlaneGeom<NS>::BYTES, bps);
   else
     return prepare_kernel(fft_group_tma_kernel<NS, LIN, LOUT, DIR, ROWS>, GroupTmaGeom<NS>::THREADS,
-                          GroupTmaGeom<NS>::BYTES, bps);
+                          GroupTmaGeom<NS, kGroupTmaStages, group_tma_store<NS, ROWS, LIN>()>::BYTES, bps);
 }
 
 template <int NS, int DIR>

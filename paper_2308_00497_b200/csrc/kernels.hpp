@@ -64,6 +64,7 @@ cudaError_t group_prepare(int log2ns);
 // of (transform, tile) work items.
 struct GroupTmaArgs {
   alignas(64) unsigned char tmap[2][128];
+  alignas(64) unsigned char omap[2][128];  // output maps (FFTGEN_GROUP_TMA_STORE)
   GroupArgs g;
   int64_t items;
 };

@@ -451,10 +451,54 @@ bool encode_tile_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, 
   return true;
 }
 
+// tensor maps of a's output for the staged tile stores of fft_group_tma_kernel
+// (FFTGEN_GROUP_TMA_STORE): rows (last group) {cols*w floats, NS, batch, 1},
+// columns (interleaved scratch) {k*2 floats, cols, NS, batch}
+bool encode_out_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, int64_t tc,
+                     unsigned char (*omap)[128]) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const int64_t ns = int64_t(1) << log2ns, ch = std::min<int64_t>(ns, 256);
+  const bool rows = shape == 2 || shape == 3;
+  const bool split_out = shape == 3;
+  const int64_t w = split_out ? 1 : 2;
+  void *planes[2] = {a.out0, split_out ? a.out1 : a.out0};
+  const int nplanes = split_out ? 2 : 1;
+  for (int i = 0; i < nplanes; ++i)
+    if ((uintptr_t)planes[i] % 16 != 0) return false;
+  if ((a.odist * w * 4) % 16 != 0) return false;
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+  if (rows) {
+    if ((a.cols * w * 4) % 16 != 0) return false;
+    dims[0] = a.cols * w; dims[1] = ns; dims[2] = batch; dims[3] = 1;
+    strides[0] = a.cols * w * 4; strides[1] = a.odist * w * 4; strides[2] = a.odist * w * 4 * batch;
+    box[0] = tc * w; box[1] = ch; box[2] = 1; box[3] = 1;
+  } else {
+    if ((a.k * 2 * 4) % 16 != 0) return false;
+    dims[0] = a.k * 2; dims[1] = a.cols; dims[2] = ns; dims[3] = batch;
+    strides[0] = a.k * 8; strides[1] = a.cols * a.k * 8; strides[2] = a.odist * 8;
+    box[0] = tc * 2; box[1] = 1; box[2] = ch; box[3] = 1;
+  }
+  for (int i = 0; i < nplanes; ++i) {
+    CUresult r = enc(reinterpret_cast<CUtensorMap *>(omap[i]), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, planes[i], dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+  }
+  return true;
+}
+
 bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
   int64_t threads, tc, smem, r0;
   group_geom(log2ns, &threads, &tc, &smem, &r0);
-  return encode_tile_maps(ta.g, log2ns, shape, batch, tc, ta.tmap);
+  if (!encode_tile_maps(ta.g, log2ns, shape, batch, tc, ta.tmap)) return false;
+  // the plane kernel (NS >= 2^11) stores from registers
+  const bool rows = shape == 2 || shape == 3;
+  const int lin = shape == 0 ? LAYOUT_INTERLEAVED : (shape == 1 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
+  if (group_tma_store_rt(1 << log2ns, rows, lin) && !group_plane(log2ns))
+    return encode_out_maps(ta.g, log2ns, shape, batch, tc, ta.omap);
+  return true;
 }
 
 }  // namespace fftgen_b200

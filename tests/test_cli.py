@@ -53,7 +53,10 @@ def test_emit_outputs_byte_stable_without_gpu():
                 "--interleaved-opt", "--emit", emit)
         a, b = run(*args), run(*args)
         assert a.returncode == 0 and a.stdout and a.stdout == b.stdout, emit
+    # 2^24: two 4096-point groups interleaved, three 256-point groups split (measured defaults)
     loops = run("compile", "--size", str(1 << 24), "--emit", "loops").stdout
+    assert loops.startswith("four-step: 2 group launches") and "HBM scratch -> HBM" in loops
+    loops = run("compile", "--size", str(1 << 24), "--layout", "split", "--emit", "loops").stdout
     assert loops.startswith("four-step: 3 group launches") and "HBM scratch -> HBM" in loops
     c = run("compile", "--size", "16", "--emit", "c")
     assert c.returncode == 1 and "LowerError" in c.stderr
