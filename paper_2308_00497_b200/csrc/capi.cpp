@@ -500,7 +500,7 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       for (size_t gi = 0; gi < p->ex.groups.size(); ++gi) {
         const GroupDesc &d = p->ex.groups[gi];
         const bool want = !(tune & FFTGEN_TUNE_NO_TMA) &&
-                          ((tune & FFTGEN_TUNE_GROUP_TMA_ALL) || group_prefers_tma(d.log2ns, gi == 0, d.rows));
+                          ((tune & FFTGEN_TUNE_GROUP_TMA_ALL) || group_prefers_tma(d.log2ns, gi == 0, d.rows, d.cols));
         int bps = 0;
         if (want && (e = group_tma_prepare(d.log2ns, &bps)) != cudaSuccess)
           return bail(FFTGEN_ERR_GPUMAP, std::string("group TMA kernel attributes: ") + cudaGetErrorString(e));

@@ -40,7 +40,7 @@ constexpr int kGroupTmaStages = FFTGEN_GROUP_TMA_STAGES;
 #define FFTGEN_GROUP_TMA_STORE 1
 #endif
 constexpr bool group_tma_store_rt(int ns, bool rows, int lin) {
-  return FFTGEN_GROUP_TMA_STORE && (rows ? ns == 512 : (ns == 1024 && lin == LAYOUT_SPLIT));
+  return FFTGEN_GROUP_TMA_STORE && (rows ? (ns == 512 || ns == 1024) : (ns == 1024 && lin == LAYOUT_SPLIT));
 }
 template <int NS, bool ROWS, int LIN> constexpr bool group_tma_store() { return group_tma_store_rt(NS, ROWS, LIN); }
 

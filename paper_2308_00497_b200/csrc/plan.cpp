@@ -348,10 +348,12 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
 #ifndef FFTGEN_PLANE_MIN_LOG2
 #define FFTGEN_PLANE_MIN_LOG2 11
 #endif
-bool group_prefers_tma(int log2ns, bool first, bool rows) {
-  // rows: the 2^9 group through the TMA kernel (staged tensor stores,
-  // fft_group_tma.cuh); 2^10 rows stay on the plain kernel (0.383 vs 0.378)
-  return (!rows && first && log2ns >= 9) || (rows && log2ns == 9) || log2ns >= FFTGEN_PLANE_MIN_LOG2;
+bool group_prefers_tma(int log2ns, bool first, bool rows, int64_t cols) {
+  // rows: the 2^9 groups and the 2^10 group of 2^19 (cols 512) through the TMA
+  // kernel with staged tensor stores (fft_group_tma.cuh); the 2^10 rows of
+  // 2^20 stay on the plain kernel (0.383 vs 0.378)
+  const bool rows_tma = rows && (log2ns == 9 || (log2ns == 10 && cols <= 512));
+  return (!rows && first && log2ns >= 9) || rows_tma || log2ns >= FFTGEN_PLANE_MIN_LOG2;
 }
 
 }  // namespace fftgen_b200

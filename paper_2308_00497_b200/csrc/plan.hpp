@@ -93,7 +93,7 @@ enum SplitMode { SPLIT_DEFAULT = 0, SPLIT_GROUPS_1024 = 1, SPLIT_TWO_PASS = 2 };
 // layout: 0 interleaved, 1 split (the default split depends on it at 2^23)
 std::vector<int> group_split(int log2n, int mode = SPLIT_DEFAULT, int layout = 0);
 // whether a group runs the persistent TMA-tile kernel by default (measured)
-bool group_prefers_tma(int log2ns, bool first, bool rows);
+bool group_prefers_tma(int log2ns, bool first, bool rows, int64_t cols = 0);
 void group_geom(int log2ns, int64_t *threads, int64_t *tc, int64_t *smem, int64_t *r0);
 
 ExecPlan build_exec_plan(int64_t n, int split_mode = SPLIT_DEFAULT, int pass_radix = 0, int layout = 0);
