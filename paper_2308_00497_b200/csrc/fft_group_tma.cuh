@@ -260,6 +260,43 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
 #define FFTGEN_GROUP_PLANE 1
 #endif
 
+// Plane kernel results by TMA tensor stores, staged through the exchange plane
+// in two halves (split: the re plane, then the im plane; interleaved: output
+// rows e < NS/2, then the rest) instead of per-lane STGs, where measured
+// faster (B200, `scripts/gpu_ab_ps.sh`): every column group and NS = 4096
+// rows (2^23 / 2^24 interleaved two-pass 0.334 / 0.310 -> 0.364 / 0.330,
+// 2^24 batch 1 0.146 -> 0.137 ms) and NS = 2048 rows of split output (2^21
+// split 0.381 -> 0.389); NS = 2048 rows of interleaved output lose (2^21 /
+// 2^22 0.385 / 0.396 -> 0.379 / 0.390) and keep the register stores.
+#ifndef FFTGEN_PLANE_STORE
+#define FFTGEN_PLANE_STORE 1
+#endif
+constexpr bool group_plane_store_rt(int ns, bool rows, int lout) {
+  return FFTGEN_PLANE_STORE && (!rows || ns == 4096 || lout == LAYOUT_SPLIT);
+}
+
+// half h of a tile's results, staged in src as [e][f] (<= 256-row boxes)
+template <int NS, int LOUT, bool ROWS>
+FFTGEN_FI void group_tma_store_half(const GroupTmaArgs &ta, const char *src, int64_t b, int64_t m0, int64_t c0,
+                                    int h) {
+  constexpr int TC = GroupGeom<NS>::TC;
+  constexpr int CH = 256;
+  if constexpr (LOUT == LAYOUT_SPLIT) {  // rows only: plane h over all NS rows
+#pragma unroll
+    for (int q = 0; q < NS / CH; ++q)
+      tma_store_4d(ta.omap[h], src + q * CH * TC * 4, (int)m0, q * CH, (int)b, 0);
+  } else {
+#pragma unroll
+    for (int q = 0; q < NS / 2 / CH; ++q) {
+      const int e0 = h * (NS / 2) + q * CH;
+      if constexpr (ROWS)
+        tma_store_4d(ta.omap[0], src + q * CH * TC * 8, (int)(m0 * 2), e0, (int)b, 0);
+      else
+        tma_store_4d(ta.omap[0], src + q * CH * TC * 8, (int)(c0 * 2), (int)m0, e0, (int)b);
+    }
+  }
+}
+
 template <int NS> struct GroupPlaneGeom {
   using GG = GroupGeom<NS>;
   using PL = typename GG::PL;
@@ -281,6 +318,8 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
   using PG = GroupPlaneGeom<NS>;
   using G = typename PG::G;
   static_assert(PG::ENABLED, "plane-exchange group kernel: NS >= 2^FFTGEN_PLANE_MIN_LOG2, two passes");
+  constexpr bool PST = group_plane_store_rt(NS, ROWS, LOUT);
+  static_assert(!PST || (PG::PLANE >= NS * PG::TC * 4 && NS / 2 >= 256), "a result half fits the plane");
   static_assert(GroupTmaGeom<NS>::RAW == PG::RAW, "same raw tile as the TMA issue helper");
   constexpr int TC = PG::TC, T = G::T, REGP = PG::REGP;
   constexpr int R0 = G::R(0), K0 = G::K(0), J0 = G::RMAX / R0;
@@ -335,6 +374,8 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
             v[j * R0 + A0] = reinterpret_cast<const float2 *>(stage)[e];
           }
         }
+        if constexpr (PST)  // the previous tile's second-half store has read the plane
+          if (j == 0 && tid == 0) bulk_wait_read0();
         if (tw) {
           const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
 #pragma unroll
@@ -367,15 +408,40 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
     } else {
       pass_compute<G, 1, DIR>(t, a.tw_local, v);
     }
-    const int64_t ob = b * a.odist;
+    if constexpr (PST) {
 #pragma unroll
-    for (int B = 0; B < R1; ++B) {
-      const int64_t e = B * COLS1 + t;
-      const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
-      SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+      for (int h = 0; h < 2; ++h) {
+        __syncthreads();  // pass-1 plane reads (h = 0) / the first half's store read (h = 1) done
+        if constexpr (LOUT == LAYOUT_SPLIT) {
+#pragma unroll
+          for (int B = 0; B < R1; ++B) P[(B * COLS1 + t) * TC + f] = h ? v[B].y : v[B].x;
+        } else {
+          float2 *P2 = reinterpret_cast<float2 *>(P);
+#pragma unroll
+          for (int B = h * (R1 / 2); B < (h + 1) * (R1 / 2); ++B)
+            P2[(B * COLS1 + t - h * (NS / 2)) * TC + f] = v[B];
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+          group_tma_store_half<NS, LOUT, ROWS>(ta, reinterpret_cast<const char *>(P), b, m0, c0, h);
+          bulk_commit();
+          if (h == 0) bulk_wait_read0();
+        }
+      }
+    } else {
+      const int64_t ob = b * a.odist;
+#pragma unroll
+      for (int B = 0; B < R1; ++B) {
+        const int64_t e = B * COLS1 + t;
+        const int64_t off = ROWS ? e * a.cols + m0 + f : (e * a.cols + m0) * a.k + c0 + f;
+        SIO<LOUT>::store(a.out0, a.out1, ob + off, v[B]);
+      }
     }
     // the next iteration's plane writes follow its post-pass-0 barrier
   }
+  if constexpr (PST)
+    if (tid == 0) bulk_wait0();
 }
 
 }  // namespace fftgen_b200

@@ -496,7 +496,8 @@ bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
   // the plane kernel (NS >= 2^11) stores from registers
   const bool rows = shape == 2 || shape == 3;
   const int lin = shape == 0 ? LAYOUT_INTERLEAVED : (shape == 1 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
-  if (group_tma_store_rt(1 << log2ns, rows, lin) && !group_plane(log2ns))
+  const int lout = shape == 2 ? LAYOUT_INTERLEAVED : (shape == 3 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
+  if (group_plane(log2ns) ? group_plane_store_rt(1 << log2ns, rows, lout) : group_tma_store_rt(1 << log2ns, rows, lin))
     return encode_out_maps(ta.g, log2ns, shape, batch, tc, ta.omap);
   return true;
 }

@@ -330,7 +330,9 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
   // vs 1.07 ms per GiB three-pass, 2^24 12+12 1.06 vs 1.06 (batch 8) and
   // 0.146 vs 0.149 ms (batch 1); split 2^23 / 2^24 1.28 / 1.48 vs 1.13 /
   // 1.14 -- the NS = 4096 tiles move 16-byte plane segments -- keep three)
-  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : (layout == 0 ? 24 : 22));
+  // (+ TMA tensor stores from the plane kernel: split 2^23 11+12 1.07 vs 1.13
+  // ms per GiB -> two; 2^24 1.22 vs 1.15 -> three)
+  const int two = mode == SPLIT_GROUPS_1024 ? 20 : (mode == SPLIT_TWO_PASS ? 24 : (layout == 0 ? 24 : 23));
   const int g = log2n <= two ? 2 : (log2n <= 28 ? 3 : 4);
   std::vector<int> out(g, log2n / g);
   // One 2^9 group among 2^8 ones goes first, where the TMA column kernel runs
