@@ -111,6 +111,7 @@ struct fftgen_plan {
   int tma_grid = 0;
   bool use_tma = true;
   bool use_tma_store = true;
+  bool use_rows = false;  // K2r row kernel (N = 8 .. 64)
 };
 
 NvtxRange::NvtxRange(const fftgen_plan *p, const char *what) {
@@ -246,6 +247,8 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                          (dist * esz) % 16 == 0;
     const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
+    if (p->use_rows && aligned && out_aligned && (dist * esz) % 16 == 0)
+      return rows_launch(p->ex.log2n, layout, direction, a, s);
     if (p->use_tma && p->tma_grid > 0 && aligned) {
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
       const int grid = (int)std::min<int64_t>((batch + tp - 1) / tp, p->tma_grid);
@@ -479,6 +482,12 @@ fftgen_status fftgen_plan_create(fftgen_plan **out, const fftgen_config *cfg) {
       }
       p->use_tma = !(tune & FFTGEN_TUNE_NO_TMA);
       p->use_tma_store = !(tune & FFTGEN_TUNE_NO_TMA_STORE);
+      // N = 8 .. 64: the row kernel (FFTGEN_TUNE_NO_TMA keeps the direct kernel)
+      if (rows_enabled(p->ex.log2n) && !p->ex.block_cap && p->use_tma) {
+        if ((e = rows_prepare(p->ex.log2n)) != cudaSuccess)
+          return bail(FFTGEN_ERR_GPUMAP, std::string("row kernel attributes: ") + cudaGetErrorString(e));
+        p->use_rows = true;
+      }
     }
     cudaStream_t ps = nullptr;  // private stream for the plan's own uploads
     if ((e = cudaStreamCreateWithFlags(&ps, cudaStreamNonBlocking)) != cudaSuccess)
@@ -797,7 +806,14 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
   o << "\n";
   if (p->ex.strategy == STRAT_BLOCK) {
     int64_t threads, tpb, smem;
-    if (p->use_tma && p->tma_grid > 0) {
+    if (p->use_rows) {
+      rows_geom(p->ex.log2n, p->cfg.layout, &threads, &smem);
+      o << "kernel fft_rows_kernel<" << p->cfg.n << "> grid[" << (p->cfg.batch + threads - 1) / threads << "] block["
+        << threads << "] smem=" << smem << "B transforms/CTA=" << threads
+        << " (one transform per thread: DFT_" << p->cfg.n
+        << " as one register codelet over the passes below; coalesced 16-byte row moves; direct kernel if"
+           " unaligned)\n";
+    } else if (p->use_tma && p->tma_grid > 0) {
       block_tma_geom(p->ex.log2n, &threads, &tpb, &smem);
       const int64_t groups = (p->cfg.batch + tpb - 1) / tpb;
       const bool single = block_tma1(p->ex.log2n);

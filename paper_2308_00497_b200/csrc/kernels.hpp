@@ -23,6 +23,12 @@ struct BlockArgs {
 
 // K2: one CTA per TPB whole transforms, N = 2^log2n <= 2^14.
 cudaError_t block_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
+// K2r (fft_rows.cu): N = 8 .. 64, one transform per thread, coalesced 16-byte
+// row moves; needs 16-byte aligned planes and dist
+bool rows_enabled(int log2n);
+cudaError_t rows_prepare(int log2n);
+cudaError_t rows_launch(int log2n, int layout, int dir, const BlockArgs &a, cudaStream_t s);
+void rows_geom(int log2n, int layout, int64_t *threads, int64_t *smem);
 cudaError_t block_prepare(int log2n, int *tma_blocks_per_sm);
 // K2 direct kernel under a pass-radix cap (8 / 16 / 32; CapPlanGeom) for the
 // sizes whose capped plan differs from the default

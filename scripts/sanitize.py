@@ -12,7 +12,7 @@ def main():
     import torch
     import paper_2308_00497_b200 as fg
 
-    cases = [(64, 5), (256, 7), (512, 3), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 150),  # K2
+    cases = [(8, 5), (16, 301), (32, 129), (64, 5), (256, 7), (512, 3), (1024, 9), (2048, 5), (4096, 7), (8192, 3), (16384, 150),  # K2
              (1 << 15, 3), (1 << 16, 2), (1 << 18, 1), (1 << 19, 1), (1 << 20, 1), (1 << 21, 1),
              (1 << 22, 1), (1 << 23, 1)]  # K5, K3 (+TMA groups, tensor-store epilogues, plane kernels)
     # non-default kernel selections: (PipelineConfig overrides, n, batch)

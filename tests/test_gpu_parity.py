@@ -328,3 +328,29 @@ def test_large_batch_persistent_grid(orc):
     for b in (0, 777, batch - 1):
         xi = x[b].reshape(-1).double().cpu().numpy()
         assert oracle.rel_l2(y[b].reshape(-1).double().cpu().numpy(), orc.forward(xi, "stockham", 4)) < 2e-6
+
+
+@pytest.mark.parametrize("n", [8, 16, 32, 64])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_row_kernel_small_sizes(orc, n, layout):
+    """K2r (fft_rows.cu, one transform per thread, coalesced 16-byte row
+    moves) for N = 8 .. 64: ragged batches (not a multiple of the CTA's
+    transforms, and a single transform), padded rows (dist > N), both
+    directions; a dist that breaks 16-byte alignment takes the direct kernel,
+    same results within tolerance."""
+    p = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=1))
+    assert f"fft_rows_kernel<{n}>" in p.describe()
+    assert f"fft_rows_kernel<{n}>" not in fg.compile_pipeline(
+        fg.PipelineConfig(n=n, layout=layout, batch=1, tuning=fg.TUNE_NO_TMA)).describe()
+    for batch in (1, 301):
+        x = seeded_batch(orc, n, batch, seed0=11)
+        want_f = orc.forward(x, "stockham", 4)
+        want_i = orc.forward(x, "stockham", 4, inverse=True)
+        for dist in (n, n + 4):
+            check(run(n, layout, -1, x, dist=dist), want_f, n)
+            check(run(n, layout, 1, x, dist=dist), want_i, n)
+    x = seeded_batch(orc, n, 37, seed0=5)
+    a = run(n, layout, -1, x, dist=n + 1)  # 4- / 8-byte row offsets: direct kernel
+    b = run(n, layout, -1, x, tuning=fg.TUNE_NO_TMA)
+    assert np.array_equal(a, b)
+    check(a, orc.forward(x, "stockham", 4), n)
