@@ -126,9 +126,12 @@ def test_cluster_in_place_and_graph(fg, orc, n):
     assert torch.equal(y, y2)  # chunked two-launch path == cluster kernel, bitwise
 
 
-@pytest.mark.parametrize("n", [1 << 15, 1 << 17])
+@pytest.mark.parametrize("n", [1 << 15, 1 << 17, 1 << 18, 1 << 19, 1 << 20, 1 << 22, 1 << 23])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 def test_fourstep_ragged_batch_and_padded_dist(fg, orc, n, layout):
+    """Padded rows through every K3 epilogue: register stores, the TMA tensor
+    stores of the NS = 512 / 1024 rows and split NS = 1024 columns, the
+    plane kernels' staged halves (2^22, 2^23)."""
     batch, dist = 3, n + 64
     x = rand((batch, dist, 2), 4)
     plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout=layout))
@@ -158,6 +161,34 @@ def test_unaligned_pointers_fall_back_to_direct_kernel(fg, orc):
     # a float2 stream that is not even 8-byte aligned is rejected, not faulted
     with pytest.raises(fg.ExecError):
         plan.execute(buf[1:1 + batch * n * 2], y)
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1 << 20, 1 << 23])
+@pytest.mark.parametrize("layout", ["interleaved", "split"])
+def test_fourstep_unaligned_output_falls_back(fg, orc, n, layout):
+    """An output that is 8- but not 16-byte aligned cannot be a TMA tensor
+    store target: those groups take the register-store kernels, same results."""
+    batch = 2
+    x = rand((batch, n, 2), 9)
+    plan = fg.compile_pipeline(fg.PipelineConfig(n=n, batch=batch, layout=layout))
+    if layout == "interleaved":
+        out = torch.full((batch * n * 2 + 4,), float("nan"), device="cuda")
+        y = out[2:2 + batch * n * 2].view(batch, n, 2)
+        plan.execute(x, y)
+        yy = torch.empty_like(x)
+        plan.execute(x, yy)
+    else:
+        re, im = x[..., 0].contiguous(), x[..., 1].contiguous()
+        out = torch.full((2, batch * n + 4), float("nan"), device="cuda")
+        ore, oim = out[0, 1:1 + batch * n].view(batch, n), out[1, 1:1 + batch * n].view(batch, n)
+        plan.execute(re, ore, im, oim)
+        y = torch.stack([ore, oim], -1)
+        a, b = torch.empty_like(re), torch.empty_like(im)
+        plan.execute(re, a, im, b)
+        yy = torch.stack([a, b], -1)
+    torch.cuda.synchronize()
+    assert torch.equal(y, yy)  # the store epilogue does not change the arithmetic
+    check_rows(orc, x, y, n, rows=(0, 1))
 
 
 def test_smaller_batch_than_planned_via_host_path(fg, orc):
