@@ -122,9 +122,9 @@ FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ t
   }
 }
 
-template <class G, int NS, int DIR, int BARID, int THREADS>
-FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ tw, float2 *v, const GroupTw<G> &gt) {
-  if constexpr (group_pq<G>()) {
+template <class G, int NS, int DIR, int BARID, int THREADS, bool ON>
+FFTGEN_FI void group_passes_rest(float2 *Xf, int t, const float2 *__restrict__ tw, float2 *v, const GroupTw<G, ON> &gt) {
+  if constexpr (ON) {
     smem_read_pass1_pq<G, NS, DIR>(Xf, t, gt.pq, v);
     return;
   }
