@@ -851,6 +851,9 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
       int64_t threads, tc, smem, r0;
       group_geom(d.log2ns, &threads, &tc, &smem, &r0);
       const bool tma = i < p->group_tma_grid.size() && p->group_tma_grid[i] > 0;
+      const bool last = i + 1 == p->ex.groups.size(), split = p->cfg.layout == FFTGEN_LAYOUT_SPLIT;
+      const int shape = last ? (split ? 3 : 2) : (i == 0 ? (split ? 1 : 0) : 4);
+      const bool stores = tma && group_tma_stores(d.log2ns, shape);
       o << "  group " << i << ": "
         << (tma ? (group_plane(d.log2ns) ? "fft_group_plane_kernel<" : "fft_group_tma_kernel<") : "fft_group_kernel<")
         << d.ns
@@ -863,7 +866,7 @@ fftgen_status fftgen_plan_describe(const fftgen_plan *p, char *buf, size_t cap) 
                                     "plain kernel if unaligned)"
                                   : " (persistent, TMA tensor tiles double-buffered; plain kernel if unaligned)")
                 : "")
-        << "\n";
+        << (stores ? " results by TMA tensor stores" : "") << "\n";
     }
   } else if (p->ex.strategy == STRAT_IDENTITY) {
     o << "identity copy\n";

@@ -78,6 +78,8 @@ struct GroupTmaArgs {
 cudaError_t group_tma_prepare(int log2ns, int *blocks_per_sm);
 // encode ta.tmap for ta.g's input; false if the input is not TMA-addressable
 bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta);
+// whether the TMA variant of this group shape stores its results by TMA tensor stores
+bool group_tma_stores(int log2ns, int shape);
 // tensor maps of a's input planes for tiles of tc transforms (shape as group_launch)
 bool encode_tile_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, int64_t tc,
                       unsigned char (*tmap)[128]);

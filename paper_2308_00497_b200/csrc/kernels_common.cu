@@ -489,16 +489,19 @@ bool encode_out_maps(const GroupArgs &a, int log2ns, int shape, int64_t batch, i
   return true;
 }
 
+bool group_tma_stores(int log2ns, int shape) {
+  const bool rows = shape == 2 || shape == 3;
+  const int lin = shape == 0 ? LAYOUT_INTERLEAVED : (shape == 1 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
+  const int lout = shape == 2 ? LAYOUT_INTERLEAVED : (shape == 3 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
+  return group_plane(log2ns) ? group_plane_store_rt(1 << log2ns, rows, lout) : group_tma_store_rt(1 << log2ns, rows, lin);
+}
+
 bool group_tma_encode(int log2ns, int shape, int64_t batch, GroupTmaArgs &ta) {
   int64_t threads, tc, smem, r0;
   group_geom(log2ns, &threads, &tc, &smem, &r0);
   if (!encode_tile_maps(ta.g, log2ns, shape, batch, tc, ta.tmap)) return false;
   // the plane kernel (NS >= 2^11) stores from registers
-  const bool rows = shape == 2 || shape == 3;
-  const int lin = shape == 0 ? LAYOUT_INTERLEAVED : (shape == 1 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
-  const int lout = shape == 2 ? LAYOUT_INTERLEAVED : (shape == 3 ? LAYOUT_SPLIT : LAYOUT_SCRATCH);
-  if (group_plane(log2ns) ? group_plane_store_rt(1 << log2ns, rows, lout) : group_tma_store_rt(1 << log2ns, rows, lin))
-    return encode_out_maps(ta.g, log2ns, shape, batch, tc, ta.omap);
+  if (group_tma_stores(log2ns, shape)) return encode_out_maps(ta.g, log2ns, shape, batch, tc, ta.omap);
   return true;
 }
 

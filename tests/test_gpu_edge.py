@@ -163,6 +163,21 @@ def test_unaligned_pointers_fall_back_to_direct_kernel(fg, orc):
         plan.execute(buf[1:1 + batch * n * 2], y)
 
 
+def test_fourstep_store_epilogues_per_group(fg):
+    """The plan states which K3 groups leave by TMA tensor stores (the
+    measured rule of fft_group_tma.cuh: NS = 512 / 2^19's NS = 1024 rows,
+    split-input NS = 1024 columns, plane-kernel columns, NS = 4096 rows and
+    NS = 2048 rows of split output)."""
+    def stores(n, layout):
+        d = fg.compile_pipeline(fg.PipelineConfig(n=n, layout=layout, batch=1)).describe()
+        return [("results by TMA tensor stores" in ln) for ln in d.splitlines() if ln.startswith("  group ")]
+    assert stores(1 << 18, "split") == [False, True] and stores(1 << 18, "interleaved") == [False, True]
+    assert stores(1 << 19, "split") == [False, True]
+    assert stores(1 << 20, "split") == [True, False] and stores(1 << 20, "interleaved") == [False, False]
+    assert stores(1 << 22, "split") == [True, True] and stores(1 << 22, "interleaved") == [True, False]
+    assert stores(1 << 24, "interleaved") == [True, True] and stores(1 << 16, "split") == [False, False]
+
+
 @pytest.mark.parametrize("n", [1 << 18, 1 << 20, 1 << 23])
 @pytest.mark.parametrize("layout", ["interleaved", "split"])
 def test_fourstep_unaligned_output_falls_back(fg, orc, n, layout):
