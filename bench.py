@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no JSON)")
     ap.add_argument("--workload", choices=["batched", "distributed"], default="batched",
                     help="distributed: one N-point transform over all ranks (config C5, e.g. --n 1073741824)")
+    ap.add_argument("--order", choices=["natural", "cyclic"], default="natural",
+                    help="distributed: output order (cyclic = X[rank + P j], two exchanges instead of three)")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
                     help="distributed: NCCL all-to-alls, or the exchanges fused into the kernels over symmetric memory")
     ap.add_argument("--launch-selftest", action="store_true",
@@ -552,7 +554,8 @@ def run_distributed(a):
     # rank r's block of the reference input x = seeded_input(n, 1), generated on the device
     x = torch.view_as_complex(fg.seeded_input(n, 1, "interleaved", seed0=1, device=local)[0][rank * m:(rank + 1) * m])
     x = x.contiguous()
-    d = DistributedFFT(n, device=local, transport=a.transport)
+    d = DistributedFFT(n, device=local, transport=a.transport, output_order=a.order)
+    cyclic = a.order == "cyclic" and world > 1
     if a.transport == "p2p":
         d.input_block().copy_(x)
         x = d.input_block()  # zero-copy input: the symmetric block itself
@@ -582,10 +585,13 @@ def run_distributed(a):
         d._barrier(); ev[1].record()
         d.stages.butterfly_peers(d._peer["x"], d._peer["recv"], direction); ev[2].record()
         d._barrier(); ev[3].record()
-        d.stages.local(rb, zb, direction); ev[4].record()
-        d._barrier(); ev[5].record()
-        d.stages.unpack_peers(d._peer["z"], out); ev[6].record()
-        d._barrier()
+        d.stages.local(rb, out if cyclic else zb, direction); ev[4].record()
+        if cyclic:
+            ev[5].record(); ev[6].record()
+        else:
+            d._barrier(); ev[5].record()
+            d.stages.unpack_peers(d._peer["z"], out); ev[6].record()
+            d._barrier()
     else:
         names = ["exchange1", "butterfly", "exchange2", "local", "exchange3", "unpack"]
         if world == 1:
@@ -596,9 +602,12 @@ def run_distributed(a):
         d.exchange(x, w0); ev[1].record()
         d.stages.butterfly(w0, w1, direction); ev[2].record()
         d.exchange(w1, w0); ev[3].record()
-        d.stages.local(w0, w1, direction); ev[4].record()
-        d.exchange(w1, w0); ev[5].record()
-        d.stages.unpack(w0, out); ev[6].record()
+        d.stages.local(w0, out if cyclic else w1, direction); ev[4].record()
+        if cyclic:
+            ev[5].record(); ev[6].record()
+        else:
+            d.exchange(w1, w0); ev[5].record()
+            d.stages.unpack(w0, out); ev[6].record()
     torch.cuda.synchronize(dev)
     stages = torch.tensor([ev[i].elapsed_time(ev[i + 1]) for i in range(6)], device=dev, dtype=torch.float64)
     dist.all_reduce(stages, op=dist.ReduceOp.MAX)
@@ -627,7 +636,7 @@ def run_distributed(a):
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         st = {k: round(float(v), 4) for k, v in zip(names, stages)}
         xms = sum(v for k, v in st.items() if "exchange" in k)
-        wire = 3 * 8 * m * (world - 1) / world
+        wire = (2 if cyclic else 3) * 8 * m * (world - 1) / world
         local_plan = d.stages.describe_local().splitlines()
         print(json.dumps({
             "metric": METRIC, "value": round(gflop(n, 1) / (ms / 1e3), 2), "unit": "GFLOP/s", "n_gpus": world,
@@ -636,9 +645,11 @@ def run_distributed(a):
             "data": "synthetic: the reference's seeded_input(N, 1) (verify.cpp:55-78) generated on the device, "
                     "block-distributed", "impl": "ours",
             "config": {"workload": f"single c2c fp32 FFT N={n} block-distributed over {world} GPU(s): "
-                                   f"P-point butterfly + local N/P plan + unpack, 3 contiguous all-to-alls "
-                                   f"({'fused into the kernels over symmetric memory' if a.transport == 'p2p' else 'NCCL'})",
-                       "transport": a.transport,
+                                   + ("P-point butterfly + local N/P plan, cyclic output order, 2 contiguous all-to-alls "
+                                      if cyclic else
+                                      "P-point butterfly + local N/P plan + unpack, 3 contiguous all-to-alls ")
+                                   + f"({'fused into the kernels over symmetric memory' if a.transport == 'p2p' else 'NCCL'})",
+                       "transport": a.transport, "output_order": a.order,
                        "n": n, "block_per_gpu": m, "chunk": m // world, "direction": a.direction,
                        "l2": "blocks of 8N/P bytes exceed the 126 MB L2 for N >= 2^25; no flush"},
             "stages_ms": st,
@@ -657,7 +668,7 @@ def run_distributed(a):
                     "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": 8 * m,
                     "ms_per_step": round(float(el[0]) * 1e3, 3), "path": "DistributedFFT.execute with pinned "
                     "host block copies in and out per rank"},
-            "gpu_launches": a.steps * (2 + d.stages.local_launches()),
+            "gpu_launches": a.steps * ((1 if cyclic else 2) + d.stages.local_launches()),
             "clocks": clk.summary()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()

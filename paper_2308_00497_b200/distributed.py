@@ -21,7 +21,11 @@
     5. exchange   contiguous output chunks         -> R3[q'][j] = X[s M + P j + q']
     6. unpack     out[P j + q'] = R3[q'][j]  (the stride-P interleave of Pi^N_P)
 
-  L1 = N/P^2.  The stages are injectable so the exchange logic is testable on
+  L1 = N/P^2.  output_order="cyclic" (the transposed-order output of SURVEY
+  8e) stops after step 4: rank s then holds X[s + P j], j < M -- the cyclic
+  distribution -- and the third all-to-all and the unpack are skipped (two
+  exchanges instead of three; a consumer that transforms back, e.g. a
+  convolution, takes the same order).  The stages are injectable so the exchange logic is testable on
   CPU with gloo (tests/test_distributed.py, a numpy restatement of the three
   stages) and `EmulatedDistributedFFT` runs P ranks in lockstep on ONE GPU
   with the real kernels, the exchanges being device copies of the same
@@ -80,6 +84,15 @@ class BatchShardedFFT:
             self.plan.execute(in0, out0, in1, out1, direction=direction, stream=stream)
 
 
+ORDERS = ("natural", "cyclic")
+
+
+def _check_order(order: str) -> str:
+    if order not in ORDERS:
+        raise ValueError(f"output_order must be 'natural' or 'cyclic', got {order!r}")
+    return order
+
+
 def check_geometry(n: int, world: int) -> None:
     if n < 4 or n & (n - 1):
         raise ValueError(f"n must be a power of two >= 4, got {n}")
@@ -98,10 +111,11 @@ class DistributedFFT:
     all_to_all_single over the group (a copy when the world is 1).
     transport="p2p" fuses the exchanges into the kernels over symmetric
     (peer-mapped) memory instead; `input_block()` is then the zero-copy
-    input buffer."""
+    input buffer.  output_order="cyclic" returns X[rank + P j] (j < M)
+    without the third exchange."""
 
     def __init__(self, n: int, group=None, device: Optional[int] = None, rank: Optional[int] = None,
-                 world: Optional[int] = None, stages=None, transport: str = "nccl"):
+                 world: Optional[int] = None, stages=None, transport: str = "nccl", output_order: str = "natural"):
         r, w = _rank_world(group)
         self.group = group
         self.rank = r if rank is None else rank
@@ -110,6 +124,7 @@ class DistributedFFT:
         self.n = n
         self.m = n // self.world
         self.l1 = self.m // self.world
+        self.output_order = _check_order(output_order)
         if stages is None:
             if device is None:
                 device = torch.cuda.current_device()
@@ -155,6 +170,9 @@ class DistributedFFT:
         self._barrier()                       # every rank's input is in place
         self.stages.butterfly_peers(self._peer["x"], self._peer["recv"], direction)
         self._barrier()                       # every receive block is complete
+        if self.output_order == "cyclic":     # X[rank + P j]: no third exchange
+            self.stages.local(recv_blk, out, direction)
+            return out                        # the next execute's first barrier orders the reuse
         self.stages.local(recv_blk, z_blk, direction)
         self._barrier()                       # every local result is complete
         self.stages.unpack_peers(self._peer["z"], out)
@@ -177,7 +195,8 @@ class DistributedFFT:
 
     def execute(self, x_local: torch.Tensor, direction: int = FORWARD,
                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """x_local: complex64 (M,) = x[rank*M : (rank+1)*M]; returns X^ of the same block."""
+        """x_local: complex64 (M,) = x[rank*M : (rank+1)*M]; returns X^ of the same
+        block (output_order "cyclic": X^[rank + P j], j < M)."""
         if x_local.numel() != self.m or x_local.dtype != torch.complex64:
             raise ValueError(f"expected a complex64 block of {self.m} elements")
         x_local = x_local.reshape(-1)
@@ -194,6 +213,9 @@ class DistributedFFT:
         self.exchange(x_local, w0)
         self.stages.butterfly(w0, w1, direction)
         self.exchange(w1, w0)
+        if self.output_order == "cyclic":
+            self.stages.local(w0, out, direction)
+            return out
         self.stages.local(w0, w1, direction)
         self.exchange(w1, w0)
         self.stages.unpack(w0, out)
@@ -216,8 +238,9 @@ class EmulatedDistributedFFT:
     runs, on one GPU."""
 
     def __init__(self, n: int, world: int, device: Optional[int] = None, stages_factory=None,
-                 transport: str = "nccl"):
+                 transport: str = "nccl", output_order: str = "natural"):
         check_geometry(n, world)
+        self.output_order = _check_order(output_order)
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         self.transport = transport
@@ -242,6 +265,10 @@ class EmulatedDistributedFFT:
             # order on one device stands in for the barriers between stages
             for r in range(P):
                 self.stages[r].butterfly_peers(blocks, w0, direction)
+            if self.output_order == "cyclic":
+                for r in range(P):
+                    self.stages[r].local(w0[r], out[r], direction)
+                return out
             for r in range(P):
                 self.stages[r].local(w0[r], w1[r], direction)
             for r in range(P):
@@ -251,6 +278,10 @@ class EmulatedDistributedFFT:
         for r in range(P):
             self.stages[r].butterfly(w0[r], w1[r], direction)
         emulated_exchange(w1, w0, self.l1)
+        if self.output_order == "cyclic":
+            for r in range(P):
+                self.stages[r].local(w0[r], out[r], direction)
+            return out
         for r in range(P):
             self.stages[r].local(w0[r], w1[r], direction)
         emulated_exchange(w1, w0, self.l1)

@@ -99,8 +99,25 @@ def test_emulated_composition_numpy_stages(world, n, direction):
     assert err < 1e-5 * np.log2(n), err
 
 
+@pytest.mark.parametrize("world,n", [(2, 1 << 10), (4, 1 << 12), (8, 1 << 12)])
+def test_emulated_cyclic_output_order(world, n):
+    """output_order="cyclic": rank s ends with X[s + P j] after two exchanges."""
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    z, want = _want(n, -1)
+    e = EmulatedDistributedFFT(n, world, stages_factory=lambda r: NumpyStages(n, world, r), output_order="cyclic")
+    m = n // world
+    outs = e.execute([torch.from_numpy(z[r * m:(r + 1) * m].copy()) for r in range(world)], -1)
+    got = np.empty(n, dtype=np.complex128)
+    for s in range(world):
+        got[s::world] = outs[s].numpy()
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err < 1e-5 * np.log2(n), err
+    with pytest.raises(ValueError):
+        EmulatedDistributedFFT(n, world, stages_factory=lambda r: NumpyStages(n, world, r), output_order="bitrev")
+
+
 # ---------------------------------------------------------------- gloo workers
-def _dist_worker(rank, world, port, n, direction, q):
+def _dist_worker(rank, world, port, n, direction, q, order="natural"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -108,25 +125,32 @@ def _dist_worker(rank, world, port, n, direction, q):
         from paper_2308_00497_b200.distributed import DistributedFFT
         z, _ = _want(n, direction)
         m = n // world
-        d = DistributedFFT(n, stages=NumpyStages(n, world, rank))
+        d = DistributedFFT(n, stages=NumpyStages(n, world, rank), output_order=order)
         local = torch.from_numpy(z[rank * m:(rank + 1) * m].copy())
         out = d.execute(local, direction=direction)
         gathered = [torch.empty_like(out) for _ in range(world)]
         dist.all_gather(gathered, out)
         if rank == 0:
-            q.put(torch.cat(gathered).numpy())
+            if order == "cyclic":  # rank s holds X[s + P j]
+                full = np.empty(n, dtype=np.complex128)
+                for s_, g in enumerate(gathered):
+                    full[s_::world] = g.numpy()
+                q.put(full)
+            else:
+                q.put(torch.cat(gathered).numpy())
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n", [(2, 1 << 10), (4, 1 << 12), (2, 1 << 13)])
+@pytest.mark.parametrize("world,n,order", [(2, 1 << 10, "natural"), (4, 1 << 12, "natural"), (2, 1 << 13, "natural"),
+                                           (2, 1 << 10, "cyclic")])
 @pytest.mark.parametrize("direction", [-1, 1])
-def test_distributed_four_step_gloo(world, n, direction):
-    """Real process group (gloo all_to_all_single), world 2 / 4."""
+def test_distributed_four_step_gloo(world, n, order, direction):
+    """Real process group (gloo all_to_all_single), world 2 / 4; both output orders."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, n, direction, q)) for r in range(world)]
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, n, direction, q, order)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=240)

@@ -111,6 +111,26 @@ def test_emulated_2p20_vs_oracle(fg, orc, world, direction):
     assert err <= tol(n) and err < 3e-6, err
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_emulated_cyclic_output_order(fg, orc, world, transport):
+    """output_order="cyclic" (two exchanges): rank s holds X[s + P j], the
+    same values the natural-order path unpacks, bitwise."""
+    from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
+    n = 1 << 20
+    x, z = seeded_complex(orc, n)
+    blocks = blocks_of(z, world)
+    cyc = EmulatedDistributedFFT(n, world, transport=transport, output_order="cyclic").execute(blocks)
+    nat = torch.cat(EmulatedDistributedFFT(n, world, transport=transport).execute(blocks))
+    got = torch.empty_like(nat)
+    for s in range(world):
+        got[s::world] = cyc[s]
+    assert torch.equal(got, nat)
+    want = oracle.as_complex(orc.forward(x[None], "stockham", 4, threads=4))[0]
+    err = np.linalg.norm(got.cpu().numpy() - want) / np.linalg.norm(want)
+    assert err <= tol(n), err
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_emulated_2p24_vs_oracle(fg, orc, world):
     from paper_2308_00497_b200.distributed import EmulatedDistributedFFT
