@@ -247,8 +247,7 @@ cudaError_t enqueue(const fftgen_plan *p, int direction, const void *in0, const 
     const bool aligned = ((uintptr_t)in0 % 16 == 0) && (!in1 || (uintptr_t)in1 % 16 == 0) &&
                          (dist * esz) % 16 == 0;
     const bool out_aligned = ((uintptr_t)out0 % 16 == 0) && (!out1 || (uintptr_t)out1 % 16 == 0);
-    if (p->use_rows && aligned && out_aligned && (dist * esz) % 16 == 0)
-      return rows_launch(p->ex.log2n, layout, direction, a, s);
+    if (p->use_rows && aligned && out_aligned) return rows_launch(p->ex.log2n, layout, direction, a, s);
     if (p->use_tma && p->tma_grid > 0 && aligned) {
       const int64_t tp = block_tma_transforms_per_cta(p->ex.log2n);
       const int grid = (int)std::min<int64_t>((batch + tp - 1) / tp, p->tma_grid);
