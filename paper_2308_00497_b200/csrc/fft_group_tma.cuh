@@ -27,6 +27,15 @@ namespace fftgen_b200 {
 #define FFTGEN_GROUP_TMA_STAGES 2
 #endif
 constexpr int kGroupTmaStages = FFTGEN_GROUP_TMA_STAGES;
+// Pass-0 global twiddles of a tile fetched before its stage wait, where
+// measured faster (`scripts/gpu_ab_tp.sh`): 2^18 0.427 / 0.422 -> 0.436 /
+// 0.434, 2^20 / 2^21 interleaved 0.404 / 0.385 -> 0.413 / 0.392; the split
+// NS = 1024 column group with tensor stores (register-bound) loses 0.5 %
+// and keeps the loads after the wait.
+#ifndef FFTGEN_GROUP_TWPRE
+#define FFTGEN_GROUP_TWPRE 1
+#endif
+
 // Results staged in a separate output buffer ([e][f], the tile of the store
 // box) and written by TMA tensor stores instead of per-lane STGs of
 // TC-element segments, where measured faster (B200, 1 GiB batches,
@@ -162,12 +171,27 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
       m0 = u0 / a.k;
       c0 = u0 - m0 * a.k;
     }
+    const int f0 = ROWS ? tid / T : tid % TC;
+    const int t0 = ROWS ? tid % T : tid / TC;
+    // this tile's pass-0 global twiddles, fetched before the stage wait
+    constexpr bool kPre = FFTGEN_GROUP_TWPRE && (ROWS || !ST);
+    float2 pre_p[kPre ? J0 : 1], pre_q[kPre ? R0 : 1];
+    if constexpr (kPre) {
+      if (a.cols > 1) {
+        const int64_t m = ROWS ? m0 + f0 : m0;
+#pragma unroll
+        for (int j = 0; j < J0; ++j) {
+          const int c = t0 + j * T;
+          pre_p[j] = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
+        }
+#pragma unroll
+        for (int A0 = 1; A0 < R0; ++A0) pre_q[A0] = __ldg(a.tw_q + m + A0 * a.cols);
+      }
+    }
     mbar_wait(&bars[s], (NST == 2 ? (it >> 1) : it) & 1);
 
     // ---- pass 0: raw tile -> registers, global twiddle, radix-R0 codelets ----
     float2 v[G::RMAX];
-    const int f0 = ROWS ? tid / T : tid % TC;
-    const int t0 = ROWS ? tid % T : tid / TC;
     {
       const int64_t m = ROWS ? m0 + f0 : m0;
       const bool tw = a.cols > 1;
@@ -187,11 +211,11 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
           }
         }
         if (tw) {
-          const float2 pw = __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
+          const float2 pw = kPre ? pre_p[kPre ? j : 0] : __ldg(ROWS ? a.tw_p + m * K0 + c : a.tw_p + c * a.cols + m);
 #pragma unroll
           for (int A0 = 0; A0 < R0; ++A0) {
             float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, kPre ? pre_q[kPre ? A0 : 0] : __ldg(qm + A0 * a.cols)) : x;
           }
         }
         reg_fft<R0, DIR>(v + j * R0);
