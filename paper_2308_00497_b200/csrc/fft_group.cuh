@@ -108,6 +108,41 @@ template <class G> struct GroupTw<G, false> {
   FFTGEN_FI void load(const float2 *__restrict__, int) {}
 };
 
+// Pass-0 global twiddles Q[A0][m] = w_s^{A0 (NS/R0) m} as products of two
+// loaded bases, Q[A0 % 8] * Q[8 (A0 / 8)] (14 loads per tile and thread
+// instead of R0 - 1 for the 32 / 64-point first passes of NS >= 2^11).
+// Every kernel of a given shape uses the same form (results bitwise equal).
+// Measured (`scripts/gpu_ab_qpq.sh`): 2^23 interleaved 0.373 -> 0.390, 2^22
+// 0.370 / 0.398 -> 0.375 / 0.404, 2^24 interleaved 0.344 -> 0.351.
+#ifndef FFTGEN_GROUP_Q_PQ_MIN
+#define FFTGEN_GROUP_Q_PQ_MIN 2048
+#endif
+// (the NS = 4096 rows group of split output ran 2.3x slower with it: excluded)
+template <int NS, int R0, bool ROWS, int LOUT> constexpr bool group_q_pq() {
+  return NS >= FFTGEN_GROUP_Q_PQ_MIN && R0 >= 16 && !(ROWS && LOUT == LAYOUT_SPLIT && NS >= 4096);
+}
+template <int R0, bool ON> struct QFact {
+  FFTGEN_FI void load(const float2 *, int64_t) {}
+  template <int DIR> FFTGEN_FI float2 apply(float2 x, const float2 *__restrict__ qm, int64_t cols, int A0) const {
+    return mul_tw<DIR>(x, __ldg(qm + A0 * cols));
+  }
+};
+template <int R0> struct QFact<R0, true> {
+  float2 lo[8], hi[R0 / 8];
+  FFTGEN_FI void load(const float2 *__restrict__ qm, int64_t cols) {
+#pragma unroll
+    for (int b = 1; b < 8; ++b) lo[b] = __ldg(qm + b * cols);
+#pragma unroll
+    for (int a = 1; a < R0 / 8; ++a) hi[a] = __ldg(qm + 8 * a * cols);
+  }
+  template <int DIR> FFTGEN_FI float2 apply(float2 x, const float2 *__restrict__, int64_t, int A0) const {
+    const int a = A0 / 8, b = A0 % 8;
+    if (b) x = mul_tw<DIR>(x, lo[b]);
+    if (a) x = mul_tw<DIR>(x, hi[a]);
+    return x;
+  }
+};
+
 // Passes 1 .. P-1 of a group sub-FFT whose pass-0 results sit in the padded
 // exchange (this column at Xf); lanes run over the tile's columns, thread t
 // owns the pass-p butterflies t + j T.
@@ -161,6 +196,8 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
     const bool tw = a.cols > 1;
     // Q[A0][m]: one address per warp (m is shared by the lanes) -> L1 broadcast
     const float2 *qm = a.tw_q + m;
+    QFact<R0, group_q_pq<NS, R0, ROWS, LOUT>()> qf;
+    if (tw) qf.load(qm, a.cols);
 #pragma unroll
     for (int j = 0; j < J0; ++j) {
       const int c = t + j * T;
@@ -175,7 +212,7 @@ FFTGEN_FI void group_tile(const GroupArgs &a, int64_t ib, int64_t ob, int64_t tt
 #pragma unroll
         for (int A0 = 0; A0 < R0; ++A0) {
           float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-          v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+          v[j * R0 + A0] = A0 ? qf.template apply<DIR>(x, qm, a.cols, A0) : x;
         }
       }
       reg_fft<R0, DIR>(v + j * R0);

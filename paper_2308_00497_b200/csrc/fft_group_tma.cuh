@@ -174,7 +174,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
     const int f0 = ROWS ? tid / T : tid % TC;
     const int t0 = ROWS ? tid % T : tid / TC;
     // this tile's pass-0 global twiddles, fetched before the stage wait
-    constexpr bool kPre = FFTGEN_GROUP_TWPRE && (ROWS || !ST);
+    constexpr bool kPre = FFTGEN_GROUP_TWPRE && (ROWS || !ST) && !group_q_pq<NS, R0, ROWS, LOUT>();
     float2 pre_p[kPre ? J0 : 1], pre_q[kPre ? R0 : 1];
     if constexpr (kPre) {
       if (a.cols > 1) {
@@ -196,6 +196,8 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
       const int64_t m = ROWS ? m0 + f0 : m0;
       const bool tw = a.cols > 1;
       const float2 *qm = a.tw_q + m;
+      QFact<R0, group_q_pq<NS, R0, ROWS, LOUT>()> qf;
+      if (tw) qf.load(qm, a.cols);
 #pragma unroll
       for (int j = 0; j < J0; ++j) {
         const int c = t0 + j * T;
@@ -215,7 +217,7 @@ fft_group_tma_kernel(const __grid_constant__ GroupTmaArgs ta) {
 #pragma unroll
           for (int A0 = 0; A0 < R0; ++A0) {
             float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, kPre ? pre_q[kPre ? A0 : 0] : __ldg(qm + A0 * a.cols)) : x;
+            v[j * R0 + A0] = A0 ? (kPre ? mul_tw<DIR>(x, pre_q[kPre ? A0 : 0]) : qf.template apply<DIR>(x, qm, a.cols, A0)) : x;
           }
         }
         reg_fft<R0, DIR>(v + j * R0);
@@ -384,6 +386,8 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
       const int64_t m = ROWS ? m0 + f0 : m0;
       const bool tw = a.cols > 1;
       const float2 *qm = a.tw_q + m;
+      QFact<R0, group_q_pq<NS, R0, ROWS, LOUT>()> qf;
+      if (tw) qf.load(qm, a.cols);
 #pragma unroll
       for (int j = 0; j < J0; ++j) {
         const int c = t0 + j * T;
@@ -405,7 +409,7 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
 #pragma unroll
           for (int A0 = 0; A0 < R0; ++A0) {
             float2 x = mul_tw<DIR>(v[j * R0 + A0], pw);
-            v[j * R0 + A0] = A0 ? mul_tw<DIR>(x, __ldg(qm + A0 * a.cols)) : x;
+            v[j * R0 + A0] = A0 ? qf.template apply<DIR>(x, qm, a.cols, A0) : x;
           }
         }
         reg_fft<R0, DIR>(v + j * R0);
