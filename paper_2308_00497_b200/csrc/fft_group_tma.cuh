@@ -323,6 +323,13 @@ FFTGEN_FI void group_tma_store_half(const GroupTmaArgs &ta, const char *src, int
   }
 }
 
+// the tile's factored pass-0 twiddle bases fetched before the stage wait
+// (`scripts` A/B: 2^22 split 0.371 -> 0.374, 2^24 interleaved 0.342-0.347 ->
+// 0.347-0.357, the rest within 0.5 %)
+#ifndef FFTGEN_PLANE_TWPRE
+#define FFTGEN_PLANE_TWPRE 1
+#endif
+
 template <int NS> struct GroupPlaneGeom {
   using GG = GroupGeom<NS>;
   using PL = typename GG::PL;
@@ -377,17 +384,20 @@ fft_group_plane_kernel(const __grid_constant__ GroupTmaArgs ta) {
       m0 = u0 / a.k;
       c0 = u0 - m0 * a.k;
     }
+    const int f0 = ROWS ? tid / T : tid % TC;
+    const int t0 = ROWS ? tid % T : tid / TC;
+    const int64_t m = ROWS ? m0 + f0 : m0;
+    const bool tw = a.cols > 1;
+    const float2 *qm = a.tw_q + m;
+    QFact<R0, group_q_pq<NS, R0, ROWS, LOUT>()> qf;
+    if constexpr (FFTGEN_PLANE_TWPRE)  // this tile's factored twiddle bases before the stage wait
+      if (tw) qf.load(qm, a.cols);
     mbar_wait(bar, it & 1);
     // ---- pass 0: raw tile -> registers, global twiddle, radix-R0 codelets ----
     float2 v[G::RMAX];
-    const int f0 = ROWS ? tid / T : tid % TC;
-    const int t0 = ROWS ? tid % T : tid / TC;
     {
-      const int64_t m = ROWS ? m0 + f0 : m0;
-      const bool tw = a.cols > 1;
-      const float2 *qm = a.tw_q + m;
-      QFact<R0, group_q_pq<NS, R0, ROWS, LOUT>()> qf;
-      if (tw) qf.load(qm, a.cols);
+      if constexpr (!FFTGEN_PLANE_TWPRE)
+        if (tw) qf.load(qm, a.cols);
 #pragma unroll
       for (int j = 0; j < J0; ++j) {
         const int c = t0 + j * T;
