@@ -70,16 +70,10 @@ template <int N, int CAP> struct CapPlanGeom {
 // Plans of the K3 group sub-FFTs: the block plan of the same size.  (Three
 // 8/16-point register passes for NS = 512 / 1024 measured slower on B200:
 // 2^18 0.31 vs 0.41, 2^20 0.29 vs 0.37 of the single-pass roofline.)
+// (NS = 2^11 / 2^12 as three 16-point passes on 1024-thread tiles measured
+// slower too.)
 template <int N> struct GroupPlan : BlockPlan<N> {};
-#ifdef FFTGEN_GROUP_BIG3
-// NS = 2^11 / 2^12 as three 16-point-codelet passes: 8x the warps of the
-// 64-point two-pass schedule (1024-thread tiles at 64 registers)
-template <> struct GroupPlan<2048> : PlanT<3, 8, 16, 16> {};
-template <> struct GroupPlan<4096> : PlanT<3, 16, 16, 16> {};
-#define FFTGEN_GROUP_MAXT_HUGE 1024
-#else
 #define FFTGEN_GROUP_MAXT_HUGE 512
-#endif
 
 // TP = transforms per CTA.  0 -> the direct kernel's default (128 threads).
 #ifndef FFTGEN_TW_FACTOR_COLS
