@@ -341,6 +341,15 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
   // (2^19 as 10+9: 0.36 vs 0.38).
   const bool large_first = log2n / g == 8 && log2n % g == 1;
   for (int i = 0; i < log2n % g; ++i) out[large_first ? i : g - 1 - i] += 1;
+  // Larger group first where the per-launch rates favour it (B200, ncu launch
+  // lists profiles/r2al_k3_launches.txt; sweeps `scripts/gpu_ab_order.sh`):
+  // 2^19 split as 10+9 0.452 vs 0.415 (the split-input NS = 1024 columns
+  // with tensor stores + the NS = 512 rows), 2^21 interleaved as 11+10 0.414
+  // vs 0.396, 2^23 split as 12+11 0.316 vs 0.312; the other layout loses
+  // (2^19 interleaved 0.426 vs 0.430, 2^21 split 0.378 vs 0.400).
+  if (mode == SPLIT_DEFAULT && g == 2 &&
+      ((layout == 1 && (log2n == 19 || log2n == 23)) || (layout == 0 && log2n == 21)))
+    std::swap(out[0], out[1]);
   return out;
 }
 
