@@ -341,15 +341,26 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
   // (2^19 as 10+9: 0.36 vs 0.38).
   const bool large_first = log2n / g == 8 && log2n % g == 1;
   for (int i = 0; i < log2n % g; ++i) out[large_first ? i : g - 1 - i] += 1;
-  // Larger group first where the per-launch rates favour it (B200, ncu launch
-  // lists profiles/r2al_k3_launches.txt; sweeps `scripts/gpu_ab_order.sh`):
-  // 2^19 split as 10+9 0.452 vs 0.415 (the split-input NS = 1024 columns
-  // with tensor stores + the NS = 512 rows), 2^21 interleaved as 11+10 0.414
-  // vs 0.396, 2^23 split as 12+11 0.316 vs 0.312; the other layout loses
-  // (2^19 interleaved 0.426 vs 0.430, 2^21 split 0.378 vs 0.400).
-  if (mode == SPLIT_DEFAULT && g == 2 &&
-      ((layout == 1 && (log2n == 19 || log2n == 23)) || (layout == 0 && log2n == 21)))
-    std::swap(out[0], out[1]);
+  // Two-group splits chosen from the per-launch rates (B200, ncu launch lists
+  // profiles/r2al_k3_launches.txt: rows groups of few points and column
+  // groups of many run fastest) and confirmed by sweeps
+  // (`scripts/gpu_ab_order.sh`, `gpu_ab_splits.sh`, `gpu_ab_splits2.sh`):
+  //   2^18 10+8 (both layouts)  0.460 / 0.458 vs 0.438 / 0.438 for 9+9
+  //   2^19 11+8 interleaved     0.470 vs 0.428 (9+10);  split 10+9 0.452 vs 0.415
+  //   2^20 12+8 interleaved     0.420 vs 0.411 (10+10); split keeps 10+10
+  //   2^21 11+10 interleaved    0.414 vs 0.396 (10+11); split keeps 10+11
+  //   2^23 12+11 split          0.316 vs 0.312 (11+12)
+  // Rows groups of 128 points lose everywhere (2^16..2^19 as 9+7 .. 12+7).
+  if (mode == SPLIT_DEFAULT && g == 2) {
+    const bool il = layout == 0;
+    int a = 0;
+    if (log2n == 18) a = 10;
+    else if (log2n == 19) a = il ? 11 : 10;
+    else if (log2n == 20 && il) a = 12;
+    else if (log2n == 21 && il) a = 11;
+    else if (log2n == 23 && !il) a = 12;
+    if (a) out = {a, log2n - a};
+  }
   return out;
 }
 

@@ -121,7 +121,8 @@ def test_fourstep_plan_shape(fg):
     assert q.launches() == 2 and q.scratch_bytes() == 4 * (1 << 16) * 8
     assert "group 0: fft_group_kernel<256>" in q.describe()
     q = fg.compile_pipeline(fg.PipelineConfig(n=1 << 18, layout="split", batch=2))
-    assert "group 0: fft_group_tma_kernel<512>" in q.describe()
+    assert [d[0] for d in q.passes()] == [1024, 256]  # measured split 10 + 8
+    assert "group 0: fft_group_tma_kernel<1024>" in q.describe()
 
 
 def test_fourstep_host_and_interpret_paths(fg, orc):
