@@ -361,6 +361,22 @@ std::vector<int> group_split(int log2n, int mode, int layout) {
     else if (log2n == 23 && !il) a = 12;
     if (a) out = {a, log2n - a};
   }
+  // three / four-group plans (`scripts/gpu_ab_splits3.sh`, batch 1): small
+  // groups first, the largest last -- 2^26 8+8+10 0.27 / 0.24 vs 0.245 /
+  // 0.226 (9+9+8), 2^27 interleaved 8+8+11 0.271 vs 0.251 (9+9+9; split keeps
+  // it: 0.238 vs 0.250), 2^28 8+9+11 0.246 / 0.217 vs 0.237 / 0.202
+  // (9+9+10), 2^29 interleaved 8+9+12 5.48 vs 6.01 ms (7+7+7+8; split keeps
+  // the four groups: 6.73 / 6.51 vs 6.32 ms for 8+9+12 / 8+10+11), 2^30
+  // interleaved 8+11+11 12.0 vs 12.3 ms (7+7+8+8; split keeps the four
+  // groups: 14.9 vs 13.0 ms); 2^25 keeps 9+8+8 (8+8+9 / 7+8+10 lose 4-10 %)
+  if (mode == SPLIT_DEFAULT) {
+    const bool il = layout == 0;
+    if (log2n == 26) out = {8, 8, 10};
+    else if (log2n == 27 && il) out = {8, 8, 11};
+    else if (log2n == 28) out = {8, 9, 11};
+    else if (log2n == 29 && il) out = {8, 9, 12};
+    else if (log2n == 30 && il) out = {8, 11, 11};
+  }
   return out;
 }
 
