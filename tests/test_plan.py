@@ -185,6 +185,26 @@ def test_pass_radix_hint_steers_block_passes(plan_tool):
             assert prod == n and len(rs) <= 4
 
 
+def test_fourstep_group_splits_follow_the_measured_table(plan_tool):
+    """group_split (plan.cpp): the per-size, per-layout splits chosen from the
+    measured per-launch rates."""
+    def ns(n, layout):
+        rc, out, err = plan_tool("passes", n, 0, layout)
+        assert rc == 0, err
+        return [int(ln.split()[0]).bit_length() - 1 for ln in out.splitlines()]
+    il, sp = 0, 1
+    assert ns(1 << 16, il) == [8, 8] and ns(1 << 17, sp) == [9, 8]
+    assert ns(1 << 18, il) == [10, 8] and ns(1 << 18, sp) == [10, 8]
+    assert ns(1 << 19, il) == [11, 8] and ns(1 << 19, sp) == [10, 9]
+    assert ns(1 << 20, il) == [12, 8] and ns(1 << 20, sp) == [10, 10]
+    assert ns(1 << 21, il) == [11, 10] and ns(1 << 21, sp) == [10, 11]
+    assert ns(1 << 23, il) == [11, 12] and ns(1 << 23, sp) == [12, 11]
+    assert ns(1 << 24, il) == [12, 12] and ns(1 << 24, sp) == [8, 8, 8]
+    assert ns(1 << 26, il) == [8, 8, 10] and ns(1 << 28, sp) == [8, 9, 11]
+    assert ns(1 << 29, il) == [8, 9, 12] and len(ns(1 << 29, sp)) == 4
+    assert ns(1 << 30, il) == [8, 11, 11] and len(ns(1 << 30, sp)) == 4
+
+
 def test_fourstep_groups_cover_large_sizes(plan_tool):
     """K3 groups: each a radix-NS Stockham stage with cols = prior product,
     k = N / s; inner groups need k >= tile, the last group has k == 1."""
