@@ -202,6 +202,12 @@ typedef int (*fftgen_exchange_fn)(void *ctx, const void *send, void *recv, size_
 /* The whole pipeline above on one rank with the caller's exchange. */
 fftgen_status fftgen_dist_execute(const fftgen_dist_plan *plan, int direction, const void *in, void *out,
                                   void *work0, void *work1, fftgen_exchange_fn exchange, void *ctx, void *stream);
+/* Cyclic (transposed) output order: exchange, butterfly,
+ * exchange, local plan only -- out[j] = X[rank + world*j] for j < n/world,
+ * two exchanges instead of three and no unpack.  `work1` is not used. */
+fftgen_status fftgen_dist_execute_cyclic(const fftgen_dist_plan *plan, int direction, const void *in, void *out,
+                                         void *work0, void *work1, fftgen_exchange_fn exchange, void *ctx,
+                                         void *stream);
 /* Peer-memory transport: every rank's blocks are mapped into this process
  * (CUDA IPC / symmetric memory over NVLink, or plain device buffers when the
  * ranks are emulated on one GPU) and the exchanges run inside the kernels:

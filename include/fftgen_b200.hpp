@@ -422,6 +422,19 @@ class DistributedPlan {
     };
     check(fftgen_dist_execute(plan_.get(), static_cast<int>(dir), in, out, work0, work1, tramp, &ctx, stream));
   }
+  // cyclic output order: out[j] = X[rank + world*j], two exchanges
+  template <class Exchange>
+  void execute_cyclic(Direction dir, const void *in, void *out, void *work0, Exchange &&exchange,
+                      void *stream = nullptr) const {
+    struct Ctx {
+      Exchange *f;
+    } ctx{&exchange};
+    auto tramp = [](void *c, const void *send, void *recv, size_t bytes, void *s) -> int {
+      return (*static_cast<Ctx *>(c)->f)(send, recv, bytes, s);
+    };
+    check(fftgen_dist_execute_cyclic(plan_.get(), static_cast<int>(dir), in, out, work0, nullptr, tramp, &ctx,
+                                     stream));
+  }
   // the stages one by one (the exchanges in between are the caller's)
   void butterfly(Direction dir, const void *recv, void *send, void *stream = nullptr) const {
     check(fftgen_dist_butterfly(plan_.get(), static_cast<int>(dir), recv, send, stream));

@@ -47,6 +47,7 @@ ABI_SYMBOLS = (
     "fftgen_dist_local", "fftgen_dist_unpack", "fftgen_dist_execute", "fftgen_dist_chunk_elems",
     "fftgen_dist_block_elems", "fftgen_dist_local_plan", "fftgen_seeded_input", "fftgen_program_text",
     "fftgen_plan_group_twiddles", "fftgen_dist_butterfly_peers", "fftgen_dist_unpack_peers",
+    "fftgen_dist_execute_cyclic",
 )
 
 
@@ -145,6 +146,7 @@ def _load() -> C.CDLL:
     L.fftgen_dist_local.argtypes = [vp, C.c_int, vp, vp, vp]
     L.fftgen_dist_unpack.argtypes = [vp, vp, vp, vp]
     L.fftgen_dist_execute.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp]
+    L.fftgen_dist_execute_cyclic.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, vp, vp]
     L.fftgen_dist_chunk_elems.argtypes = [vp]
     L.fftgen_dist_chunk_elems.restype = i64
     L.fftgen_dist_block_elems.argtypes = [vp]

@@ -236,6 +236,28 @@ fftgen_status fftgen_dist_execute(const fftgen_dist_plan *p, int direction, cons
   return fftgen_dist_unpack(p, w0, out, stream);
 }
 
+fftgen_status fftgen_dist_execute_cyclic(const fftgen_dist_plan *p, int direction, const void *in, void *out,
+                                         void *w0, void *w1, fftgen_exchange_fn exchange, void *ctx, void *stream) {
+  (void)w1;
+  if (!p) return dfail(FFTGEN_ERR_INVALID, "NULL plan");
+  if (!exchange) return dfail(FFTGEN_ERR_INVALID, "NULL exchange callback");
+  fftgen_status st;
+  if ((st = check_pair(p, in, w0)) != FFTGEN_OK || (st = check_pair(p, w0, out)) != FFTGEN_OK ||
+      (st = check_pair(p, in, out)) != FFTGEN_OK)
+    return st;
+  const size_t chunk = (size_t)p->l1 * 8;
+  auto xchg = [&](const void *s, void *r) -> fftgen_status {
+    const int rc = exchange(ctx, s, r, chunk, stream);
+    return rc == 0 ? FFTGEN_OK : dfail(FFTGEN_ERR_EXEC, "exchange callback failed with " + std::to_string(rc));
+  };
+  // the butterfly writes `out` (free until the local plan), which the second
+  // exchange moves back into w0 for the local plan
+  if ((st = xchg(in, w0)) != FFTGEN_OK) return st;
+  if ((st = fftgen_dist_butterfly(p, direction, w0, out, stream)) != FFTGEN_OK) return st;
+  if ((st = xchg(out, w0)) != FFTGEN_OK) return st;
+  return fftgen_dist_local(p, direction, w0, out, stream);
+}
+
 fftgen_status fftgen_seeded_input(int layout, int64_t n, int64_t batch, uint64_t seed0, void *out0, void *out1,
                                   int64_t dist, int device, void *stream) {
   const bool split = layout == FFTGEN_LAYOUT_SPLIT;
