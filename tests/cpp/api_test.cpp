@@ -182,6 +182,7 @@ extern "C" int cudaFree(void *);
 extern "C" int cudaMemcpy(void *, const void *, size_t, int);
 extern "C" int cudaMemcpyAsync(void *, const void *, size_t, int, void *);
 extern "C" int cudaDeviceSynchronize();
+extern "C" int cudaMemset(void *, int, size_t);
 
 static void dist_tests() {
   CHECK(throws<DimensionError>([] { DistributedPlan(1 << 12, 3, 0); }));
@@ -214,6 +215,17 @@ static void dist_tests() {
   for (int64_t j = 0; j < n; ++j) got[j] = {out[2 * j], out[2 * j + 1]}, w[j] = {want[2 * j], want[2 * j + 1]};
   CHECK(calls == 3);
   CHECK(rel_l2(got, w) < 3e-6);
+  // cyclic output order (world 1: the natural order) with two exchanges
+  calls = 0;
+  cudaMemset(y, 0, 8 * n);
+  dp.execute_cyclic(Direction::Forward, x, y, w0, [&](const void *s, void *r, size_t bytes, void *st) {
+    ++calls;
+    return cudaMemcpyAsync(r, s, bytes, 3, st);
+  });
+  cudaDeviceSynchronize();
+  std::vector<float> outc(2 * n);
+  cudaMemcpy(outc.data(), y, 8 * n, 2);
+  CHECK(calls == 2 && outc == out);
   // a failing exchange surfaces as ExecError
   CHECK(throws<ExecError>([&] { dp.execute(Direction::Forward, x, y, w0, w1, [](const void *, void *, size_t, void *) { return 7; }); }));
   CHECK(throws<ExecError>([&] { dp.butterfly(Direction::Forward, x, x); }));  // out of place only
